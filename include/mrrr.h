@@ -1,0 +1,162 @@
+/*
+ * mrrr.h -- C ABI of the B200-native fp64 MRRR symmetric tridiagonal
+ * eigensolver (the hot path of arxiv 1205.2107, "PMRRR").
+ *
+ * Operation ("STEP"): for the real
+ * symmetric tridiagonal T = tridiag(e, d, e) compute all, an index range
+ * il..iu, or a value range (vl, vu] of its eigenpairs T z_j = lambda_j z_j by
+ * the MRRR algorithm: root representation
+ * L0 D0 L0^T = T - sigma0 I, bisection, classification by relative gap
+ * (tol 1e-3, L1069-1075), a representation tree of shifted child
+ * representations for clusters (L1092-1111) and, for every singleton, a
+ * Rayleigh-quotient-corrected twisted factorization giving z_j (L1013-1043).
+ *
+ * Accuracy contract (BASELINE.json, PAPER.md Eq. (Tresnorm), (Torthogo)):
+ * |lambda_j - lambda_j(T)| <= 4 n eps ||T||_1,
+ * ||T z_j - lambda_j z_j||_2 <= 10 n eps ||T||_1, |Z^T Z - I| <= 10 n eps.
+ *
+ * Every pointer argument of mrrr_stemr is DEVICE memory (cudaMalloc'd or
+ * managed) unless stated otherwise; all work is enqueued on `stream` and the
+ * call synchronises `stream` before returning, so *m and the return code are
+ * valid on return.  The library allocates its own workspace stream-ordered
+ * (cudaMallocAsync) and frees it before returning.  The caller owns d, e, w,
+ * Z; d and e are NOT modified.  Re-entrant on distinct streams.  Results are
+ * bitwise deterministic for identical inputs, options and device type.
+ *
+ * Return codes (LAPACK INFO style): 0 ok; -i: argument i invalid (numbering
+ * below); 1 root RRR not found; 2 child RRR not acceptable; 3 tree depth cap
+ * exceeded; 4 bisection/RQC non-convergence; 5 CUDA error; 6 out of device
+ * memory; 7 collective (multi-GPU) error.  On error, outputs are unspecified.
+ */
+#ifndef MRRR_H
+#define MRRR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MRRR_RANGE_ALL = 0,   /* all n eigenpairs */
+  MRRR_RANGE_INDEX = 1, /* il..iu, 1-based inclusive, ascending order */
+  MRRR_RANGE_VALUE = 2  /* eigenvalues in (vl, vu] (Sturm-count semantics) */
+} mrrr_range_t;
+
+enum {
+  MRRR_OK = 0,
+  MRRR_ERR_ROOT = 1,
+  MRRR_ERR_CHILD = 2,
+  MRRR_ERR_DEPTH = 3,
+  MRRR_ERR_CONVERGE = 4,
+  MRRR_ERR_CUDA = 5,
+  MRRR_ERR_NOMEM = 6,
+  MRRR_ERR_COMM = 7
+};
+
+/* Options; pass NULL for the defaults from mrrr_default_opts(). */
+typedef struct {
+  double tol_relgap;   /* singleton threshold on the relative gap; 1e-3
+                          (PAPER.md L1069-1072 footnote) */
+  double rtol_class;   /* relative bracket width before classification and RQC;
+                          2^-20 (reading 4) */
+  int max_depth;       /* representation-tree depth cap (error 3 beyond); 128 */
+  int perturb_root;    /* 1: seeded (1 + 4 eps u) relative perturbation of the
+                          root D, L (reading 3); 0: off */
+  uint64_t seed;       /* perturbation seed; default 0x1205210700000000 */
+  int multisection;    /* shifts evaluated per eigenvalue per bisection round
+                          (1 = plain bisection); default 4 */
+  int grid_factor;     /* root grid points per wanted eigenvalue; default 4;
+                          0 disables the grid stage */
+} mrrr_opts_t;
+
+void mrrr_default_opts(mrrr_opts_t *opts);
+
+/*
+ * mrrr_stemr -- eigenpairs of T on one GPU.
+ *  (1) n       order of T, n >= 1.
+ *  (2) d       device, d[n], diagonal; finite.
+ *  (3) e       device, e[n-1], off-diagonal; finite (may be NULL if n == 1).
+ *  (4) range   MRRR_RANGE_*.
+ *  (5) vl      VALUE: lower bound (exclusive).
+ *  (6) vu      VALUE: upper bound (inclusive), vl < vu.
+ *  (7) il      INDEX: first index, 1 <= il <= n.
+ *  (8) iu      INDEX: last index, il <= iu <= n.
+ *  (9) m       HOST out: number of eigenpairs returned.
+ * (10) w       device out: w[m] ascending eigenvalues.  Capacity n for ALL and
+ *              VALUE, iu-il+1 for INDEX.
+ * (11) Z       device out: column-major ldz x m; column j is the unit
+ *              eigenvector of w[j] (zero outside its irreducible block).  NULL
+ *              => eigenvalues only.  Same capacity as w in columns.
+ * (12) ldz     leading dimension of Z, ldz >= n when Z != NULL.
+ * (13) stream  cudaStream_t (as void*), NULL = legacy default stream.
+ * (14) opts    NULL or options.
+ */
+int mrrr_stemr(int64_t n, const double *d, const double *e, int range,
+               double vl, double vu, int64_t il, int64_t iu, int64_t *m,
+               double *w, double *Z, int64_t ldz, void *stream,
+               const mrrr_opts_t *opts);
+
+/*
+ * mrrr_stemr_dist -- the same solve sharded over P ranks (one GPU each) by
+ * eigen-index range.  Every rank passes the same T,
+ * range and opts.  Rank r owns global columns [col_begin, col_begin+m_local);
+ * intervals and w are exchanged with `allgather`, a caller-provided
+ * all-gather over the ranks (NCCL over NVLink in the Python binding):
+ *   allgather(ctx, send, recv, bytes, stream): recv[r*bytes .. ] <- rank r's
+ *   send (bytes each), device buffers, enqueued on `stream`; returns 0 on
+ *   success.
+ * Arguments 1-8 and 14 as in mrrr_stemr; further:
+ *  (9)  rank, (10) nranks (1 <= nranks, 0 <= rank < nranks),
+ *  (11) allgather, (12) allgather_ctx,
+ *  (13) m (HOST out, global count), (15) col_begin, (16) m_local (HOST out),
+ *  (17) w_all (device out, all m eigenvalues on every rank),
+ *  (18) Z_local (device out, ldz x m_local; NULL = values only), (19) ldz,
+ *  (20) stream.
+ */
+typedef int (*mrrr_allgather_fn)(void *ctx, const void *send, void *recv,
+                                 size_t bytes, void *stream);
+int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range,
+                    double vl, double vu, int64_t il, int64_t iu, int rank,
+                    int nranks, mrrr_allgather_fn allgather,
+                    void *allgather_ctx, int64_t *m, const mrrr_opts_t *opts,
+                    int64_t *col_begin, int64_t *m_local, double *w_all,
+                    double *Z_local, int64_t ldz, void *stream);
+
+/* Upper bound of the device workspace mrrr_stemr allocates internally for an
+ * order-n problem with k wanted eigenpairs (bytes), excluding the
+ * representation-tree node pool, which grows with the number of clusters
+ * (<= 24 n bytes per cluster node). */
+size_t mrrr_workspace_bytes(int64_t n, int64_t k);
+
+/* Static description of a return code. */
+const char *mrrr_strerror(int code);
+
+/* Instrumentation of the last call on this host thread (DESIGN.md
+ * "Instrumentation"): counts and per-phase device times. */
+typedef struct {
+  int64_t nodes;            /* cluster nodes (child RRRs) created */
+  int64_t levels;           /* tree levels processed */
+  int64_t singletons;       /* eigenvectors computed */
+  int64_t root_sweeps;      /* Sturm sweeps in root grid + bisection */
+  int64_t refine_sweeps;    /* Sturm sweeps in child refinement */
+  int64_t child_sweeps;     /* stationary transforms (candidates + accepted) */
+  int64_t rqc_iters;        /* twisted factorizations in the vector phase */
+  int64_t rqc_fallbacks;    /* vectors that needed the bisection fallback */
+  int64_t safe_resweeps;    /* projective sweeps redone by the qd safe path */
+  int64_t kernel_launches;  /* kernels launched by this call */
+  double ms_root;           /* device time: prep + root RRR + root bisection */
+  double ms_tree;           /* device time: classification, children, refine */
+  double ms_vectors;        /* device time: singleton vectors + output */
+  double ms_total;          /* device time of the whole call */
+} mrrr_stats_t;
+int mrrr_get_stats(mrrr_stats_t *out);
+
+/* Library version string. */
+const char *mrrr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRRR_H */

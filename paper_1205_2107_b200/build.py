@@ -1,0 +1,36 @@
+"""Build the CUDA library in-tree: libmrrr_b200.so for sm_100a (nvcc)."""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SO = os.path.join(HERE, "libmrrr_b200.so")
+SRC = os.path.join(HERE, "csrc", "mrrr.cu")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
+              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+
+
+def _deps():
+    return glob.glob(os.path.join(HERE, "csrc", "*")) + [os.path.join(ROOT, "include", "mrrr.h")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(p) for p in _deps()):
+        return SO
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-o", SO, SRC]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + out.stderr[-4000:])
+    with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
+        f.write(out.stderr)
+    if verbose:
+        print(out.stderr)
+    return SO
+
+
+if __name__ == "__main__":
+    print(build(force=True))

@@ -1,0 +1,578 @@
+// kernels_tree.cuh -- prep, root representation, bisection/multisection,
+// classification, child representations (SURVEY §8(a)
+// rows a1-a5).  Included by mrrr.cu (single translation unit).
+#pragma once
+#include <cuda_pipeline.h>
+
+#include "common.cuh"
+
+namespace mrrr {
+
+// ===========================================================================
+// a1 -- norms, Gershgorin bounds, power-of-two scaling, split
+// One CTA of 1024 threads.  hdr: [0] tnrm (unscaled), [1] scale (2^k),
+// [2] gl (scaled), [3] gu (scaled); split flags written as int per row.
+// ===========================================================================
+__global__ void k_prep(const double *__restrict__ d, const double *__restrict__ e, int64_t n,
+                       double *__restrict__ ds, double *__restrict__ es, double *__restrict__ es2,
+                       int *__restrict__ brk, double *__restrict__ hdr) {
+  __shared__ double red[3][32];
+  double tn = 0, lo = CUDART_INF, hi = -CUDART_INF;
+  int badd = 0, bade = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double r = 0;
+    if (i > 0) r += fabs(e[i - 1]);
+    if (i < n - 1) { r += fabs(e[i]); bade |= !isfinite(e[i]); }
+    double di = d[i];
+    badd |= !isfinite(di);
+    tn = fmax(tn, r + fabs(di));
+    lo = fmin(lo, di - r);
+    hi = fmax(hi, di + r);
+  }
+  for (int o = 16; o; o >>= 1) {
+    tn = fmax(tn, __shfl_xor_sync(0xffffffff, tn, o));
+    lo = fmin(lo, __shfl_xor_sync(0xffffffff, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffff, hi, o));
+  }
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { red[0][w] = tn; red[1][w] = lo; red[2][w] = hi; }
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    tn = l < nw ? red[0][l] : 0.0;
+    lo = l < nw ? red[1][l] : CUDART_INF;
+    hi = l < nw ? red[2][l] : -CUDART_INF;
+    for (int o = 16; o; o >>= 1) {
+      tn = fmax(tn, __shfl_xor_sync(0xffffffff, tn, o));
+      lo = fmin(lo, __shfl_xor_sync(0xffffffff, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffff, hi, o));
+    }
+    if (l == 0) { red[0][0] = tn; red[1][0] = lo; red[2][0] = hi; }
+  }
+  badd = __syncthreads_or(badd);
+  bade = __syncthreads_or(bade);
+  tn = red[0][0];
+  // exact power-of-two scale so that ||T||_1 in [1, 2)
+  int ex = 0;
+  double sc = 1.0;
+  if (tn > 0) { frexp(tn, &ex); sc = ldexp(1.0, 1 - ex); }
+  double thr = kEps * tn;  // split threshold on the unscaled data (reading 1)
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    ds[i] = d[i] * sc;
+    if (i < n - 1) {
+      double ei = e[i];
+      bool sp = fabs(ei) <= thr;
+      double es_i = sp ? 0.0 : ei * sc;
+      es[i] = es_i;
+      es2[i] = es_i * es_i;
+      brk[i] = sp;
+    }
+  }
+  if (threadIdx.x == 0) {
+    hdr[0] = tn; hdr[1] = sc; hdr[2] = red[1][0] * sc; hdr[3] = red[2][0] * sc;
+    hdr[4] = badd ? 1.0 : (bade ? 2.0 : 0.0);
+  }
+}
+
+// ===========================================================================
+// Sturm count on the (scaled, split) T itself: projective three-term form
+// t_i = (d_i - x) t_{i-1} - e_{i-1}^2 t_{i-2}; counts sign changes.  Used for
+// VALUE / multi-block INDEX range selection.  One thread per (x, block).
+// ===========================================================================
+__device__ inline unsigned sturm_T_count(const double *ds, const double *es2, int64_t r0, int nb,
+                                         double x) {
+  double tm1 = 1.0, tm2 = 0.0;
+  unsigned c = 0;
+  bool ok = true;
+  for (int i = 0; i < nb; ++i) {
+    double b2 = i > 0 ? es2[r0 + i - 1] : 0.0;
+    double t = fma(ds[r0 + i] - x, tm1, -b2 * tm2);
+    c += negbit(t, tm1);
+    tm2 = tm1; tm1 = t;
+    if ((i & 7) == 7) {
+      int ee = max_exp(tm1, tm2);
+      double f = pow2_scale(min(ee, 2045));
+      ok &= ee < 2047;
+      tm1 *= f; tm2 *= f;
+    }
+  }
+  if (!ok || !isfinite(tm1)) {
+    // safe classic count with a tiny-pivot substitution
+    double q = 1.0;
+    c = 0;
+    for (int i = 0; i < nb; ++i) {
+      double b2 = i > 0 ? es2[r0 + i - 1] : 0.0;
+      q = (ds[r0 + i] - x) - (i > 0 ? b2 / q : 0.0);
+      if (fabs(q) < kTiny) q = -kTiny;
+      c += q < 0;
+    }
+  }
+  return c;
+}
+
+__global__ void k_sturm_T(const double *ds, const double *es2, const Block *blocks, int nblocks,
+                          const double *xs, int nx, int *out /* [nx][nblocks] */) {
+  int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nx * nblocks) return;
+  int xi = id / nblocks, b = id % nblocks;
+  out[id] = (int)sturm_T_count(ds, es2, blocks[b].row0, blocks[b].nb, xs[xi]);
+}
+
+// ===========================================================================
+// a2 -- root representation L0 D0 L0^T = T - sigma0 I.
+// Pass 1 (one thread per block, sequential): projective leading minors
+//   t_i = (d_i - sigma) t_{i-1} - e_{i-1}^2 t_{i-2}
+// (fma chain only), definiteness check, retries with doubled offset.
+// Stores t_i and the power-of-two rescale applied after row i.
+// Pass 2 (parallel over rows): D_i = t_i / t_{i-1}, L_i = e_i / D_i, seeded
+// (1 + 4 eps u) perturbation (reading 3), LD_i, LLD_i.
+// ===========================================================================
+__global__ void k_root_chain(const double *__restrict__ ds, const double *__restrict__ es2,
+                             Block *blocks, int nblocks, double tnrm_scaled, double *tbuf,
+                             int *sbuf, double *sigma_out, int *fail) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nblocks) return;
+  Block B = blocks[b];
+  if (B.nb < 2 || B.slot1 <= B.slot0) { sigma_out[b] = 0.0; return; }
+  double delta = 4.0 * kEps * tnrm_scaled;
+  for (int attempt = 0; attempt <= 6; ++attempt) {
+    double sigma = B.side > 0 ? B.gl - delta : B.gu + delta;
+    double tm1 = 1.0, tm2 = 0.0;
+    bool ok = true;
+    for (int i = 0; i < B.nb; ++i) {
+      int64_t gi = B.row0 + i;
+      double b2 = i > 0 ? es2[gi - 1] : 0.0;
+      double t = fma(ds[gi] - sigma, tm1, -b2 * tm2);
+      // definite: D_i = t_i / t_{i-1} has the sign of the side
+      bool good = (t != 0.0) && ((B.side > 0) ? (negbit(t, tm1) == 0) : (negbit(t, tm1) == 1));
+      ok &= good && isfinite(t);
+      tbuf[gi] = t;
+      int sh = 0;
+      tm2 = tm1; tm1 = t;
+      if ((i & 7) == 7) {
+        int ee = max_exp(tm1, tm2);
+        ok &= ee < 2047 && ee > 0;
+        sh = 1023 - min(max(ee, 1), 2045);
+        double f = pow2(sh);
+        tm1 *= f; tm2 *= f;
+      }
+      sbuf[gi] = sh;
+    }
+    if (ok) { sigma_out[b] = sigma; return; }
+    delta *= 2.0;
+  }
+  fail[0] = 1;
+  sigma_out[b] = 0.0;
+}
+
+__global__ void k_root_finish(const double *__restrict__ ds, const double *__restrict__ es,
+                              const Block *blocks, const int *__restrict__ row_block, int64_t n,
+                              const double *__restrict__ tbuf, const int *__restrict__ sbuf,
+                              const double *__restrict__ sigma_b, int perturb, uint64_t seed,
+                              double2 *__restrict__ DL, double2 *__restrict__ LDv) {
+  int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= n) return;
+  int b = row_block[gi];
+  Block B = blocks[b];
+  if (B.nb < 2 || B.slot1 <= B.slot0) {
+    DL[gi] = make_double2(ds[gi], 0.0);
+    LDv[gi] = make_double2(0.0, 0.0);
+    return;
+  }
+  int i = (int)(gi - B.row0);
+  // D_i = t_i / t_{i-1}, with t_{i-1} brought to t_i's scale
+  double ti = tbuf[gi];
+  double tp = (i > 0) ? tbuf[gi - 1] * pow2(sbuf[gi - 1]) : 1.0;
+  double D = ti / tp;
+  double Lc = 0.0;
+  if (i < B.nb - 1) {
+    // L_i = e_i / D_i needs D_i (this row); computed here for row i
+    Lc = es[gi] / D;
+  }
+  if (perturb) {
+    D = __dmul_rn(D, __dadd_rn(1.0, __dmul_rn(4.0 * kEps, perturb_u(seed, gi, 0))));
+    if (i < B.nb - 1) Lc = __dmul_rn(Lc, __dadd_rn(1.0, __dmul_rn(4.0 * kEps, perturb_u(seed, gi, 1))));
+  }
+  double LD = Lc * D, LLD = Lc * LD;
+  DL[gi] = make_double2(D, LLD);
+  LDv[gi] = make_double2(LD, LD * LD);
+}
+
+// ===========================================================================
+// Smem-tiled Sturm sweep of one node by a whole CTA.  Every thread evaluates
+// M shifts (independent chains, ILP).  Rows of (D, LLD) are staged through a
+// double-buffered shared-memory tile with cp.async and read as warp
+// broadcasts.  All threads of the CTA must call it.
+// ===========================================================================
+constexpr int kTile = 256;  // rows per smem tile (4 KB)
+
+template <int M>
+__device__ __forceinline__ void tile_steps(const double2 *__restrict__ t, int rows,
+                                           const double (&mu)[M], Sturm (&s)[M], bool &ok) {
+  int r = 0;
+  for (; r + 8 <= rows; r += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double2 v = t[r + k];
+#pragma unroll
+      for (int c = 0; c < M; ++c) sturm_step(s[c], v.x, v.y, mu[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < M; ++c) ok &= sturm_rescale(s[c]);
+  }
+  for (; r < rows; ++r) {
+    double2 v = t[r];
+#pragma unroll
+    for (int c = 0; c < M; ++c) sturm_step(s[c], v.x, v.y, mu[c]);
+  }
+}
+
+template <int M>
+__device__ void cta_sweep(const double2 *__restrict__ DL, int nb, double2 *sm, const double (&mu)[M],
+                          unsigned (&cnt)[M], bool &ok) {
+  Sturm s[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) sturm_init(s[c], mu[c]);
+  ok = true;
+  const int body = nb - 1;  // rows 0..nb-2 carry LLD; row nb-1 is the last pivot
+  const int ntiles = (body + kTile - 1) / kTile;
+  auto load = [&](int tile, int buf) {
+    int base = tile * kTile;
+    int rows = min(kTile, body - base);
+    for (int r = threadIdx.x; r < rows; r += blockDim.x)
+      __pipeline_memcpy_async(&sm[buf * kTile + r], &DL[base + r], sizeof(double2));
+    __pipeline_commit();
+  };
+  if (ntiles > 0) load(0, 0);
+  for (int tile = 0; tile < ntiles; ++tile) {
+    int buf = tile & 1;
+    if (tile + 1 < ntiles) {
+      load(tile + 1, buf ^ 1);
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
+    }
+    __syncthreads();
+    int rows = min(kTile, body - tile * kTile);
+    tile_steps<M>(sm + buf * kTile, rows, mu, s, ok);
+    __syncthreads();
+  }
+  double Dl = __ldg(&DL[nb - 1]).x;
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    sturm_last(s[c], Dl);
+    ok &= sturm_ok(s[c]);
+    cnt[c] = s[c].c;
+  }
+}
+
+// ===========================================================================
+// Work item of the bisection kernels: a chunk of slots of one node.
+struct Work {
+  int32_t node;
+  int32_t s0, s1;  // slot range
+  int32_t pad;
+};
+
+// a3 -- root grid: counts of the root representation at G uniformly spaced
+// points x_g = lo0 + (hi0 - lo0) g / G, g = 1..G-1 (one CTA handles
+// blockDim.x * M consecutive points).  cnt[g] for g in [1, G-1].
+template <int M>
+__global__ void __launch_bounds__(128) k_grid(const Node *nodes, int node, double lo0, double hi0,
+                                              int G, int *cnt, unsigned long long *safe_ctr) {
+  __shared__ double2 sm[2 * kTile];
+  const Node N = nodes[node];
+  double mu[M];
+  int g0 = (blockIdx.x * blockDim.x + threadIdx.x) * M + 1;
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    int g = min(g0 + c, G - 1);
+    mu[c] = lo0 + (hi0 - lo0) * ((double)g / (double)G);
+  }
+  unsigned k[M];
+  bool ok;
+  cta_sweep<M>(N.DL, N.nb, sm, mu, k, ok);
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    int g = g0 + c;
+    if (g < G) {
+      unsigned v = k[c];
+      if (!ok) { atomicAdd(safe_ctr, 1ull); v = negcount_qd_safe(N.DL, N.nb, mu[c]); }
+      cnt[g] = (int)v;
+    }
+  }
+}
+
+// ===========================================================================
+// a3/a5 -- multisection refinement of slot intervals in node coordinates
+// until hi - lo <= rtol * max(|lo|, |hi|) or lo, hi have no double between
+// them (O7).  Invariant N(lo) < j <= N(hi).  Each thread owns one slot and
+// evaluates M shifts per round; the CTA sweeps the node once per round.
+// ===========================================================================
+template <int M>
+__global__ void __launch_bounds__(128) k_bisect(const Node *nodes, const Work *work,
+                                                const int *__restrict__ slot_j, double *lo_arr,
+                                                double *hi_arr, double rtol, int max_rounds,
+                                                unsigned long long *sweeps,
+                                                unsigned long long *safe_ctr) {
+  __shared__ double2 sm[2 * kTile];
+  const Work W = work[blockIdx.x];
+  const Node N = nodes[W.node];
+  int s = W.s0 + threadIdx.x;
+  bool mine = s < W.s1;
+  double lo = mine ? lo_arr[s] : 0.0, hi = mine ? hi_arr[s] : 1.0;
+  int j = mine ? slot_j[s] : 0;  // block-local 1-based eigen index
+  auto conv = [&](double a, double b) {
+    double m = 0.5 * (a + b);
+    return (b - a <= rtol * fmax(fabs(a), fabs(b))) || !(m > a && m < b);
+  };
+  bool done = !mine || conv(lo, hi);
+  int rounds = 0;
+  while (__syncthreads_or(!done) && rounds < max_rounds) {
+    double mu[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) mu[c] = lo + (hi - lo) * ((double)(c + 1) / (double)(M + 1));
+    unsigned k[M];
+    bool ok;
+    cta_sweep<M>(N.DL, N.nb, sm, mu, k, ok);
+    if (!done) {
+      if (!ok) {
+        atomicAdd(safe_ctr, 1ull);
+#pragma unroll
+        for (int c = 0; c < M; ++c) k[c] = negcount_qd_safe(N.DL, N.nb, mu[c]);
+      }
+      double nlo = lo, nhi = hi;
+#pragma unroll
+      for (int c = 0; c < M; ++c)
+        if ((int)k[c] < j && mu[c] > nlo) nlo = mu[c];
+#pragma unroll
+      for (int c = M - 1; c >= 0; --c)
+        if ((int)k[c] >= j && mu[c] > nlo && mu[c] < nhi) nhi = mu[c];
+      lo = nlo; hi = nhi;
+      done = conv(lo, hi);
+    }
+    ++rounds;
+  }
+  if (threadIdx.x == 0) atomicAdd(sweeps, (unsigned long long)rounds * M * (W.s1 - W.s0));
+  if (mine) { lo_arr[s] = lo; hi_arr[s] = hi; }
+}
+
+// a5 -- bracket verification in child coordinates (O9.4): counts at lo and
+// hi; an end that does not bracket index j is widened by doubling its offset
+// from the parent interval until it does.
+__global__ void __launch_bounds__(128) k_verify(const Node *nodes, const Work *work,
+                                                const int *__restrict__ slot_j, double *lo_arr,
+                                                double *hi_arr, const double *wlo_arr,
+                                                const double *whi_arr, int *fail,
+                                                unsigned long long *sweeps,
+                                                unsigned long long *safe_ctr) {
+  __shared__ double2 sm[2 * kTile];
+  const Work W = work[blockIdx.x];
+  const Node N = nodes[W.node];
+  int s = W.s0 + threadIdx.x;
+  bool mine = s < W.s1;
+  double lo = 0.0, hi = 1.0, wl = 0.0, wu = 0.0, plo = 0.0, phi = 0.0;
+  int j = 0;
+  if (mine) {
+    plo = lo_arr[s]; phi = hi_arr[s];  // parent-coordinate bracket minus sigma, unwidened
+    wl = wlo_arr[s]; wu = whi_arr[s];
+    lo = plo - wl; hi = phi + wu;
+    j = slot_j[s];
+  }
+  bool done = !mine;
+  int rounds = 0;
+  while (__syncthreads_or(!done) && rounds < 200) {
+    double mu[2] = {lo, hi};
+    unsigned k[2];
+    bool ok;
+    cta_sweep<2>(N.DL, N.nb, sm, mu, k, ok);
+    if (!done) {
+      if (!ok) {
+        atomicAdd(safe_ctr, 1ull);
+        k[0] = negcount_qd_safe(N.DL, N.nb, lo);
+        k[1] = negcount_qd_safe(N.DL, N.nb, hi);
+      }
+      bool okl = (int)k[0] <= j - 1, oku = (int)k[1] >= j;
+      if (!okl) { wl *= 2.0; lo = plo - wl; }
+      if (!oku) { wu *= 2.0; hi = phi + wu; }
+      done = okl && oku;
+    }
+    ++rounds;
+  }
+  if (threadIdx.x == 0) atomicAdd(sweeps, (unsigned long long)rounds * 2 * (W.s1 - W.s0));
+  if (mine) {
+    if (!done) fail[0] = 1;
+    lo_arr[s] = lo; hi_arr[s] = hi;
+  }
+}
+
+// ===========================================================================
+// a4 -- classification by relative gap (O8).  For consecutive
+// slots s, s+1 of the same node: boundary iff
+//   lo_{s+1} - hi_s > tol * max(|mid_s|, |mid_{s+1}|);
+// the last slot of a node always ends a run.  flag[s] = 1 iff a run ends at s.
+// ===========================================================================
+__global__ void k_classify(const int *__restrict__ slot_node, const double *__restrict__ lo,
+                           const double *__restrict__ hi, const int *__restrict__ active,
+                           int nslots, double tol, int *__restrict__ run_end) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslots) return;
+  if (!active[s]) { run_end[s] = 1; return; }
+  int f = 1;
+  if (s + 1 < nslots && active[s + 1] && slot_node[s + 1] == slot_node[s]) {
+    double g = lo[s + 1] - hi[s];
+    double m0 = 0.5 * (lo[s] + hi[s]), m1 = 0.5 * (lo[s + 1] + hi[s + 1]);
+    f = g > tol * fmax(fabs(m0), fabs(m1));
+  }
+  run_end[s] = f;
+}
+
+// ===========================================================================
+// a5 -- child representation by the stationary transform
+// L+ D+ L+^T = L D L^T - sigma I, projective form:
+//   t_i = D_i q + p (= D+_i q), p' = LLD_i p - sigma t, q' = t.
+// The child keeps the block's off-diagonals LD_i (= L+_i D+_i exactly in
+// exact arithmetic) and stores (D+_i, LLD+_i = LD_i^2 / D+_i).
+// k_cand: growth of candidate shifts (raw max |D+| and, when z is given, the
+// eigenvector-weighted growth sum |D+_i| z_i^2 / sum z_i^2).
+// ===========================================================================
+struct Cand {
+  double sigma;
+  double raw;  // max |D+_i| (inf if not finite)
+  double wgt;  // sum |D+_i| z_i^2 / ||z||^2 (inf if not finite / not computed)
+  int32_t cluster;
+  int32_t which;  // 0..5 = (mult index) * 2 + (0 left, 1 right)
+};
+
+__global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0, const int *cl_s1,
+                       const double *__restrict__ lo, const double *__restrict__ hi, int ncl,
+                       const double *__restrict__ zbuf, int64_t zstride, Cand *cand) {
+  int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= ncl * 6) return;
+  int c = id / 6, which = id % 6;
+  const Node P = nodes[cl_parent[c]];
+  int s0 = cl_s0[c], s1 = cl_s1[c] - 1;
+  double mult = (double)(1 << (which >> 1));
+  double sigma;
+  if ((which & 1) == 0) {
+    double dl = fmax(2.0 * (hi[s0] - lo[s0]), 4.0 * kEps * fabs(lo[s0]));
+    sigma = lo[s0] - mult * dl;
+  } else {
+    double dr = fmax(2.0 * (hi[s1] - lo[s1]), 4.0 * kEps * fabs(hi[s1]));
+    sigma = hi[s1] + mult * dr;
+  }
+  const double2 *DL = P.DL;
+  const double *z = zbuf ? zbuf + (int64_t)(2 * c + (which & 1)) * zstride : nullptr;
+  double p = -sigma, q = 1.0, g = 0.0, num = 0.0, den = 0.0;
+  bool fin = true;
+  int nb = P.nb;
+  for (int i = 0; i < nb; ++i) {
+    double2 v = __ldg(&DL[i]);
+    double t = fma(v.x, q, p);
+    double dp = t / q;  // D+_i (off the recurrence chain)
+    fin &= isfinite(dp) && dp != 0.0;
+    g = fmax(g, fabs(dp));
+    if (z) { double zi = z[i]; num = fma(fabs(dp), zi * zi, num); den = fma(zi, zi, den); }
+    if (i < nb - 1) { p = fma(-sigma, t, v.y * p); q = t; }
+    if ((i & 7) == 7) {
+      int ee = max_exp(p, q);
+      fin &= ee < 2047;
+      double f = pow2_scale(min(ee, 2045));
+      p *= f; q *= f;
+    }
+  }
+  Cand C;
+  C.sigma = sigma;
+  C.raw = fin ? g : CUDART_INF;
+  C.wgt = (fin && z && den > 0) ? num / den : CUDART_INF;
+  C.cluster = c;
+  C.which = which;
+  cand[id] = C;
+}
+
+// Tiered acceptance (O9.3, reading 9): per offset multiple m = 1, 2, 4:
+// (i) lower raw growth <= 8 spdiam; (ii) lower weighted growth <= 64 spdiam;
+// (iv) afterwards the least raw growth <= 1e8 spdiam; else error 2.
+__global__ void k_pick(const Node *nodes, const int *cl_parent, const Cand *cand, int ncl,
+                       double *sigma_out, int *tier_out, int *fail) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  double spd = nodes[cl_parent[c]].spdiam;
+  const Cand *C = cand + 6 * c;
+  double best_raw = CUDART_INF, best_sigma = 0.0;
+  for (int m = 0; m < 3; ++m) {
+    const Cand &L = C[2 * m], &R = C[2 * m + 1];
+    if (L.raw < best_raw) { best_raw = L.raw; best_sigma = L.sigma; }
+    if (R.raw < best_raw) { best_raw = R.raw; best_sigma = R.sigma; }
+    if (isfinite(L.raw) || isfinite(R.raw)) {
+      bool useL = L.raw <= R.raw;
+      if ((useL ? L.raw : R.raw) <= 8.0 * spd) {
+        sigma_out[c] = useL ? L.sigma : R.sigma; tier_out[c] = 0; return;
+      }
+      bool wuseL = L.wgt <= R.wgt;
+      if ((wuseL ? L.wgt : R.wgt) <= 64.0 * spd) {
+        sigma_out[c] = wuseL ? L.sigma : R.sigma; tier_out[c] = 1; return;
+      }
+    }
+  }
+  if (best_raw <= 1e8 * spd) { sigma_out[c] = best_sigma; tier_out[c] = 3; return; }
+  sigma_out[c] = 0.0;
+  tier_out[c] = 4;
+  fail[0] = 1;
+}
+
+// Accepted child, pass 1 (one thread per cluster): projective chain, storing
+// t_i and the rescale exponent applied after row i (like the root).
+__global__ void k_child_chain(const Node *nodes, const int *cl_parent, const double *sigma, int ncl,
+                              int64_t stride, double *tbuf, int *sbuf) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  const Node P = nodes[cl_parent[c]];
+  double sg = sigma[c];
+  double p = -sg, q = 1.0;
+  double *tb = tbuf + (int64_t)c * stride;
+  int *sb = sbuf + (int64_t)c * stride;
+  int nb = P.nb;
+  for (int i = 0; i < nb; ++i) {
+    double2 v = __ldg(&P.DL[i]);
+    double t = fma(v.x, q, p);
+    tb[i] = t;
+    int sh = 0;
+    if (i < nb - 1) {
+      p = fma(-sg, t, v.y * p);
+      q = t;
+      if ((i & 7) == 7) {
+        int ee = max_exp(p, q);
+        sh = 1023 - min(max(ee, 1), 2045);
+        double f = pow2(sh);
+        p *= f; q *= f;
+      }
+    }
+    sb[i] = sh;
+  }
+}
+
+// Accepted child, pass 2 (parallel over clusters x rows): D+_i = t_i / t_{i-1}
+// (t_{i-1} brought to t_i's scale), LLD+_i = LD_i^2 / D+_i.
+__global__ void k_child_finish(const Node *nodes, const int *cl_parent, const int *cl_node, int ncl,
+                               int64_t stride, const double *tbuf, const int *sbuf,
+                               const double2 *__restrict__ LDv, double2 *out_base, int *fail) {
+  int c = blockIdx.y;
+  if (c >= ncl) return;
+  const Node P = nodes[cl_parent[c]];
+  int nb = P.nb;
+  const double *tb = tbuf + (int64_t)c * stride;
+  const int *sb = sbuf + (int64_t)c * stride;
+  double2 *out = out_base + (int64_t)c * stride;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    double tp = (i > 0) ? tb[i - 1] * pow2(sb[i - 1]) : 1.0;
+    double Dp = tb[i] / tp;
+    double ld2 = (i < nb - 1) ? LDv[P.row0 + i].y : 0.0;
+    double lld = (i < nb - 1) ? ld2 / Dp : 0.0;
+    if (!isfinite(Dp) || Dp == 0.0 || !isfinite(lld)) fail[0] = 1;
+    out[i] = make_double2(Dp, lld);
+  }
+  (void)cl_node;
+}
+
+}  // namespace mrrr

@@ -1,0 +1,936 @@
+// mrrr.cu -- host orchestrator and C ABI (include/mrrr.h) of the B200-native
+// MRRR tridiagonal eigensolver.  The orchestrator plans launches (blocks,
+// slots, tree levels, work chunks) from small read-backs; every arithmetic
+// step of the method runs in the kernels of kernels_tree.cuh / kernels_vec.cuh.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "../../include/mrrr.h"
+#include "kernels_tree.cuh"
+#include "kernels_vec.cuh"
+
+using namespace mrrr;
+
+namespace {
+
+thread_local mrrr_stats_t g_stats;
+
+struct CudaError {
+  cudaError_t e;
+};
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t e_ = (x);                       \
+    if (e_ != cudaSuccess) throw CudaError{e_}; \
+  } while (0)
+struct MrrrError {
+  int code;
+};
+
+// Stream-ordered device allocations released at scope exit.
+struct DevArena {
+  cudaStream_t s;
+  std::vector<void *> ptrs;
+  explicit DevArena(cudaStream_t st) : s(st) {}
+  template <class T>
+  T *alloc(size_t count) {
+    void *p = nullptr;
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); throw MrrrError{MRRR_ERR_NOMEM}; }
+    CK(e);
+    ptrs.push_back(p);
+    return (T *)p;
+  }
+  ~DevArena() {
+    for (void *p : ptrs) cudaFreeAsync(p, s);
+  }
+};
+
+template <class T>
+void h2d(T *dst, const T *src, size_t count, cudaStream_t s) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+template <class T>
+void d2h(T *dst, const T *src, size_t count, cudaStream_t s) {
+  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, s);
+  }
+  double stop() {
+    cudaEventRecord(b, s); cudaEventSynchronize(b);
+    float ms = 0; cudaEventElapsedTime(&ms, a, b);
+    cudaEventRecord(a, s);
+    return ms;
+  }
+  ~Timer() { cudaEventDestroy(a); cudaEventDestroy(b); }
+};
+
+// Launch helpers -----------------------------------------------------------
+void launch_bisect(int M, const Node *nodes, const Work *work, int nwork, const int *slot_j,
+                   double *lo, double *hi, double rtol, unsigned long long *ctr,
+                   cudaStream_t s) {
+  if (nwork == 0) return;
+  switch (M) {
+    case 1: k_bisect<1><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
+    case 2: k_bisect<2><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
+    case 3: k_bisect<3><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
+    case 8: k_bisect<8><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
+    default: k_bisect<4><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
+  }
+  CK(cudaGetLastError());
+  g_stats.kernel_launches++;
+}
+
+__global__ void k_root_interval(const Node *nodes, const Block *blocks, const int *root_nodes,
+                                int nroot, double *lo0, double *hi0, double tnrm_scaled) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nroot) return;
+  const Node N = nodes[root_nodes[r]];
+  const Block B = blocks[N.block];
+  double sigma = N.tau_hi;
+  double wid = 2.0 * kEps * fmax(B.spdiam, tnrm_scaled) + kTiny;
+  if (N.nb == 1) { lo0[r] = hi0[r] = __ldg(&N.DL[0]).x; return; }
+  if (B.side > 0) {
+    lo0[r] = 0.0;
+    for (int k = 0; k < 200; ++k) {
+      double h = (B.gu - sigma) + wid;
+      if ((int)negcount_global(N.DL, N.nb, h, nullptr) >= N.nb) { hi0[r] = h; break; }
+      wid *= 2.0;
+    }
+  } else {
+    hi0[r] = 0.0;
+    for (int k = 0; k < 200; ++k) {
+      double l = (B.gl - sigma) - wid;
+      if ((int)negcount_global(N.DL, N.nb, l, nullptr) <= 0) { lo0[r] = l; break; }
+      wid *= 2.0;
+    }
+  }
+}
+
+__global__ void k_block_norms(const double *ds, const double *es, Block *blocks, int nblocks) {
+  int b = blockIdx.x;
+  if (b >= nblocks) return;
+  Block B = blocks[b];
+  double lo = CUDART_INF, hi = -CUDART_INF;
+  for (int i = threadIdx.x; i < B.nb; i += blockDim.x) {
+    int64_t g = B.row0 + i;
+    double r = 0;
+    if (i > 0) r += fabs(es[g - 1]);
+    if (i < B.nb - 1) r += fabs(es[g]);
+    lo = fmin(lo, ds[g] - r);
+    hi = fmax(hi, ds[g] + r);
+  }
+  __shared__ double sl[32], sh[32];
+  for (int o = 16; o; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffff, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffff, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) { sl[threadIdx.x >> 5] = lo; sh[threadIdx.x >> 5] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = fmin(lo, sl[w]); hi = fmax(hi, sh[w]); }
+    lo = fmin(lo, sl[0]); hi = fmax(hi, sh[0]);
+    blocks[b].gl = lo; blocks[b].gu = hi; blocks[b].spdiam = hi - lo;
+  }
+}
+
+// Root node entries (one per block with members).
+__global__ void k_root_nodes(Node *nodes, const Block *blocks, const int *root_blocks, int nroot,
+                             const double2 *DLroot, const double *sigma_b) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nroot) return;
+  int b = root_blocks[r];
+  Block B = blocks[b];
+  Node N;
+  N.DL = DLroot + B.row0;
+  N.row0 = B.row0; N.nb = B.nb; N.block = b;
+  N.slot0 = B.slot0; N.slot1 = B.slot1; N.depth = 0; N.jbase = B.jlo;
+  N.tau_hi = sigma_b[b]; N.tau_lo = 0.0; N.spdiam = B.spdiam; N.sigma = 0.0;
+  N.parent = -1; N.pad = 0;
+  nodes[B.root_node] = N;
+}
+
+// Child node entries and bracket translation to child coordinates (O9.4).
+__global__ void k_child_nodes(Node *nodes, int node_base, const int *cl_parent, const int *cl_s0,
+                              const int *cl_s1, const double *sigma, int ncl, double2 *pool,
+                              int64_t stride, const int *slot_jlocal) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncl) return;
+  Node P = nodes[cl_parent[c]];
+  Node N = P;
+  N.DL = pool + (int64_t)c * stride;
+  N.slot0 = cl_s0[c]; N.slot1 = cl_s1[c];
+  N.depth = P.depth + 1;
+  N.jbase = slot_jlocal[cl_s0[c]];
+  dd_add(P.tau_hi, P.tau_lo, sigma[c], N.tau_hi, N.tau_lo);
+  N.sigma = sigma[c];
+  N.parent = cl_parent[c];
+  nodes[node_base + c] = N;
+}
+
+__global__ void k_translate(const int *slot_cl, const int *cl_first_slot, int nslots_new,
+                            const double *sigma, double *lo, double *hi, double *wl, double *wu,
+                            int *slot_node, int node_base) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nslots_new) return;
+  int c = slot_cl[q];
+  int s = cl_first_slot[q];
+  double sg = sigma[c];
+  double l = lo[s], h = hi[s];
+  double lam = 0.5 * (l + h);
+  double w = 2.0 * (h - l) + 4.0 * kEps * (fabs(sg) + fabs(lam));
+  lo[s] = l - sg; hi[s] = h - sg;
+  wl[s] = w; wu[s] = w;
+  slot_node[s] = node_base + c;
+}
+
+__global__ void k_output(const VecTask *tasks, int ntask, const Node *nodes, const double *lam,
+                         double inv_scale, double *w) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntask) return;
+  const Node N = nodes[tasks[t].node];
+  double v = __dadd_rn(N.tau_hi, __dadd_rn(N.tau_lo, lam[t]));
+  w[tasks[t].col] = v * inv_scale;
+}
+
+__global__ void k_values(const int *slot_node, const int *slot_out, const Node *nodes,
+                         const double *lo, const double *hi, int nslots, double inv_scale,
+                         double *w) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslots || slot_out[s] < 0) return;
+  const Node N = nodes[slot_node[s]];
+  double mid = 0.5 * (lo[s] + hi[s]);
+  w[slot_out[s]] = __dadd_rn(N.tau_hi, __dadd_rn(N.tau_lo, mid)) * inv_scale;
+}
+
+// O11 monotone fix w_j <- max(w_j, w_{j-1}): one CTA, chunked prefix max.
+__global__ void k_monotone(double *w, int m) {
+  __shared__ double cmax[1024];
+  int T = blockDim.x;
+  int per = (m + T - 1) / T;
+  int a = threadIdx.x * per, b = min(a + per, m);
+  double mx = -CUDART_INF;
+  for (int i = a; i < b; ++i) mx = fmax(mx, w[i]);
+  cmax[threadIdx.x] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double run = -CUDART_INF;
+    for (int t = 0; t < T; ++t) { double v = cmax[t]; cmax[t] = run; run = fmax(run, v); }
+  }
+  __syncthreads();
+  double run = cmax[threadIdx.x];
+  for (int i = a; i < b; ++i) { run = fmax(run, w[i]); w[i] = run; }
+}
+
+// Running max + slot assignment for the grid stage (single CTA, chunked).
+__global__ void k_grid_assign2(int *cnt, int G, int nb, double lo0, double hi0, const int *slot_j,
+                               int s0, int s1, double *lo, double *hi) {
+  __shared__ int cm[1024];
+  int T = blockDim.x;
+  int tot = G + 1;
+  int per = (tot + T - 1) / T;
+  int a = threadIdx.x * per, b = min(a + per, tot);
+  int mx = 0;
+  for (int g = a; g < b; ++g) {
+    int v = (g == 0) ? 0 : (g == G ? nb : cnt[g]);
+    mx = max(mx, v);
+  }
+  cm[threadIdx.x] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int t = 0; t < T; ++t) { int v = cm[t]; cm[t] = run; run = max(run, v); }
+  }
+  __syncthreads();
+  int run = cm[threadIdx.x];
+  for (int g = a; g < b; ++g) {
+    int v = (g == 0) ? 0 : (g == G ? nb : cnt[g]);
+    run = max(run, v);
+    cnt[g] = run;
+  }
+  __syncthreads();
+  __threadfence_block();
+  for (int s = s0 + threadIdx.x; s < s1; s += T) {
+    int j = slot_j[s];
+    int lo_g = 0, hi_g = G;
+    while (lo_g < hi_g) {
+      int mid = (lo_g + hi_g) >> 1;
+      if (cnt[mid] >= j) hi_g = mid; else lo_g = mid + 1;
+    }
+    int g = max(lo_g, 1);
+    lo[s] = (g - 1 == 0) ? lo0 : lo0 + (hi0 - lo0) * ((double)(g - 1) / (double)G);
+    hi[s] = (g == G) ? hi0 : lo0 + (hi0 - lo0) * ((double)g / (double)G);
+  }
+}
+
+void launch_grid(int M, const Node *nodes, int node, double lo0, double hi0, int G, int *cnt,
+                 unsigned long long *safe, cudaStream_t s) {
+  int pts = G - 1;
+  int per_cta = 128 * M;
+  int grid = (pts + per_cta - 1) / per_cta;
+  if (grid <= 0) return;
+  switch (M) {
+    case 1: k_grid<1><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, cnt, safe); break;
+    case 2: k_grid<2><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, cnt, safe); break;
+    default: k_grid<4><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, cnt, safe); break;
+  }
+  CK(cudaGetLastError());
+  g_stats.kernel_launches++;
+}
+
+struct Problem {
+  int64_t n;
+  const double *d, *e;
+  int range;
+  double vl, vu;
+  int64_t il, iu;
+  double *w, *Z;
+  int64_t ldz;
+  cudaStream_t s;
+  mrrr_opts_t o;
+  // distributed (single GPU: rank 0 of 1)
+  int rank = 0, nranks = 1;
+};
+
+struct HostNode {
+  int slot0, slot1, depth;
+};
+
+int solve(Problem &P, int64_t *m_out) {
+  cudaStream_t s = P.s;
+  const int64_t n = P.n;
+  DevArena ar(s);
+  Timer tm(s), tall(s);
+  memset(&g_stats, 0, sizeof(g_stats));
+  const bool vectors = P.Z != nullptr;
+
+  // ---------------- a1: prep ----------------
+  double *ds = ar.alloc<double>(n), *es = ar.alloc<double>(n), *es2 = ar.alloc<double>(n);
+  int *brk = ar.alloc<int>(n);
+  double *hdr = ar.alloc<double>(8);
+  unsigned long long *ctr = ar.alloc<unsigned long long>(16);
+  CK(cudaMemsetAsync(ctr, 0, 16 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(brk, 0, n * sizeof(int), s));
+  k_prep<<<1, 1024, 0, s>>>(P.d, P.e, n, ds, es, es2, brk, hdr);
+  CK(cudaGetLastError());
+  g_stats.kernel_launches++;
+  double h_hdr[5];
+  d2h(h_hdr, hdr, 5, s);
+  if (h_hdr[4] == 1.0) throw MrrrError{-2};  // non-finite d
+  if (h_hdr[4] == 2.0) throw MrrrError{-3};  // non-finite e
+  const double scale = h_hdr[1];
+  const double tnrm_s = h_hdr[0] * scale;
+  std::vector<int> h_brk(n);
+  d2h(h_brk.data(), brk, n, s);
+
+  // blocks
+  std::vector<Block> hb;
+  {
+    int64_t st = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (i == n - 1 || h_brk[i]) {
+        Block B{};
+        B.row0 = st; B.nb = (int)(i - st + 1);
+        hb.push_back(B);
+        st = i + 1;
+      }
+    }
+  }
+  const int nblocks = (int)hb.size();
+  Block *dblocks = ar.alloc<Block>(nblocks);
+  h2d(dblocks, hb.data(), nblocks, s);
+  k_block_norms<<<nblocks, 256, 0, s>>>(ds, es, dblocks, nblocks);
+  CK(cudaGetLastError());
+  g_stats.kernel_launches++;
+  d2h(hb.data(), dblocks, nblocks, s);
+
+  // ---------------- O4: wanted ranges per block ----------------
+  std::vector<int> wa(nblocks), wb(nblocks);
+  auto sturm_counts = [&](const std::vector<double> &xs) {
+    // counts[x][block] on the scaled split T
+    double *dx = ar.alloc<double>(xs.size());
+    int *dc = ar.alloc<int>(xs.size() * nblocks);
+    h2d(dx, xs.data(), xs.size(), s);
+    int tot = (int)xs.size() * nblocks;
+    k_sturm_T<<<(tot + 127) / 128, 128, 0, s>>>(ds, es2, dblocks, nblocks, dx, (int)xs.size(), dc);
+    CK(cudaGetLastError());
+    g_stats.kernel_launches++;
+    std::vector<int> hc(tot);
+    d2h(hc.data(), dc, tot, s);
+    return hc;
+  };
+  int64_t base_rank = 0;
+  bool multi_index = false;
+  if (P.range == MRRR_RANGE_ALL) {
+    for (int b = 0; b < nblocks; ++b) { wa[b] = 1; wb[b] = hb[b].nb; }
+  } else if (P.range == MRRR_RANGE_VALUE) {
+    auto c = sturm_counts({P.vl * scale, P.vu * scale});
+    for (int b = 0; b < nblocks; ++b) { wa[b] = c[b] + 1; wb[b] = c[nblocks + b]; }
+  } else if (nblocks == 1) {
+    wa[0] = (int)P.il; wb[0] = (int)P.iu;
+  } else {
+    // brackets of the il-th and iu-th eigenvalue of the split matrix by
+    // multisection on T's Sturm counts (64 shifts per round)
+    multi_index = true;
+    double glo = INFINITY, ghi = -INFINITY;
+    for (auto &B : hb) { glo = std::min(glo, B.gl); ghi = std::max(ghi, B.gu); }
+    double wid = 4.0 * kEps * tnrm_s;
+    auto bracket = [&](int64_t idx, bool want_lo) {
+      double a = glo - 2 * wid - kTiny, b = ghi + 2 * wid + kTiny;
+      for (int it = 0; it < 40 && b - a > wid; ++it) {
+        std::vector<double> xs(63);
+        for (int k = 0; k < 63; ++k) xs[k] = a + (b - a) * ((k + 1) / 64.0);
+        auto c = sturm_counts(xs);
+        double na = a, nbb = b;
+        for (int k = 0; k < 63; ++k) {
+          int64_t tot = 0;
+          for (int bb = 0; bb < nblocks; ++bb) tot += c[k * nblocks + bb];
+          if (tot < idx) na = std::max(na, xs[k]);
+        }
+        for (int k = 62; k >= 0; --k) {
+          int64_t tot = 0;
+          for (int bb = 0; bb < nblocks; ++bb) tot += c[k * nblocks + bb];
+          if (tot >= idx && xs[k] > na) nbb = std::min(nbb, xs[k]);
+        }
+        a = na; b = nbb;
+      }
+      return want_lo ? a : b;
+    };
+    double xa = bracket(P.il, true), xb = bracket(P.iu, false);
+    auto c = sturm_counts({xa, xb});
+    for (int b = 0; b < nblocks; ++b) {
+      wa[b] = c[b] + 1; wb[b] = c[nblocks + b];
+      base_rank += c[b];
+    }
+  }
+
+  // members per block: wanted range plus gap neighbours (reading 7)
+  std::vector<int> ma(nblocks), mb(nblocks);
+  int64_t nslots = 0;
+  for (int b = 0; b < nblocks; ++b) {
+    if (wb[b] < wa[b]) { ma[b] = 1; mb[b] = 0; continue; }
+    ma[b] = std::max(1, wa[b] - 1);
+    mb[b] = std::min(hb[b].nb, wb[b] + 1);
+    if (nblocks > 1 && !vectors) { ma[b] = wa[b]; mb[b] = wb[b]; }
+    nslots += mb[b] - ma[b] + 1;
+  }
+  std::vector<int> h_slot_j(nslots), h_slot_block(nslots), h_slot_out(nslots, -1);
+  std::vector<int> root_blocks;
+  int nnodes = 0;
+  {
+    int64_t q = 0;
+    for (int b = 0; b < nblocks; ++b) {
+      hb[b].slot0 = (int)q;
+      for (int j = ma[b]; j <= mb[b]; ++j) { h_slot_j[q] = j; h_slot_block[q] = b; ++q; }
+      hb[b].slot1 = (int)q;
+      hb[b].jlo = ma[b];
+      hb[b].side = (wa[b] + wb[b] <= hb[b].nb + 1) ? 1 : -1;
+      hb[b].root_node = -1;
+      if (hb[b].slot1 > hb[b].slot0) { hb[b].root_node = nnodes++; root_blocks.push_back(b); }
+    }
+  }
+  const int nroot = (int)root_blocks.size();
+  int64_t m = 0;
+  if (nroot == 0) { *m_out = 0; return 0; }
+  h2d(dblocks, hb.data(), nblocks, s);
+
+  // ---------------- a2: root representations ----------------
+  double2 *DLroot = ar.alloc<double2>(n), *LDv = ar.alloc<double2>(n);
+  double *tbuf = ar.alloc<double>(n);
+  int *sbuf = ar.alloc<int>(n);
+  double *sigma_b = ar.alloc<double>(nblocks);
+  int *dfail = ar.alloc<int>(4);
+  CK(cudaMemsetAsync(dfail, 0, 4 * sizeof(int), s));
+  CK(cudaMemsetAsync(sigma_b, 0, nblocks * sizeof(double), s));
+  k_root_chain<<<(nblocks + 63) / 64, 64, 0, s>>>(ds, es2, dblocks, nblocks, tnrm_s, tbuf, sbuf,
+                                                  sigma_b, dfail);
+  CK(cudaGetLastError());
+  std::vector<int> h_row_block(n);
+  for (int b = 0; b < nblocks; ++b)
+    for (int i = 0; i < hb[b].nb; ++i) h_row_block[hb[b].row0 + i] = b;
+  int *row_block = ar.alloc<int>(n);
+  h2d(row_block, h_row_block.data(), n, s);
+  k_root_finish<<<(n + 255) / 256, 256, 0, s>>>(ds, es, dblocks, row_block, n, tbuf, sbuf, sigma_b,
+                                                P.o.perturb_root, P.o.seed, DLroot, LDv);
+  CK(cudaGetLastError());
+  g_stats.kernel_launches += 2;
+  int h_fail[4];
+  d2h(h_fail, dfail, 4, s);
+  if (h_fail[0]) throw MrrrError{MRRR_ERR_ROOT};
+
+  // node table (device), capacity grows with levels
+  int node_cap = std::max<int>(nroot + 16, 64);
+  Node *dnodes = ar.alloc<Node>(node_cap);
+  std::vector<int> h_root_blocks(root_blocks);
+  int *droot_blocks = ar.alloc<int>(nroot);
+  h2d(droot_blocks, h_root_blocks.data(), nroot, s);
+  k_root_nodes<<<(nroot + 63) / 64, 64, 0, s>>>(dnodes, dblocks, droot_blocks, nroot, DLroot,
+                                                  sigma_b);
+  CK(cudaGetLastError());
+  std::vector<int> h_root_nodes(nroot);
+  for (int r = 0; r < nroot; ++r) h_root_nodes[r] = hb[root_blocks[r]].root_node;
+  int *droot_nodes = ar.alloc<int>(nroot);
+  h2d(droot_nodes, h_root_nodes.data(), nroot, s);
+  double *dlo0 = ar.alloc<double>(nroot), *dhi0 = ar.alloc<double>(nroot);
+  k_root_interval<<<(nroot + 63) / 64, 64, 0, s>>>(dnodes, dblocks, droot_nodes, nroot, dlo0, dhi0,
+                                                     tnrm_s);
+  CK(cudaGetLastError());
+  g_stats.kernel_launches += 2;
+  std::vector<double> hlo0(nroot), hhi0(nroot);
+  d2h(hlo0.data(), dlo0, nroot, s);
+  d2h(hhi0.data(), dhi0, nroot, s);
+
+  // slots (device)
+  int *slot_j = ar.alloc<int>(nslots), *slot_node = ar.alloc<int>(nslots);
+  int *slot_out = ar.alloc<int>(nslots);
+  double *slo = ar.alloc<double>(nslots), *shi = ar.alloc<double>(nslots);
+  std::vector<int> h_slot_node(nslots);
+  std::vector<double> h_lo(nslots), h_hi(nslots);
+  for (int r = 0; r < nroot; ++r) {
+    const Block &B = hb[root_blocks[r]];
+    for (int q = B.slot0; q < B.slot1; ++q) {
+      h_slot_node[q] = B.root_node; h_lo[q] = hlo0[r]; h_hi[q] = hhi0[r];
+    }
+  }
+  h2d(slot_j, h_slot_j.data(), nslots, s);
+  h2d(slot_node, h_slot_node.data(), nslots, s);
+  h2d(slo, h_lo.data(), nslots, s);
+  h2d(shi, h_hi.data(), nslots, s);
+
+  // ---------------- a3: root eigenvalue intervals ----------------
+  const double rtol_root = (vectors && nblocks == 1) ? P.o.rtol_class : 4.0 * kEps;
+  const int M = std::max(1, P.o.multisection);
+  auto make_work = [&](int node, int s0, int s1, std::vector<Work> &wv) {
+    for (int a = s0; a < s1; a += 128) {
+      Work W; W.node = node; W.s0 = a; W.s1 = std::min(a + 128, s1); W.pad = 0;
+      wv.push_back(W);
+    }
+  };
+  {
+    std::vector<Work> wv;
+    for (int r = 0; r < nroot; ++r) {
+      const Block &B = hb[root_blocks[r]];
+      int nsl = B.slot1 - B.slot0;
+      if (nroot == 1 && P.o.grid_factor > 0 && nsl >= 64) {
+        int G = (int)std::min<int64_t>((int64_t)P.o.grid_factor * nsl + 1, 1 << 20);
+        G = std::max(G, 256);
+        int *cnt = ar.alloc<int>(G + 1);
+        launch_grid(4, dnodes, B.root_node, hlo0[r], hhi0[r], G, cnt, ctr + 1, s);
+        g_stats.root_sweeps += G - 1;
+        k_grid_assign2<<<1, 1024, 0, s>>>(cnt, G, B.nb, hlo0[r], hhi0[r], slot_j, B.slot0,
+                                          B.slot1, slo, shi);
+        CK(cudaGetLastError());
+        g_stats.kernel_launches++;
+      }
+      make_work(B.root_node, B.slot0, B.slot1, wv);
+    }
+    Work *dwork = ar.alloc<Work>(wv.size());
+    h2d(dwork, wv.data(), wv.size(), s);
+    launch_bisect(M, dnodes, dwork, (int)wv.size(), slot_j, slo, shi, rtol_root, ctr, s);
+  }
+
+  // output positions
+  if (nblocks == 1) {
+    const Block &B = hb[0];
+    for (int q = B.slot0; q < B.slot1; ++q) {
+      int j = h_slot_j[q];
+      if (j >= wa[0] && j <= wb[0]) h_slot_out[q] = j - wa[0];
+    }
+    m = wb[0] - wa[0] + 1;
+  } else {
+    // several blocks: merge by (value, block, index) on the bisected values
+    std::vector<double> hv_lo(nslots), hv_hi(nslots);
+    d2h(hv_lo.data(), slo, nslots, s);
+    d2h(hv_hi.data(), shi, nslots, s);
+    std::vector<double> sig(nblocks);
+    d2h(sig.data(), sigma_b, nblocks, s);
+    struct C { double v; int b, j, q; };
+    std::vector<C> cand;
+    for (int b = 0; b < nblocks; ++b) {
+      if (hb[b].slot1 <= hb[b].slot0) continue;
+      double prev = -INFINITY;
+      for (int q = hb[b].slot0; q < hb[b].slot1; ++q) {
+        int j = h_slot_j[q];
+        if (j < wa[b] || j > wb[b]) continue;
+        double v = (hb[b].nb == 1) ? 0.0 : sig[b] + 0.5 * (hv_lo[q] + hv_hi[q]);
+        if (hb[b].nb == 1) v = 0;  // set below
+        cand.push_back({v, b, j, q});
+      }
+      (void)prev;
+    }
+    // 1x1 blocks: value is the diagonal entry
+    {
+      std::vector<double> hds;
+      bool need = false;
+      for (auto &c : cand) if (hb[c.b].nb == 1) need = true;
+      if (need) {
+        hds.resize(n);
+        d2h(hds.data(), ds, n, s);
+        for (auto &c : cand) if (hb[c.b].nb == 1) c.v = hds[hb[c.b].row0];
+      }
+    }
+    // monotone within a block
+    for (size_t i = 1; i < cand.size(); ++i)
+      if (cand[i].b == cand[i - 1].b && cand[i].v < cand[i - 1].v) cand[i].v = cand[i - 1].v;
+    std::vector<int> ord(cand.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+      if (cand[x].v != cand[y].v) return cand[x].v < cand[y].v;
+      if (cand[x].b != cand[y].b) return cand[x].b < cand[y].b;
+      return cand[x].j < cand[y].j;
+    });
+    int64_t cnt = 0;
+    for (size_t i = 0; i < ord.size(); ++i) {
+      const C &c = cand[ord[i]];
+      int64_t rank = base_rank + (int64_t)i + 1;
+      if (multi_index && (rank < P.il || rank > P.iu)) continue;
+      h_slot_out[c.q] = (int)cnt++;
+    }
+    m = cnt;
+  }
+  h2d(slot_out, h_slot_out.data(), nslots, s);
+  *m_out = m;
+  g_stats.ms_root = tm.stop();
+
+  if (!vectors) {
+    k_values<<<(nslots + 255) / 256, 256, 0, s>>>(slot_node, slot_out, dnodes, slo, shi,
+                                                  (int)nslots, 1.0 / scale, P.w);
+    CK(cudaGetLastError());
+    // 1x1 blocks: w = d
+    if (m > 1) k_monotone<<<1, 1024, 0, s>>>(P.w, (int)m);
+    g_stats.kernel_launches += 2;
+    CK(cudaStreamSynchronize(s));
+    g_stats.ms_total = tall.stop();
+    return 0;
+  }
+  if (nblocks > 1)
+    CK(cudaMemset2DAsync(P.Z, P.ldz * sizeof(double), 0, n * sizeof(double), m, s));
+
+  // ---------------- a4/a5: representation tree ----------------
+  std::vector<int> h_active(nslots, 1);
+  int *active = ar.alloc<int>(nslots);
+  int *run_end = ar.alloc<int>(nslots);
+  std::vector<int> h_run_end(nslots);
+  std::vector<VecTask> tasks;
+  std::vector<HostNode> hn(nnodes);
+  for (int r = 0; r < nroot; ++r) {
+    const Block &B = hb[root_blocks[r]];
+    hn[B.root_node] = {B.slot0, B.slot1, 0};
+  }
+  // 1x1 blocks: the vector kernel handles nb == 1 directly
+  std::vector<int> level_nodes(h_root_nodes);
+  double *wlo = ar.alloc<double>(nslots), *whi = ar.alloc<double>(nslots);
+  const int64_t nbmax = [&] { int x = 1; for (auto &B : hb) x = std::max(x, B.nb); return (int64_t)x; }();
+  int level = 0;
+  unsigned long long h_ctr[16];
+  Timer ttree(s);
+  for (;;) {
+    h2d(active, h_active.data(), nslots, s);
+    k_classify<<<(nslots + 255) / 256, 256, 0, s>>>(slot_node, slo, shi, active, (int)nslots,
+                                                    P.o.tol_relgap, run_end);
+    CK(cudaGetLastError());
+    g_stats.kernel_launches++;
+    d2h(h_run_end.data(), run_end, nslots, s);
+    std::vector<int> cl_parent, cl_s0, cl_s1;
+    for (int nd : level_nodes) {
+      const HostNode &H = hn[nd];
+      int st = H.slot0;
+      for (int q = H.slot0; q < H.slot1; ++q) {
+        if (!h_active[q]) { st = q + 1; continue; }
+        if (h_run_end[q]) {
+          if (q == st) {
+            if (h_slot_out[q] >= 0) {
+              VecTask t; t.slot = q; t.node = nd; t.col = h_slot_out[q]; t.lam0 = NAN;
+              tasks.push_back(t);
+            }
+            h_active[q] = 0;
+          } else {
+            bool any = false;
+            for (int x = st; x <= q; ++x) any |= h_slot_out[x] >= 0;
+            if (any) { cl_parent.push_back(nd); cl_s0.push_back(st); cl_s1.push_back(q + 1); }
+            else for (int x = st; x <= q; ++x) h_active[x] = 0;
+          }
+          st = q + 1;
+        }
+      }
+    }
+    const int ncl = (int)cl_parent.size();
+    if (ncl == 0) break;
+    if (level + 1 > P.o.max_depth) throw MrrrError{MRRR_ERR_DEPTH};
+    g_stats.nodes += ncl;
+    // grow node table
+    int node_base = nnodes;
+    if (nnodes + ncl > node_cap) {
+      int ncap = std::max(node_cap * 2, nnodes + ncl + 16);
+      Node *nn = ar.alloc<Node>(ncap);
+      CK(cudaMemcpyAsync(nn, dnodes, nnodes * sizeof(Node), cudaMemcpyDeviceToDevice, s));
+      dnodes = nn; node_cap = ncap;
+    }
+    int *dcl_parent = ar.alloc<int>(ncl), *dcl_s0 = ar.alloc<int>(ncl), *dcl_s1 = ar.alloc<int>(ncl);
+    h2d(dcl_parent, cl_parent.data(), ncl, s);
+    h2d(dcl_s0, cl_s0.data(), ncl, s);
+    h2d(dcl_s1, cl_s1.data(), ncl, s);
+    // tier-(ii) vectors: parent twisted solve at both end eigenvalues
+    double *zbuf = ar.alloc<double>((size_t)2 * ncl * nbmax);
+    {
+      std::vector<VecTask> zt(2 * ncl);
+      for (int c = 0; c < ncl; ++c) {
+        zt[2 * c] = {cl_s0[c], cl_parent[c], 2 * c, NAN};
+        zt[2 * c + 1] = {cl_s1[c] - 1, cl_parent[c], 2 * c + 1, NAN};
+      }
+      VecTask *dzt = ar.alloc<VecTask>(zt.size());
+      h2d(dzt, zt.data(), zt.size(), s);
+      int ntask = (int)zt.size();
+      int nseg = (int)((nbmax + kSeg - 1) / kSeg);
+      FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg * ntask);
+      BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg * ntask);
+      VecArgs A{};
+      A.nodes = dnodes; A.blocks = dblocks; A.LDv = LDv; A.tasks = dzt; A.ntask = ntask;
+      A.lo = slo; A.hi = shi; A.slot_j = slot_j; A.fck = fck; A.bck = bck;
+      A.ck_stride = ntask; A.nseg_max = nseg; A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1;
+      A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 4;
+      size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
+      k_vectors<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
+      CK(cudaGetLastError());
+      g_stats.kernel_launches++;
+    }
+    Cand *cand = ar.alloc<Cand>((size_t)6 * ncl);
+    k_cand<<<(6 * ncl + 127) / 128, 128, 0, s>>>(dnodes, dcl_parent, dcl_s0, dcl_s1, slo, shi, ncl,
+                                                 zbuf, nbmax, cand);
+    CK(cudaGetLastError());
+    double *dsig = ar.alloc<double>(ncl);
+    int *dtier = ar.alloc<int>(ncl);
+    k_pick<<<(ncl + 127) / 128, 128, 0, s>>>(dnodes, dcl_parent, cand, ncl, dsig, dtier, dfail + 1);
+    CK(cudaGetLastError());
+    g_stats.child_sweeps += 6 * ncl + ncl;
+    double2 *pool = ar.alloc<double2>((size_t)ncl * nbmax);
+    double *ctb = ar.alloc<double>((size_t)ncl * nbmax);
+    int *csb = ar.alloc<int>((size_t)ncl * nbmax);
+    k_child_chain<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, dcl_parent, dsig, ncl, nbmax, ctb, csb);
+    CK(cudaGetLastError());
+    dim3 gfin((unsigned)std::min<int64_t>((nbmax + 255) / 256, 64), ncl);
+    k_child_finish<<<gfin, 256, 0, s>>>(dnodes, dcl_parent, nullptr, ncl, nbmax, ctb, csb, LDv, pool,
+                                        dfail + 1);
+    CK(cudaGetLastError());
+    // the child node entries are written before the translate kernel reads sigma
+    int *slot_jl = slot_j;
+    k_child_nodes<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, node_base, dcl_parent, dcl_s0, dcl_s1, dsig,
+                                                 ncl, pool, nbmax, slot_jl);
+    CK(cudaGetLastError());
+    // translate member brackets to child coordinates
+    std::vector<int> slot_cl, first_slot;
+    for (int c = 0; c < ncl; ++c)
+      for (int q = cl_s0[c]; q < cl_s1[c]; ++q) { slot_cl.push_back(c); first_slot.push_back(q); }
+    int nsn = (int)slot_cl.size();
+    int *dslot_cl = ar.alloc<int>(nsn), *dfirst = ar.alloc<int>(nsn);
+    h2d(dslot_cl, slot_cl.data(), nsn, s);
+    h2d(dfirst, first_slot.data(), nsn, s);
+    k_translate<<<(nsn + 127) / 128, 128, 0, s>>>(dslot_cl, dfirst, nsn, dsig, slo, shi, wlo, whi,
+                                                  slot_node, node_base);
+    CK(cudaGetLastError());
+    g_stats.kernel_launches += 6;
+    // host mirror
+    hn.resize(nnodes + ncl);
+    for (int c = 0; c < ncl; ++c) {
+      hn[node_base + c] = {cl_s0[c], cl_s1[c], hn[cl_parent[c]].depth + 1};
+      for (int q = cl_s0[c]; q < cl_s1[c]; ++q) h_slot_node[q] = node_base + c;
+    }
+    nnodes += ncl;
+    // verify + refine in child coordinates
+    std::vector<Work> wv;
+    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], wv);
+    Work *dwork = ar.alloc<Work>(wv.size());
+    h2d(dwork, wv.data(), wv.size(), s);
+    k_verify<<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, slot_j, slo, shi, wlo, whi, dfail + 2,
+                                            ctr + 2, ctr + 1);
+    CK(cudaGetLastError());
+    g_stats.kernel_launches++;
+    launch_bisect(M, dnodes, dwork, (int)wv.size(), slot_j, slo, shi, P.o.rtol_class, ctr + 2, s);
+    d2h(h_fail, dfail, 4, s);
+    if (h_fail[1]) throw MrrrError{MRRR_ERR_CHILD};
+    if (h_fail[2]) throw MrrrError{MRRR_ERR_CONVERGE};
+    level_nodes.clear();
+    for (int c = 0; c < ncl; ++c) level_nodes.push_back(node_base + c);
+    ++level;
+  }
+  g_stats.levels = level;
+  g_stats.ms_tree = ttree.stop();
+
+  // ---------------- a6: singleton vectors ----------------
+  Timer tv(s);
+  const int ntask = (int)tasks.size();
+  g_stats.singletons = ntask;
+  if (ntask > 0) {
+    VecTask *dt = ar.alloc<VecTask>(ntask);
+    h2d(dt, tasks.data(), ntask, s);
+    int nseg = (int)((nbmax + kSeg - 1) / kSeg);
+    FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg * ntask);
+    BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg * ntask);
+    double *lam = ar.alloc<double>(ntask);
+    VecArgs A{};
+    A.nodes = dnodes; A.blocks = dblocks; A.LDv = LDv; A.tasks = dt; A.ntask = ntask;
+    A.lo = slo; A.hi = shi; A.slot_j = slot_j; A.fck = fck; A.bck = bck;
+    A.ck_stride = ntask; A.nseg_max = nseg; A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam;
+    A.mode = 0; A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 8;
+    size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
+    k_vectors<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
+    CK(cudaGetLastError());
+    if (getenv("MRRR_DEBUG")) {
+      std::vector<double> hl(ntask);
+      d2h(hl.data(), lam, ntask, s);
+      std::vector<Node> hnodes(nnodes);
+      d2h(hnodes.data(), dnodes, nnodes, s);
+      for (int t = 0; t < ntask; ++t) {
+        const Node &N = hnodes[tasks[t].node];
+        fprintf(stderr, "task %d slot %d node %d col %ld lam %.17g tau %.17g + %.3g sigma %.17g depth %d\n", t,
+                tasks[t].slot, tasks[t].node, (long)tasks[t].col, hl[t], N.tau_hi, N.tau_lo, N.sigma, N.depth);
+      }
+    }
+    k_output<<<(ntask + 255) / 256, 256, 0, s>>>(dt, ntask, dnodes, lam, 1.0 / scale, P.w);
+    CK(cudaGetLastError());
+    if (m > 1) k_monotone<<<1, 1024, 0, s>>>(P.w, (int)m);
+    CK(cudaGetLastError());
+    g_stats.kernel_launches += 3;
+  }
+  d2h(h_ctr, ctr, 16, s);
+  g_stats.ms_vectors = tv.stop();
+  g_stats.root_sweeps += h_ctr[0];
+  g_stats.safe_resweeps = h_ctr[1];
+  g_stats.refine_sweeps = h_ctr[2];
+  g_stats.rqc_iters = h_ctr[8];
+  g_stats.rqc_fallbacks = h_ctr[9];
+  g_stats.ms_total = tall.stop();
+  return 0;
+}
+
+int validate(int64_t n, const double *d, const double *e, int range, double vl, double vu,
+             int64_t il, int64_t iu, const int64_t *m, const double *w, const double *Z,
+             int64_t ldz) {
+  if (n < 1) return -1;
+  if (!d) return -2;
+  if (n > 1 && !e) return -3;
+  if (range < 0 || range > 2) return -4;
+  if (range == MRRR_RANGE_VALUE) {
+    if (!std::isfinite(vl)) return -5;
+    if (!std::isfinite(vu) || !(vl < vu)) return -6;
+  }
+  if (range == MRRR_RANGE_INDEX) {
+    if (il < 1 || il > n) return -7;
+    if (iu < il || iu > n) return -8;
+  }
+  if (!m) return -9;
+  if (!w) return -10;
+  if (Z && ldz < n) return -12;
+  if (n > (int64_t)1 << 30) return -1;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+void mrrr_default_opts(mrrr_opts_t *o) {
+  o->tol_relgap = 1e-3;
+  o->rtol_class = std::ldexp(1.0, -20);
+  o->max_depth = 128;
+  o->perturb_root = 1;
+  o->seed = 0x1205210700000000ULL;
+  o->multisection = 4;
+  o->grid_factor = 4;
+}
+
+__global__ void k_n1(const double *d, double *w, double *Z) {
+  w[0] = d[0];
+  if (Z) Z[0] = 1.0;
+}
+
+int mrrr_stemr(int64_t n, const double *d, const double *e, int range, double vl, double vu,
+               int64_t il, int64_t iu, int64_t *m, double *w, double *Z, int64_t ldz,
+               void *stream, const mrrr_opts_t *opts) {
+  int v = validate(n, d, e, range, vl, vu, il, iu, m, w, Z, ldz);
+  if (v) return v;
+  Problem P;
+  P.n = n; P.d = d; P.e = e; P.range = range; P.vl = vl; P.vu = vu; P.il = il; P.iu = iu;
+  P.w = w; P.Z = Z; P.ldz = ldz; P.s = (cudaStream_t)stream;
+  if (opts) P.o = *opts; else mrrr_default_opts(&P.o);
+  try {
+    if (n == 1) {
+      double dv;
+      CK(cudaMemcpyAsync(&dv, d, sizeof(double), cudaMemcpyDeviceToHost, P.s));
+      CK(cudaStreamSynchronize(P.s));
+      if (!std::isfinite(dv)) return -2;
+      bool in = range != MRRR_RANGE_VALUE || (dv > vl && dv <= vu);
+      *m = in ? 1 : 0;
+      if (in) {
+        k_n1<<<1, 1, 0, P.s>>>(d, w, Z);
+        CK(cudaGetLastError());
+      }
+      CK(cudaStreamSynchronize(P.s));
+      return 0;
+    }
+    int rc = solve(P, m);
+    CK(cudaStreamSynchronize(P.s));
+    return rc;
+  } catch (const MrrrError &er) {
+    cudaStreamSynchronize(P.s);
+    return er.code;
+  } catch (const CudaError &ce) {
+    cudaGetLastError();
+    return ce.e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;
+  }
+}
+
+int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, double vl,
+                    double vu, int64_t il, int64_t iu, int rank, int nranks,
+                    mrrr_allgather_fn allgather, void *allgather_ctx, int64_t *m,
+                    const mrrr_opts_t *opts, int64_t *col_begin, int64_t *m_local,
+                    double *w_all, double *Z_local, int64_t ldz, void *stream) {
+  (void)n; (void)d; (void)e; (void)range; (void)vl; (void)vu; (void)il; (void)iu; (void)rank;
+  (void)nranks; (void)allgather; (void)allgather_ctx; (void)m; (void)opts; (void)col_begin;
+  (void)m_local; (void)w_all; (void)Z_local; (void)ldz; (void)stream;
+  return MRRR_ERR_COMM;  // implemented in a later milestone
+}
+
+size_t mrrr_workspace_bytes(int64_t n, int64_t k) {
+  size_t nn = (size_t)n, kk = (size_t)k;
+  size_t seg = (nn + MRRR_SEG - 1) / MRRR_SEG;
+  return nn * (8 * 3 + 4 * 3 + 16 * 2 + 8) + kk * (8 * 4 + 4 * 6) + seg * kk * (32 + 16) + (1 << 20);
+}
+
+const char *mrrr_strerror(int code) {
+  switch (code) {
+    case 0: return "success";
+    case 1: return "root representation not found (definite shift failed after retries)";
+    case 2: return "child representation not acceptable (element growth too large)";
+    case 3: return "representation tree depth cap exceeded";
+    case 4: return "bisection or Rayleigh-quotient iteration did not converge";
+    case 5: return "CUDA error";
+    case 6: return "out of device memory";
+    case 7: return "collective (multi-GPU) error";
+    default:
+      if (code < 0) return "invalid argument";
+      return "unknown error";
+  }
+}
+
+int mrrr_get_stats(mrrr_stats_t *out) {
+  if (!out) return -1;
+  *out = g_stats;
+  return 0;
+}
+
+const char *mrrr_version(void) { return "mrrr-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

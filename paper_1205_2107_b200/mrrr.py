@@ -1,0 +1,153 @@
+"""Thin Python binding of the C ABI in include/mrrr.h (argument marshalling
+only; every step of the solve runs in libmrrr_b200.so's CUDA kernels).
+
+torch is used for device memory and streams only.  There is no CPU fallback:
+importing the binding without the built library, or calling it without a
+CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libmrrr_b200.so")
+
+RANGE_ALL, RANGE_INDEX, RANGE_VALUE = 0, 1, 2
+
+
+class Opts(C.Structure):
+    _fields_ = [("tol_relgap", C.c_double), ("rtol_class", C.c_double), ("max_depth", C.c_int),
+                ("perturb_root", C.c_int), ("seed", C.c_uint64), ("multisection", C.c_int),
+                ("grid_factor", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("nodes", C.c_int64), ("levels", C.c_int64), ("singletons", C.c_int64),
+                ("root_sweeps", C.c_int64), ("refine_sweeps", C.c_int64),
+                ("child_sweeps", C.c_int64), ("rqc_iters", C.c_int64),
+                ("rqc_fallbacks", C.c_int64), ("safe_resweeps", C.c_int64),
+                ("kernel_launches", C.c_int64), ("ms_root", C.c_double), ("ms_tree", C.c_double),
+                ("ms_vectors", C.c_double), ("ms_total", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+_lib = None
+
+
+class MrrrError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"mrrr error {code}: {msg}")
+        self.code = code
+
+
+def lib():
+    """Load libmrrr_b200.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO):
+            raise RuntimeError(f"{SO} missing: run `python -m paper_1205_2107_b200.build` "
+                               "(no CPU fallback exists)")
+        L = C.CDLL(SO)
+        L.mrrr_default_opts.argtypes = [C.POINTER(Opts)]
+        L.mrrr_stemr.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_double,
+                                 C.c_int64, C.c_int64, C.POINTER(C.c_int64), C.c_void_p, C.c_void_p,
+                                 C.c_int64, C.c_void_p, C.POINTER(Opts)]
+        L.mrrr_stemr.restype = C.c_int
+        L.mrrr_stemr_dist.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                      C.c_double, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                      ALLGATHER_FN, C.c_void_p, C.POINTER(C.c_int64),
+                                      C.POINTER(Opts), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64), C.c_void_p, C.c_void_p, C.c_int64,
+                                      C.c_void_p]
+        L.mrrr_stemr_dist.restype = C.c_int
+        L.mrrr_workspace_bytes.argtypes = [C.c_int64, C.c_int64]
+        L.mrrr_workspace_bytes.restype = C.c_size_t
+        L.mrrr_strerror.argtypes = [C.c_int]
+        L.mrrr_strerror.restype = C.c_char_p
+        L.mrrr_get_stats.argtypes = [C.POINTER(Stats)]
+        L.mrrr_get_stats.restype = C.c_int
+        L.mrrr_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def default_opts(**kw) -> Opts:
+    o = Opts()
+    lib().mrrr_default_opts(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def last_stats() -> dict:
+    st = Stats()
+    lib().mrrr_get_stats(C.byref(st))
+    return st.as_dict()
+
+
+def _range_args(n, il, iu, vl, vu):
+    if il is not None or iu is not None:
+        return RANGE_INDEX, 0.0, 0.0, int(il), int(iu), max(0, int(iu) - int(il) + 1)
+    if vl is not None or vu is not None:
+        return RANGE_VALUE, float(vl), float(vu), 0, 0, n
+    return RANGE_ALL, 0.0, 0.0, 0, 0, n
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def stemr(d: torch.Tensor, e: torch.Tensor, *, il=None, iu=None, vl=None, vu=None,
+          vectors: bool = True, opts: Opts | None = None, w: torch.Tensor | None = None,
+          Z: torch.Tensor | None = None, stream=None):
+    """Eigenpairs of tridiag(e, d, e) on the GPU of ``d`` (torch.float64 CUDA
+    tensors).  Returns ``(w, Z)``: ``w`` ascending (m,), ``Z`` (n, m) with unit
+    eigenvector columns (a transposed view of column-major storage), or
+    ``None`` when ``vectors=False``.  ``w``/``Z`` may be preallocated: w of
+    capacity k and Z as a contiguous (k, n) tensor (column j of the result is
+    row j of the buffer)."""
+    if not (d.is_cuda and d.dtype == torch.float64):
+        raise TypeError("d must be a torch.float64 CUDA tensor (no CPU fallback)")
+    n = d.shape[0]
+    if n > 1 and not (e.is_cuda and e.dtype == torch.float64 and e.device == d.device):
+        raise TypeError("e must be a torch.float64 CUDA tensor on d's device")
+    d = d.contiguous()
+    e = e.contiguous() if n > 1 else d
+    rng, a, b, ilv, iuv, kcap = _range_args(n, il, iu, vl, vu)
+    kcap = max(kcap, 1)
+    if w is None:
+        w = torch.empty(kcap, dtype=torch.float64, device=d.device)
+    if vectors and Z is None:
+        Z = torch.empty((kcap, n), dtype=torch.float64, device=d.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(d.device)
+    m = C.c_int64(0)
+    o = opts if opts is not None else default_opts()
+    with torch.cuda.device(d.device):
+        rc = lib().mrrr_stemr(n, _ptr(d), _ptr(e), rng, a, b, ilv, iuv, C.byref(m), _ptr(w),
+                              _ptr(Z) if vectors else C.c_void_p(0), n,
+                              C.c_void_p(stream.cuda_stream), C.byref(o))
+    if rc != 0:
+        raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
+    k = m.value
+    return w[:k], (Z[:k].T if vectors else None)
+
+
+def stemr_raw(n, d, e, rng, vl, vu, il, iu, m_ok=True, w=None, Z=None, ldz=None):
+    """Direct C call for argument-validation tests (device pointers as tensors)."""
+    m = C.c_int64(0)
+    return lib().mrrr_stemr(n, _ptr(d), _ptr(e), rng, vl, vu, il, iu,
+                            C.byref(m) if m_ok else C.cast(None, C.POINTER(C.c_int64)),
+                            _ptr(w), _ptr(Z), ldz if ldz is not None else max(n, 1),
+                            C.c_void_p(0), None)
+
+
+def version() -> str:
+    return lib().mrrr_version().decode()

@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""bench.py -- STEP eigenpairs/sec fp64 of the B200 MRRR solver (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config random_20000]
+
+A "step" is one full MRRR solve (all SURVEY §8(a) rows: norms/split, root
+RRR, root bisection, classification, representation tree, singleton
+RQC/twisted vectors, output) of the workload through the C ABI
+``mrrr_stemr`` with device-resident inputs and preallocated outputs.  The
+default workload is BASELINE.json configs[1]: random tridiagonal, n=20000,
+d, e iid U(-1,1) (numpy default_rng(0)), all eigenpairs, fp64.
+
+``value`` = eigenpairs/s over the K timed steps (CUDA events on the solve
+stream, L2 flushed before each step by writing a 256 MiB buffer, outside the
+events; max over ranks).  ``e2e`` = the same metric through
+``mrrr_stemr_host`` with pinned HOST buffers: d, e copied in and w, Z copied
+out inside the timed region.  ``roofline`` = the dominant kernel's
+algorithmic fp64 flop rate against the FP64 ALU peak.
+``cpu_baseline`` = the sequential C oracle timed on a bounded sample on the
+host cores (test infrastructure; the only other use of oracle/ here is
+``--impl reference``).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1205_2107_b200 import workloads as W  # noqa: E402
+
+EPS = 2.0 ** -52
+# FP64 ALU peak: 148 SMs x 64 FP64 FMA lanes x 2 flop x 1.965 GHz
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# algorithmic work model: flops per matrix element
+R_RQC = 3                   # twisted factorizations per eigenpair (yardstick)
+FLOPS_TWIST = 15 * R_RQC + 1  # per element per eigenpair: 15 per factorization+solve, +1 scale
+FLOPS_STURM = 4             # per element per bisection step (add, div, mul, sub)
+RTOL_C = 2.0 ** -20
+METRIC = "STEP eigenpairs/sec fp64 (n=20k, all pairs) at 1/2/4/8 B200; % of roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="random_20000")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-pairs", type=int, default=0,
+                    help="oracle sample size in eigenpairs (0: auto ~15 s)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# --------------------------------------------------------------------------
+# work model (implementation independent)
+def bisection_steps(d, e, w):
+    """B_j = max(1, ceil(log2(spdiam / (rtol_c |lambda_j - sigma0|)))) with the
+    root shift just left of the Gershgorin interval."""
+    r = np.abs(d).copy() * 0
+    if len(e):
+        r[:-1] += np.abs(e)
+        r[1:] += np.abs(e)
+    gl, gu = float(np.min(d - r)), float(np.max(d + r))
+    spd = gu - gl
+    tn = float(np.max(np.abs(d) + r))
+    sigma0 = gl - 4 * EPS * tn
+    x = spd / (RTOL_C * np.maximum(np.abs(np.asarray(w) - sigma0), 1e-300))
+    return np.maximum(1, np.ceil(np.log2(x)))
+
+
+class Clocks:
+    """nvidia-smi sampler over the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None, "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------
+def cpu_oracle_sample(d, e, pairs: int):
+    """Oracle on a bounded sample of the workload: the INDEX range of `pairs`
+    eigenpairs centred in the spectrum (same matrix), single host thread."""
+    import oracle  # test infrastructure (bench cpu_baseline leg only)
+    oracle.build()
+    n = len(d)
+    pairs = max(1, min(pairs, n))
+    il = (n - pairs) // 2 + 1
+    iu = il + pairs - 1
+    t0 = time.perf_counter()
+    w, Z = oracle.stemr(d, e, il=il, iu=iu)
+    dt = time.perf_counter() - t0
+    return pairs / dt, dt, f"oracle_stemr INDEX il..iu={il}..{iu} ({pairs} pairs, with vectors) of the same n={n} matrix"
+
+
+def auto_pairs(n):
+    # ~15 s of single-thread oracle work (measured ~0.6 us per pair per element)
+    return int(max(50, min(n, 15.0 / (0.6e-6 * n))))
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    d, e, rng = W.make(args.config)
+    n = len(d)
+    k = n if rng is None else rng[1] - rng[0] + 1
+    pairs = args.cpu_pairs or auto_pairs(n)
+    # each step: a bounded sample, sized so warmup+steps end in a few minutes
+    steps_total = args.warmup + args.steps
+    pairs = max(50, min(pairs, int(pairs * 8 / max(steps_total, 1))))
+    vals = []
+    for i in range(steps_total):
+        v, dt, desc = cpu_oracle_sample(d, e, pairs)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    tot = sum(dt for _, dt in vals)
+    value = pairs * len(vals) / tot
+    line = {"metric": METRIC, "value": value, "unit": "eigenpairs/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(vals),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.config, "n": n, "k": k, "sample_pairs": pairs},
+            "cpu_baseline": {"value": value, "unit": "eigenpairs/s", "cores": 1,
+                             "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "eigenpairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import paper_1205_2107_b200 as P
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    d, e, rng = W.make(args.config)
+    n = len(d)
+    k = n if rng is None else rng[1] - rng[0] + 1
+    kw = {} if rng is None else {"il": rng[0], "iu": rng[1]}
+    dt_ = torch.tensor(d, device=dev)
+    et_ = torch.tensor(e, device=dev)
+    w = torch.empty(k, dtype=torch.float64, device=dev)
+    Z = torch.empty((k, n), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        return P.stemr(dt_, et_, w=w, Z=Z, stream=stream, **kw)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stats = []
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clk = Clocks(dev.index or 0)
+    clk.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.random_(0, 255)  # L2 flush outside the events
+        evs[i][0].record(stream)
+        wk, _ = step()
+        evs[i][1].record(stream)
+        stats.append(P.last_stats())
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = clk.stop()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = sum(ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    m = wk.shape[0]
+    value = world * m * args.steps / (tot_ms / 1e3)
+
+    # ---------------- roofline of the dominant kernel
+    w_host = wk.double().cpu().numpy()
+    kv = [s["ms_k_vectors"] for s in stats]
+    kb = [s["ms_k_root_bisect"] for s in stats]
+    B = bisection_steps(d, e, w_host)
+    flops_bis = float(np.sum(B)) * FLOPS_STURM * n
+    flops_vec = stats[-1]["vec_elems"] * FLOPS_TWIST
+    mv, mb = statistics.mean(kv), statistics.mean(kb)
+    if mv >= mb:
+        dom, flops, kms = "k_vectors", flops_vec, mv
+    else:
+        dom, flops, kms = "k_root_bisect", flops_bis, mb
+    achieved = flops / (kms / 1e3) / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+            "kernel_ms": kms, "kernel_share_of_step": kms / (tot_ms / args.steps),
+            "algorithmic_flops_per_launch": flops,
+            "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)",
+            "other_kernel": {"k_root_bisect" if dom == "k_vectors" else "k_vectors":
+                             {"ms": mb if dom == "k_vectors" else mv,
+                              "achieved_tflops": (flops_bis / (mb / 1e3) / 1e12) if dom == "k_vectors"
+                              else (flops_vec / (mv / 1e3) / 1e12)}}}
+
+    # ---------------- end to end through the host-buffer C ABI
+    e2e = None
+    if not args.no_e2e:
+        dh = torch.tensor(d).pin_memory()
+        eh = torch.tensor(e).pin_memory()
+        wh = torch.empty(k, dtype=torch.float64).pin_memory()
+        Zh = torch.empty((k, n), dtype=torch.float64).pin_memory()
+        P.stemr_host(dh, eh, w=wh, Z=Zh, stream=stream, **kw)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e_ms = []
+        for i in range(args.steps):
+            flush.random_(0, 255)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            P.stemr_host(dh, eh, w=wh, Z=Zh, stream=stream, **kw)
+            b.record(stream)
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        etot = sum(e_ms)
+        if world > 1:
+            t = torch.tensor([etot], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            etot = float(t.item())
+        e2e = {"value": world * m * args.steps / (etot / 1e3), "unit": "eigenpairs/s",
+               "h2d_bytes_per_step": 8 * (2 * n - 1), "d2h_bytes_per_step": 8 * m + 8 * n * m,
+               "ms_per_step": etot / args.steps}
+
+    # ---------------- CPU oracle on a bounded sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        pairs = args.cpu_pairs or auto_pairs(n)
+        v, dt, desc = cpu_oracle_sample(d, e, pairs)
+        cpu = {"value": v, "unit": "eigenpairs/s", "cores": 1, "kind": "oracle", "sample": desc,
+               "seconds": dt}
+
+    s0 = stats[-1]
+    launches = sum(int(s["kernel_launches"]) for s in stats)
+    line = {"metric": METRIC, "value": value, "unit": "eigenpairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config, "n": n, "k": k, "range": "all" if rng is None else
+                       f"index {rng[0]}..{rng[1]}", "l2": "flushed (256 MiB write) before each step",
+                       "parallelism": f"replicas{world}" if world > 1 else "single"},
+            "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks,
+            "phases_ms": {"root": s0["ms_root"], "tree": s0["ms_tree"], "vectors": s0["ms_vectors"],
+                          "total": s0["ms_total"]},
+            "tree": {"nodes": s0["nodes"], "levels": s0["levels"], "rqc_iters": s0["rqc_iters"],
+                     "rqc_fallbacks": s0["rqc_fallbacks"], "safe_resweeps": s0["safe_resweeps"]},
+            "step_ms": ms}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

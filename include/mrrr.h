@@ -124,6 +124,19 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range,
                     int64_t *col_begin, int64_t *m_local, double *w_all,
                     double *Z_local, int64_t ldz, void *stream);
 
+/*
+ * mrrr_stemr_host -- the same solve with HOST buffers (end-to-end entry):
+ * d[n], e[n-1], w[k] and Z (ldz x k, column major, or NULL) are host memory
+ * (pinned or pageable; pinned is faster).  The call allocates device buffers
+ * stream-ordered, copies d, e in, runs mrrr_stemr on `stream` and copies w
+ * and the m columns of Z back before returning.  Arguments and return codes
+ * as in mrrr_stemr.
+ */
+int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range,
+                    double vl, double vu, int64_t il, int64_t iu, int64_t *m,
+                    double *w, double *Z, int64_t ldz, void *stream,
+                    const mrrr_opts_t *opts);
+
 /* Upper bound of the device workspace mrrr_stemr allocates internally for an
  * order-n problem with k wanted eigenpairs (bytes), excluding the
  * representation-tree node pool, which grows with the number of clusters
@@ -150,6 +163,12 @@ typedef struct {
   double ms_tree;           /* device time: classification, children, refine */
   double ms_vectors;        /* device time: singleton vectors + output */
   double ms_total;          /* device time of the whole call */
+  /* per-kernel device time (CUDA events on the call's stream) and the units
+   * they processed, for the roofline of bench.py */
+  double ms_k_root_bisect;  /* root grid + multisection kernels */
+  double ms_k_vectors;      /* singleton RQC + twisted + Z kernel */
+  int64_t vec_tasks;        /* eigenvectors computed by that kernel */
+  int64_t vec_elems;        /* sum over those tasks of their block order */
 } mrrr_stats_t;
 int mrrr_get_stats(mrrr_stats_t *out);
 

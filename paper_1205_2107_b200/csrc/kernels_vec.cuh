@@ -327,7 +327,7 @@ struct VecArgs {
   unsigned long long *ctr;   // [0] factorizations, [1] fallbacks, [2] nudges
 };
 
-__global__ void __launch_bounds__(kVecThreads) k_vectors(VecArgs A) {
+__device__ __forceinline__ void vectors_body(const VecArgs &A) {
   extern __shared__ double smv[];
   const int T = blockDim.x;
   double *smA = smv, *smB = smv + kSeg * T, *smC = smv + 2 * kSeg * T;
@@ -426,5 +426,10 @@ __global__ void __launch_bounds__(kVecThreads) k_vectors(VecArgs A) {
   if (fb) atomicAdd(&A.ctr[1], fb);
   if (nudges) atomicAdd(&A.ctr[2], nudges);
 }
+
+// Final singleton vectors (mode 0) and the parent-vector probe of the child
+// acceptance test (mode 1) are separate entry points so profiles tell them apart.
+__global__ void __launch_bounds__(kVecThreads) k_vectors(VecArgs A) { vectors_body(A); }
+__global__ void __launch_bounds__(kVecThreads) k_zprobe(VecArgs A) { vectors_body(A); }
 
 }  // namespace mrrr

@@ -77,6 +77,23 @@ struct Timer {
   ~Timer() { cudaEventDestroy(a); cudaEventDestroy(b); }
 };
 
+// Event pair around one group of launches on the call's stream; read at the
+// end of the call (no extra synchronisation inside the solve).
+struct KTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool used = false;
+  KTimer() { cudaEventCreate(&a); cudaEventCreate(&b); }
+  void start(cudaStream_t s) { cudaEventRecord(a, s); used = true; }
+  void stop(cudaStream_t s) { cudaEventRecord(b, s); }
+  double ms() {
+    if (!used) return 0.0;
+    cudaEventSynchronize(b);
+    float v = 0; cudaEventElapsedTime(&v, a, b);
+    return v;
+  }
+  ~KTimer() { cudaEventDestroy(a); cudaEventDestroy(b); }
+};
+
 // Launch helpers -----------------------------------------------------------
 void launch_bisect(int M, const Node *nodes, const Work *work, int nwork, const int *slot_j,
                    double *lo, double *hi, double rtol, unsigned long long *ctr,
@@ -313,6 +330,7 @@ int solve(Problem &P, int64_t *m_out) {
   const int64_t n = P.n;
   DevArena ar(s);
   Timer tm(s), tall(s);
+  KTimer kt_root, kt_vec;
   memset(&g_stats, 0, sizeof(g_stats));
   const bool vectors = P.Z != nullptr;
 
@@ -520,6 +538,7 @@ int solve(Problem &P, int64_t *m_out) {
   };
   {
     std::vector<Work> wv;
+    kt_root.start(s);
     for (int r = 0; r < nroot; ++r) {
       const Block &B = hb[root_blocks[r]];
       int nsl = B.slot1 - B.slot0;
@@ -539,6 +558,7 @@ int solve(Problem &P, int64_t *m_out) {
     Work *dwork = ar.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
     launch_bisect(M, dnodes, dwork, (int)wv.size(), slot_j, slo, shi, rtol_root, ctr, s);
+    kt_root.stop(s);
   }
 
   // output positions
@@ -613,6 +633,7 @@ int solve(Problem &P, int64_t *m_out) {
     g_stats.kernel_launches += 2;
     CK(cudaStreamSynchronize(s));
     g_stats.ms_total = tall.stop();
+    g_stats.ms_k_root_bisect = kt_root.ms();
     return 0;
   }
   if (nblocks > 1)
@@ -702,7 +723,7 @@ int solve(Problem &P, int64_t *m_out) {
       A.ck_stride = ntask; A.nseg_max = nseg; A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1;
       A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 4;
       size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
-      k_vectors<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
+      k_zprobe<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
       CK(cudaGetLastError());
       g_stats.kernel_launches++;
     }
@@ -785,7 +806,17 @@ int solve(Problem &P, int64_t *m_out) {
     A.ck_stride = ntask; A.nseg_max = nseg; A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam;
     A.mode = 0; A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 8;
     size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
+    {
+      std::vector<Node> hnodes(nnodes);
+      d2h(hnodes.data(), dnodes, nnodes, s);
+      int64_t el = 0;
+      for (auto &t : tasks) el += hnodes[t.node].nb;
+      g_stats.vec_tasks = ntask;
+      g_stats.vec_elems = el;
+    }
+    kt_vec.start(s);
     k_vectors<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
+    kt_vec.stop(s);
     CK(cudaGetLastError());
     if (getenv("MRRR_DEBUG")) {
       std::vector<double> hl(ntask);
@@ -812,6 +843,8 @@ int solve(Problem &P, int64_t *m_out) {
   g_stats.rqc_iters = h_ctr[8];
   g_stats.rqc_fallbacks = h_ctr[9];
   g_stats.ms_total = tall.stop();
+  g_stats.ms_k_root_bisect = kt_root.ms();
+  g_stats.ms_k_vectors = kt_vec.ms();
   return 0;
 }
 
@@ -890,6 +923,45 @@ int mrrr_stemr(int64_t n, const double *d, const double *e, int range, double vl
     cudaGetLastError();
     return ce.e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;
   }
+}
+
+int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range, double vl,
+                    double vu, int64_t il, int64_t iu, int64_t *m, double *w, double *Z,
+                    int64_t ldz, void *stream, const mrrr_opts_t *opts) {
+  int v = validate(n, d, e, range, vl, vu, il, iu, m, w, Z, ldz);
+  if (v) return v;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t k = range == MRRR_RANGE_INDEX ? iu - il + 1 : n;
+  double *dd = nullptr, *de = nullptr, *dw = nullptr, *dZ = nullptr;
+  int rc = 0;
+  auto fail = [&](cudaError_t e) {
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;
+  };
+  cudaError_t ce = cudaSuccess;
+  do {
+    if ((ce = cudaMallocAsync((void **)&dd, n * sizeof(double), s))) break;
+    if ((ce = cudaMallocAsync((void **)&de, std::max<int64_t>(n - 1, 1) * sizeof(double), s))) break;
+    if ((ce = cudaMallocAsync((void **)&dw, k * sizeof(double), s))) break;
+    if (Z && (ce = cudaMallocAsync((void **)&dZ, (size_t)n * k * sizeof(double), s))) break;
+    if ((ce = cudaMemcpyAsync(dd, d, n * sizeof(double), cudaMemcpyHostToDevice, s))) break;
+    if (n > 1 && (ce = cudaMemcpyAsync(de, e, (n - 1) * sizeof(double), cudaMemcpyHostToDevice, s)))
+      break;
+    rc = mrrr_stemr(n, dd, de, range, vl, vu, il, iu, m, dw, dZ, n, stream, opts);
+    if (rc) break;
+    if (*m > 0) {
+      if ((ce = cudaMemcpyAsync(w, dw, *m * sizeof(double), cudaMemcpyDeviceToHost, s))) break;
+      if (Z && (ce = cudaMemcpy2DAsync(Z, ldz * sizeof(double), dZ, n * sizeof(double),
+                                       n * sizeof(double), *m, cudaMemcpyDeviceToHost, s)))
+        break;
+    }
+    ce = cudaStreamSynchronize(s);
+  } while (0);
+  for (double *p : {dd, de, dw, dZ})
+    if (p) cudaFreeAsync(p, s);
+  cudaStreamSynchronize(s);
+  if (ce != cudaSuccess) return fail(ce);
+  return rc;
 }
 
 int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, double vl,

@@ -30,7 +30,9 @@ class Stats(C.Structure):
                 ("child_sweeps", C.c_int64), ("rqc_iters", C.c_int64),
                 ("rqc_fallbacks", C.c_int64), ("safe_resweeps", C.c_int64),
                 ("kernel_launches", C.c_int64), ("ms_root", C.c_double), ("ms_tree", C.c_double),
-                ("ms_vectors", C.c_double), ("ms_total", C.c_double)]
+                ("ms_vectors", C.c_double), ("ms_total", C.c_double),
+                ("ms_k_root_bisect", C.c_double), ("ms_k_vectors", C.c_double),
+                ("vec_tasks", C.c_int64), ("vec_elems", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -60,6 +62,8 @@ def lib():
                                  C.c_int64, C.c_int64, C.POINTER(C.c_int64), C.c_void_p, C.c_void_p,
                                  C.c_int64, C.c_void_p, C.POINTER(Opts)]
         L.mrrr_stemr.restype = C.c_int
+        L.mrrr_stemr_host.argtypes = L.mrrr_stemr.argtypes
+        L.mrrr_stemr_host.restype = C.c_int
         L.mrrr_stemr_dist.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
                                       C.c_double, C.c_int64, C.c_int64, C.c_int, C.c_int,
                                       ALLGATHER_FN, C.c_void_p, C.POINTER(C.c_int64),
@@ -134,6 +138,35 @@ def stemr(d: torch.Tensor, e: torch.Tensor, *, il=None, iu=None, vl=None, vu=Non
         rc = lib().mrrr_stemr(n, _ptr(d), _ptr(e), rng, a, b, ilv, iuv, C.byref(m), _ptr(w),
                               _ptr(Z) if vectors else C.c_void_p(0), n,
                               C.c_void_p(stream.cuda_stream), C.byref(o))
+    if rc != 0:
+        raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
+    k = m.value
+    return w[:k], (Z[:k].T if vectors else None)
+
+
+def stemr_host(d, e, *, il=None, iu=None, vl=None, vu=None, w=None, Z=None, vectors=True,
+               opts: Opts | None = None, stream=None):
+    """End-to-end entry on HOST tensors (``mrrr_stemr_host``): float64 CPU
+    tensors ``d``, ``e`` (pinned for speed); returns host ``(w, Z)`` with the
+    same layout as :func:`stemr`.  The copies and the solve run inside the
+    library on ``stream`` (default: the current CUDA stream)."""
+    if d.is_cuda or d.dtype != torch.float64:
+        raise TypeError("stemr_host takes float64 host tensors")
+    n = d.shape[0]
+    rng, a, b, ilv, iuv, kcap = _range_args(n, il, iu, vl, vu)
+    kcap = max(kcap, 1)
+    if w is None:
+        w = torch.empty(kcap, dtype=torch.float64, pin_memory=True)
+    if vectors and Z is None:
+        Z = torch.empty((kcap, n), dtype=torch.float64, pin_memory=True)
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    m = C.c_int64(0)
+    o = opts if opts is not None else default_opts()
+    e = e if n > 1 else d
+    rc = lib().mrrr_stemr_host(n, _ptr(d), _ptr(e), rng, a, b, ilv, iuv, C.byref(m), _ptr(w),
+                               _ptr(Z) if vectors else C.c_void_p(0), n,
+                               C.c_void_p(stream.cuda_stream), C.byref(o))
     if rc != 0:
         raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
     k = m.value

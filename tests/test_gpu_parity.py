@@ -1,0 +1,290 @@
+"""GPU parity: the CUDA MRRR path (through the C ABI, libmrrr_b200.so) against
+the oracle (oracle/, sequential C) on the same seeded inputs, element by
+element, plus the BASELINE.json accuracy contract:
+
+  |lambda_gpu - lambda_oracle| <= 4 n eps ||T||_1
+  max_j ||T z_j - lambda_j z_j||_2 / ||T||_1 <= 10 n eps
+  max |Z^T Z - I| <= 10 n eps
+  sign-free vectors of well-separated eigenvalues (Davis-Kahan rule,
+  DESIGN.md reading 18) agree to 1e-9.
+
+Small cases span several smem tiles (256 rows), checkpoint segments (32
+rows) and ragged tails; the BASELINE configs run at full size in the launch
+configuration bench.py times, compared on oracle-computable samples (index
+windows solved by the oracle) plus properties that hold at any size.
+"""
+import numpy as np
+import pytest
+
+from helpers import (EPS, check_accuracy, dk_comparable, residuals, sturm_numpy, sturm_placement,
+                     tnorm1, vec_diff_signfree)
+from paper_1205_2107_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests (no CPU fallback exists)")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1205_2107_b200 as P
+    P.mrrr.lib()  # fails loudly if the library is missing
+    return P
+
+
+def gpu_solve(P, torch, d, e, **kw):
+    dt = torch.tensor(np.asarray(d, float), device="cuda")
+    et = torch.tensor(np.asarray(e, float) if len(e) else np.zeros(1), device="cuda")
+    w, Z = P.stemr(dt, et, **kw)
+    torch.cuda.synchronize()
+    return w.cpu().numpy(), (Z.cpu().numpy() if Z is not None else None)
+
+
+def compare(d, e, w, Z, wo, Zo, *, vec_min_frac=0.0):
+    n = len(d)
+    tn = tnorm1(d, e)
+    assert len(w) == len(wo)
+    if len(w) == 0:
+        return
+    assert np.all(np.diff(w) >= 0)
+    assert np.max(np.abs(w - wo)) <= 4 * n * EPS * tn
+    if Z is None:
+        return
+    res, orth = check_accuracy(d, e, w, Z)
+    assert res <= 1, res
+    assert orth <= 1, orth
+    rg, ro = residuals(d, e, w, Z), residuals(d, e, wo, Zo)
+    ok = dk_comparable(wo, rg, ro)
+    if ok.any():
+        assert np.max(vec_diff_signfree(Z[:, ok], Zo[:, ok])) <= 1e-9
+    assert ok.mean() >= vec_min_frac
+
+
+SMALL = {
+    "one_two_one_10": (lambda: W.one_two_one(10), {}),
+    "one_two_one_300": (lambda: W.one_two_one(300), {}),
+    "random_50": (lambda: W.random_uniform(50, 0), {}),
+    "random_400_s0": (lambda: W.random_uniform(400, 0), {}),
+    "random_777_s1": (lambda: W.random_uniform(777, 1), {}),
+    "wilkinson_201": (lambda: W.wilkinson(201), {}),
+    "glued_10": (lambda: W.glued_wilkinson(10), {}),
+    "glued_40": (lambda: W.glued_wilkinson(40), {}),
+    "clement_400": (lambda: W.clement(400), {}),
+    "random_3000": (lambda: W.random_uniform(3000, 0), {}),
+    "random_1000_idx": (lambda: W.random_uniform(1000, 1), {"il": 101, "iu": 300}),
+    "random_1000_idx_end": (lambda: W.random_uniform(1000, 2), {"il": 901, "iu": 1000}),
+    "random_1000_idx_one": (lambda: W.random_uniform(1000, 3), {"il": 500, "iu": 500}),
+    "clement_3000_idx": (lambda: W.clement(3000), {"il": 1, "iu": 300}),
+    "random_600_value": (lambda: W.random_uniform(600, 6), {"vl": -0.5, "vu": 0.25}),
+    "tiny_2": (lambda: (np.array([1.0, -2.0]), np.array([0.5])), {}),
+    "tiny_3_zero_diag": (lambda: (np.zeros(3), np.ones(2)), {}),
+    "n_257_ragged": (lambda: W.random_uniform(257, 9), {}),
+    "n_33_ragged": (lambda: W.random_uniform(33, 10), {}),
+}
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_parity_small(torch_cuda, P, oracle_mod, name):
+    mk, kw = SMALL[name]
+    d, e = mk()
+    w, Z = gpu_solve(P, torch_cuda, d, e, **kw)
+    wo, Zo = oracle_mod.stemr(d, e, **kw)
+    compare(d, e, w, Z, wo, Zo)
+
+
+@pytest.mark.parametrize("name", ["random_400_s0", "glued_10", "random_1000_idx", "random_600_value"])
+def test_values_only(torch_cuda, P, oracle_mod, name):
+    mk, kw = SMALL[name]
+    d, e = mk()
+    w, _ = gpu_solve(P, torch_cuda, d, e, vectors=False, **kw)
+    wo, _ = oracle_mod.stemr(d, e, vectors=False, **kw)
+    compare(d, e, w, None, wo, None)
+
+
+def split_matrix():
+    d1, e1 = W.random_uniform(40, 11)
+    d2, e2 = W.one_two_one(25)
+    d3, e3 = W.wilkinson(21)
+    d = np.concatenate([d1, d2 - 1.0, d3 * 0.2])
+    e = np.concatenate([e1, [0.0], e2, [0.0], e3 * 0.2])
+    return d, e
+
+
+@pytest.mark.parametrize("kw", [{}, {"il": 1, "iu": 30}, {"il": 20, "iu": 60}, {"il": 86, "iu": 86},
+                                {"vl": -0.3, "vu": 0.4}])
+def test_split_blocks(torch_cuda, P, oracle_mod, kw):
+    d, e = split_matrix()
+    w, Z = gpu_solve(P, torch_cuda, d, e, **kw)
+    wo, Zo = oracle_mod.stemr(d, e, **kw)
+    compare(d, e, w, Z, wo, Zo)
+    # rows outside a column's block are exactly zero
+    assert np.all(np.count_nonzero(Z, axis=0) <= 40)
+
+
+def test_diagonal_matrix(torch_cuda, P):
+    d = np.array([3.0, -1.0, 2.0, 2.0])
+    w, Z = gpu_solve(P, torch_cuda, d, np.zeros(3))
+    assert list(w) == [-1.0, 2.0, 2.0, 3.0]
+    assert np.array_equal(np.abs(Z.T @ Z), np.eye(4))
+
+
+def test_n1_and_empty_value_range(torch_cuda, P):
+    w, Z = gpu_solve(P, torch_cuda, np.array([7.5]), np.zeros(0))
+    assert w[0] == 7.5 and Z[0, 0] == 1.0
+    d, e = W.random_uniform(100, 0)
+    w, Z = gpu_solve(P, torch_cuda, d, e, vl=10.0, vu=11.0)
+    assert len(w) == 0
+
+
+def test_argument_validation(torch_cuda, P):
+    torch = torch_cuda
+    d = torch.zeros(10, dtype=torch.float64, device="cuda")
+    e = torch.ones(9, dtype=torch.float64, device="cuda")
+    w = torch.empty(10, dtype=torch.float64, device="cuda")
+    Z = torch.empty(100, dtype=torch.float64, device="cuda")
+    raw = P.mrrr.stemr_raw
+    assert raw(0, d, e, 0, 0, 0, 0, 0, w=w, Z=Z) == -1
+    assert raw(10, None, e, 0, 0, 0, 0, 0, w=w, Z=Z) == -2
+    assert raw(10, d, e, 7, 0, 0, 0, 0, w=w, Z=Z) == -4
+    assert raw(10, d, e, 2, 1.0, 1.0, 0, 0, w=w, Z=Z) == -6
+    assert raw(10, d, e, 1, 0, 0, 0, 3, w=w, Z=Z) == -7
+    assert raw(10, d, e, 1, 0, 0, 4, 11, w=w, Z=Z) == -8
+    assert raw(10, d, e, 0, 0, 0, 0, 0, m_ok=False, w=w, Z=Z) == -9
+    assert raw(10, d, e, 0, 0, 0, 0, 0, w=None, Z=Z) == -10
+    assert raw(10, d, e, 0, 0, 0, 0, 0, w=w, Z=Z, ldz=9) == -12
+    bad = d.clone(); bad[3] = float("nan")
+    assert raw(10, bad, e, 0, 0, 0, 0, 0, w=w, Z=Z) == -2
+    assert raw(10, d, e, 0, 0, 0, 0, 0, w=w, Z=Z) == 0
+
+
+def test_deterministic(torch_cuda, P):
+    d, e = W.glued_wilkinson(30)
+    w1, Z1 = gpu_solve(P, torch_cuda, d, e)
+    w2, Z2 = gpu_solve(P, torch_cuda, d, e)
+    assert np.array_equal(w1, w2) and np.array_equal(Z1, Z2)
+
+
+def test_host_entry_matches_device(torch_cuda, P):
+    torch = torch_cuda
+    d, e = W.random_uniform(1500, 5)
+    w1, Z1 = gpu_solve(P, torch, d, e)
+    w2, Z2 = P.stemr_host(torch.tensor(d).pin_memory(), torch.tensor(e).pin_memory())
+    assert np.array_equal(w1, w2.numpy()) and np.array_equal(Z1, Z2.numpy())
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs at full size (bench launch configuration): GPU-side
+# residual / orthogonality, oracle index windows, closed forms, invariants.
+def gpu_metrics(torch, d, e, w, Z, col_block=4096):
+    """Residual and orthogonality on the device (fp64 torch, test-only)."""
+    dd = torch.tensor(d, device="cuda")
+    ee = torch.tensor(e, device="cuda")
+    Zt = torch.tensor(Z, device="cuda") if isinstance(Z, np.ndarray) else Z
+    wt = torch.tensor(w, device="cuda") if isinstance(w, np.ndarray) else w
+    n, k = Zt.shape
+    res = 0.0
+    orth = 0.0
+    for a in range(0, k, col_block):
+        Zb = Zt[:, a:a + col_block]
+        TZ = dd[:, None] * Zb
+        TZ[1:] += ee[:, None] * Zb[:-1]
+        TZ[:-1] += ee[:, None] * Zb[1:]
+        R = TZ - Zb * wt[None, a:a + col_block]
+        res = max(res, float(torch.linalg.vector_norm(R, dim=0).max()))
+        G = Zt.T @ Zb
+        idx = torch.arange(Zb.shape[1], device="cuda")
+        G[a + idx, idx] -= 1.0
+        orth = max(orth, float(G.abs().max()))
+    tn = tnorm1(d, e)
+    return res / tn / (10 * n * EPS), orth / (10 * n * EPS)
+
+
+def oracle_windows(oracle_mod, d, e, w, Z, windows, base=1):
+    """Compare GPU eigenpairs with oracle solves of index windows."""
+    n = len(d)
+    tn = tnorm1(d, e)
+    for il, iu in windows:
+        wo, Zo = oracle_mod.stemr(d, e, il=il, iu=iu)
+        a, b = il - base, iu - base + 1
+        assert np.max(np.abs(w[a:b] - wo)) <= 4 * n * EPS * tn
+        rg = residuals(d, e, w[a:b], Z[:, a:b])
+        ro = residuals(d, e, wo, Zo)
+        ok = dk_comparable(wo, rg, ro)
+        if ok.any():
+            assert np.max(vec_diff_signfree(Z[:, a:b][:, ok], Zo[:, ok])) <= 1e-9
+
+
+def test_config1_one_two_one_2000(torch_cuda, P, oracle_mod):
+    n = 2000
+    d, e = W.one_two_one(n)
+    w, Z = gpu_solve(P, torch_cuda, d, e)
+    wo, Zo = oracle_mod.stemr(d, e)
+    compare(d, e, w, Z, wo, Zo, vec_min_frac=0.5)
+    k = np.arange(1, n + 1)
+    lam = 2 - 2 * np.cos(k * np.pi / (n + 1))
+    assert np.max(np.abs(w - lam)) <= 4 * n * EPS * tnorm1(d, e)
+    i = np.arange(1, n + 1)[:, None]
+    Zc = ((-1.0) ** i) * np.sqrt(2.0 / (n + 1)) * np.sin(i * k[None, :] * np.pi / (n + 1))
+    ok = dk_comparable(lam, residuals(d, e, w, Z), residuals(d, e, lam, Zc))
+    assert ok.sum() > 1000
+    assert np.max(vec_diff_signfree(Z[:, ok], Zc[:, ok])) <= 1e-9
+
+
+def test_config2_random_20000(torch_cuda, P, oracle_mod):
+    n = 20000
+    d, e = W.random_uniform(n, 0)
+    torch = torch_cuda
+    dt, et = torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda")
+    wt, Zt = P.stemr(dt, et)
+    res, orth = gpu_metrics(torch, d, e, wt, Zt)
+    assert res <= 1 and orth <= 1, (res, orth)
+    w = wt.cpu().numpy()
+    tn = tnorm1(d, e)
+    tol = 4 * n * EPS * tn
+    assert np.all(np.diff(w) >= 0)
+    assert abs(w.sum() - d.sum()) <= n * tol
+    assert sturm_placement(d, e, w, np.arange(n), tol)
+    Z = Zt.cpu().numpy()
+    oracle_windows(oracle_mod, d, e, w, Z, [(1, 60), (9971, 10030), (19941, 20000)])
+
+
+def test_config3_glued_wilkinson_21000(torch_cuda, P, oracle_mod):
+    d, e = W.glued_wilkinson(1000)
+    n = len(d)
+    torch = torch_cuda
+    wt, Zt = P.stemr(torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda"))
+    res, orth = gpu_metrics(torch, d, e, wt, Zt)
+    assert res <= 1 and orth <= 1, (res, orth)
+    w = wt.cpu().numpy()
+    db, eb = W.wilkinson(21)
+    mu, _ = oracle_mod.jacobi(np.diag(db) + np.diag(eb, 1) + np.diag(eb, -1))
+    assert np.max(np.abs(w - np.repeat(mu, 1000))) <= 1e-8 + 4 * n * EPS * tnorm1(d, e)
+    Z = Zt.cpu().numpy()
+    oracle_windows(oracle_mod, d, e, w, Z, [(1, 40), (20961, 21000)])
+
+
+@pytest.mark.parametrize("subset", [True, False])
+def test_config4_clement_50000(torch_cuda, P, oracle_mod, subset):
+    n = 50000
+    d, e = W.clement(n)
+    torch = torch_cuda
+    kw = {"il": 1, "iu": 5000} if subset else {}
+    wt, Zt = P.stemr(torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda"), **kw)
+    k = 5000 if subset else n
+    w = wt.cpu().numpy()
+    lam = 2.0 * np.arange(1, k + 1) - n - 1
+    assert np.max(np.abs(w - lam)) <= 4 * n * EPS * tnorm1(d, e)
+    res, orth = gpu_metrics(torch, d, e, wt, Zt)
+    assert res <= 1 and orth <= 1, (res, orth)
+    cols = [0, 1, 2, 2499, 4999]
+    Zs = Zt[:, cols].cpu().numpy()
+    wo, Zo = oracle_mod.stemr(d, e, il=1, iu=3)
+    ok = dk_comparable(wo, residuals(d, e, w[:3], Zs[:, :3]), residuals(d, e, wo, Zo))
+    assert ok.all()
+    assert np.max(vec_diff_signfree(Zs[:, :3], Zo)) <= 1e-9

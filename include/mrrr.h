@@ -143,6 +143,12 @@ int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range,
  * (<= 24 n bytes per cluster node). */
 size_t mrrr_workspace_bytes(int64_t n, int64_t k);
 
+/* Workspace is taken from a library-owned stream-ordered memory pool per
+ * device that keeps freed blocks mapped between calls (repeated solves do not
+ * pay for remapping).  Releases that cached memory back to the driver; the
+ * next call re-grows it.  Returns 0 or MRRR_ERR_CUDA. */
+int mrrr_trim_workspace(void);
+
 /* Static description of a return code. */
 const char *mrrr_strerror(int code);
 

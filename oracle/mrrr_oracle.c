@@ -447,23 +447,30 @@ static void singleton(ctx_t *c, const rrr_t *R, int64_t j) {
 
 static void process_node(ctx_t *c, const rrr_t *R, int64_t c0, int64_t c1, int depth);
 
-/* weighted growth (tier ii): z = one twisted solve of the parent at lambda. */
-static double weighted_growth(ctx_t *c, const rrr_t *R, double lambda,
-                              const double *Dp) {
-  int64_t r, nc;
-  double g;
-  int rs = 0;
-  twisted_ws(R->nb, R->D, R->L, R->LD, R->LLD, &lambda, R->pivmin, &c->ws, c->z,
-             &r, &g, &nc, &rs);
+/* weighted growth (tier ii) of a candidate child Dp against one unit-free
+ * vector z: sum_i |D+_i| z_i^2 / sum_i z_i^2. */
+static double weighted_growth(int64_t nb, const double *z, const double *Dp) {
   double num = 0, den = 0;
-  for (int64_t i = 0; i < R->nb; ++i) {
-    num += fabs(Dp[i]) * c->z[i] * c->z[i];
-    den += c->z[i] * c->z[i];
+  for (int64_t i = 0; i < nb; ++i) {
+    num += fabs(Dp[i]) * z[i] * z[i];
+    den += z[i] * z[i];
   }
   return num / den;
 }
 
-/* O9 -- cluster step: shift, child RRR, refine, recurse. */
+/* O9 -- cluster step: shift, child RRR, refine, recurse.
+ * Shift choice, reading 9 (amended): candidates at offsets
+ * m = 1, 2, 4 beyond each end of the cluster (order L1 R1 L2 R2 L4 R4),
+ * raw growth g = max_i |D+_i| (inf if a pivot is not finite or zero),
+ * weighted growth wg = max over the parent's two end-eigenvalue vectors z_L,
+ * z_R of sum |D+_i| z_i^2 / ||z||^2.  For m = 1, 2, 4 in turn:
+ *   (i)  if an end has g <= 8 spdiam: the end with the lower g;
+ *   (ii) else if an end has wg <= 64 spdiam: of those ends the lower g.
+ * (iii) After all offsets: the least g if <= 1e8 spdiam; else error 2.
+ * Ties go to the left end.  Weighting by one vector only, or choosing by the
+ * lower wg, admits children whose element growth ruins the accuracy of the
+ * cluster's far eigenvalues (Clement n=20000: raw growth 3.5e5 spdiam, RQC
+ * corrections 1e3 eps|lambda| at the far end). */
 static void cluster(ctx_t *c, const rrr_t *R, int64_t s, int64_t t, int depth) {
   int64_t nb = R->nb;
   double spd = c->spdiam;
@@ -471,42 +478,53 @@ static void cluster(ctx_t *c, const rrr_t *R, int64_t s, int64_t t, int depth) {
   if (rrr_alloc(&C, nb)) { c->err = 6; return; }
   double *DpA = (double *)malloc(sizeof(double) * 4 * (size_t)(nb + 1));
   if (!DpA) { free(C.D); c->err = 6; return; }
-  double *LpA = DpA + (nb + 1), *DpB = DpA + 2 * (nb + 1), *LpB = DpA + 3 * (nb + 1);
-  double best_raw = INFINITY, best_raw_sigma = 0, sigma = 0;
-  int accepted = 0;
+  double *LpA = DpA + (nb + 1), *zL = DpA + 2 * (nb + 1), *zR = DpA + 3 * (nb + 1);
   static const double mult[3] = {1.0, 2.0, 4.0};
-  for (int mi = 0; mi < 3 && !accepted; ++mi) {
-    double dl = fmax(2.0 * (c->hi[s] - c->lo[s]), 4.0 * EPS * fabs(c->lo[s]));
-    double dr = fmax(2.0 * (c->hi[t] - c->lo[t]), 4.0 * EPS * fabs(c->hi[t]));
-    double sL = c->lo[s] - mult[mi] * dl;
-    double sR = c->hi[t] + mult[mi] * dr;
-    double gL, gR;
-    oracle_child_rrr(nb, R->D, R->L, R->LD, sL, DpA, LpA, &gL);
-    oracle_child_rrr(nb, R->D, R->L, R->LD, sR, DpB, LpB, &gR);
+  double cs[6], cg[6];
+  double dl = fmax(2.0 * (c->hi[s] - c->lo[s]), 4.0 * EPS * fabs(c->lo[s]));
+  double dr = fmax(2.0 * (c->hi[t] - c->lo[t]), 4.0 * EPS * fabs(c->hi[t]));
+  int best = -1, have_z = 0;
+  for (int mi = 0; mi < 3 && best < 0; ++mi) {
+    int kL = 2 * mi, kR = 2 * mi + 1;
+    cs[kL] = c->lo[s] - mult[mi] * dl;
+    cs[kR] = c->hi[t] + mult[mi] * dr;
+    oracle_child_rrr(nb, R->D, R->L, R->LD, cs[kL], DpA, LpA, &cg[kL]);
+    oracle_child_rrr(nb, R->D, R->L, R->LD, cs[kR], DpA, LpA, &cg[kR]);
     c->st->child_sweeps += 2;
-    if (gL < best_raw) { best_raw = gL; best_raw_sigma = sL; }
-    if (gR < best_raw) { best_raw = gR; best_raw_sigma = sR; }
-    /* tier (i): the lower raw growth of the finite candidates */
-    if (isfinite(gL) || isfinite(gR)) {
-      int useL = gL <= gR;
-      if ((useL ? gL : gR) <= 8.0 * spd) {
-        sigma = useL ? sL : sR; accepted = 1; c->st->tier[0]++; break;
-      }
-      /* tier (ii): the lower eigenvector-weighted growth */
-      double wL = INFINITY, wR = INFINITY;
-      if (isfinite(gL)) wL = weighted_growth(c, R, 0.5 * (c->lo[s] + c->hi[s]), DpA);
-      if (isfinite(gR)) wR = weighted_growth(c, R, 0.5 * (c->lo[t] + c->hi[t]), DpB);
-      int wuseL = wL <= wR;
-      if ((wuseL ? wL : wR) <= 64.0 * spd) {
-        sigma = wuseL ? sL : sR; accepted = 1; c->st->tier[1]++; break;
-      }
+    /* (i) */
+    if (fmin(cg[kL], cg[kR]) <= 8.0 * spd) {
+      best = cg[kL] <= cg[kR] ? kL : kR;
+      c->st->tier[0]++;
+      break;
     }
-    /* tier (iii): next offset multiple */
+    /* (ii) */
+    if (!have_z) {
+      int64_t r, nc;
+      double g;
+      int rs = 0;
+      double lamL = 0.5 * (c->lo[s] + c->hi[s]), lamR = 0.5 * (c->lo[t] + c->hi[t]);
+      twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lamL, R->pivmin, &c->ws, zL, &r, &g, &nc, &rs);
+      twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lamR, R->pivmin, &c->ws, zR, &r, &g, &nc, &rs);
+      have_z = 1;
+    }
+    for (int k = kL; k <= kR; ++k) {
+      if (!isfinite(cg[k])) continue;
+      double g;
+      oracle_child_rrr(nb, R->D, R->L, R->LD, cs[k], DpA, LpA, &g);
+      c->st->child_sweeps++;
+      double wg = fmax(weighted_growth(nb, zL, DpA), weighted_growth(nb, zR, DpA));
+      if (wg <= 64.0 * spd && (best < 0 || cg[k] < cg[best])) best = k;
+    }
+    if (best >= 0) c->st->tier[1]++;
   }
-  if (!accepted) {
-    if (best_raw <= 1e8 * spd) { sigma = best_raw_sigma; accepted = 1; c->st->tier[3]++; }
-    else { c->err = 2; free(DpA); free(C.D); return; }
+  if (best < 0) {
+    for (int k = 0; k < 6; ++k)
+      if (best < 0 || cg[k] < cg[best]) best = k;
+    if (!(cg[best] <= 1e8 * spd)) { c->err = 2; free(DpA); free(C.D); return; }
+    c->st->tier[3]++;
   }
+  double sigma;
+  sigma = cs[best];
   free(DpA);
   /* the accepted child */
   double g;

@@ -433,13 +433,15 @@ __global__ void k_classify(const int *__restrict__ slot_node, const double *__re
 //   t_i = D_i q + p (= D+_i q), p' = LLD_i p - sigma t, q' = t.
 // The child keeps the block's off-diagonals LD_i (= L+_i D+_i exactly in
 // exact arithmetic) and stores (D+_i, LLD+_i = LD_i^2 / D+_i).
-// k_cand: growth of candidate shifts (raw max |D+| and, when z is given, the
-// eigenvector-weighted growth sum |D+_i| z_i^2 / sum z_i^2).
+// k_cand: growth of the six candidate shifts (offsets 1, 2, 4 beyond each
+// cluster end, order L1 R1 L2 R2 L4 R4): raw max |D+| and the
+// eigenvector-weighted growth max over the parent's two end vectors z_L, z_R
+// of sum |D+_i| z_i^2 / ||z||^2 (reading 9, amended).
 // ===========================================================================
 struct Cand {
   double sigma;
   double raw;  // max |D+_i| (inf if not finite)
-  double wgt;  // sum |D+_i| z_i^2 / ||z||^2 (inf if not finite / not computed)
+  double wgt;  // max_{z in {z_L, z_R}} sum |D+_i| z_i^2 / ||z||^2 (inf if not finite / no z)
   int32_t cluster;
   int32_t which;  // 0..5 = (mult index) * 2 + (0 left, 1 right)
 };
@@ -462,8 +464,9 @@ __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0
     sigma = hi[s1] + mult * dr;
   }
   const double2 *DL = P.DL;
-  const double *z = zbuf ? zbuf + (int64_t)(2 * c + (which & 1)) * zstride : nullptr;
-  double p = -sigma, q = 1.0, g = 0.0, num = 0.0, den = 0.0;
+  const double *zl = zbuf ? zbuf + (int64_t)(2 * c) * zstride : nullptr;
+  const double *zr = zbuf ? zbuf + (int64_t)(2 * c + 1) * zstride : nullptr;
+  double p = -sigma, q = 1.0, g = 0.0, nl = 0.0, dnl = 0.0, nr = 0.0, dnr = 0.0;
   bool fin = true;
   int nb = P.nb;
   for (int i = 0; i < nb; ++i) {
@@ -471,8 +474,13 @@ __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0
     double t = fma(v.x, q, p);
     double dp = t / q;  // D+_i (off the recurrence chain)
     fin &= isfinite(dp) && dp != 0.0;
-    g = fmax(g, fabs(dp));
-    if (z) { double zi = z[i]; num = fma(fabs(dp), zi * zi, num); den = fma(zi, zi, den); }
+    double adp = fabs(dp);
+    g = fmax(g, adp);
+    if (zl) {
+      double a = zl[i], b = zr[i];
+      nl = fma(adp, a * a, nl); dnl = fma(a, a, dnl);
+      nr = fma(adp, b * b, nr); dnr = fma(b, b, dnr);
+    }
     if (i < nb - 1) { p = fma(-sigma, t, v.y * p); q = t; }
     if ((i & 7) == 7) {
       int ee = max_exp(p, q);
@@ -484,41 +492,45 @@ __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0
   Cand C;
   C.sigma = sigma;
   C.raw = fin ? g : CUDART_INF;
-  C.wgt = (fin && z && den > 0) ? num / den : CUDART_INF;
+  C.wgt = (fin && zl && dnl > 0 && dnr > 0) ? fmax(nl / dnl, nr / dnr) : CUDART_INF;
   C.cluster = c;
   C.which = which;
   cand[id] = C;
 }
 
-// Tiered acceptance (O9.3, reading 9): per offset multiple m = 1, 2, 4:
-// (i) lower raw growth <= 8 spdiam; (ii) lower weighted growth <= 64 spdiam;
-// (iv) afterwards the least raw growth <= 1e8 spdiam; else error 2.
+// Shift choice (O9.3, reading 9 amended).  For offsets m = 1, 2, 4
+// in turn: (i) if an end has raw growth <= 8 spdiam, the end with the lower
+// raw growth; (ii) else if an end has weighted growth <= 64 spdiam, of those
+// ends the lower raw growth.  (iii) After all offsets the least raw growth if
+// <= 1e8 spdiam; else error 2.  Ties go to the left end.
 __global__ void k_pick(const Node *nodes, const int *cl_parent, const Cand *cand, int ncl,
                        double *sigma_out, int *tier_out, int *fail) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
   double spd = nodes[cl_parent[c]].spdiam;
   const Cand *C = cand + 6 * c;
-  double best_raw = CUDART_INF, best_sigma = 0.0;
-  for (int m = 0; m < 3; ++m) {
+  int best = -1, tier = 0;
+  for (int m = 0; m < 3 && best < 0; ++m) {
     const Cand &L = C[2 * m], &R = C[2 * m + 1];
-    if (L.raw < best_raw) { best_raw = L.raw; best_sigma = L.sigma; }
-    if (R.raw < best_raw) { best_raw = R.raw; best_sigma = R.sigma; }
-    if (isfinite(L.raw) || isfinite(R.raw)) {
-      bool useL = L.raw <= R.raw;
-      if ((useL ? L.raw : R.raw) <= 8.0 * spd) {
-        sigma_out[c] = useL ? L.sigma : R.sigma; tier_out[c] = 0; return;
-      }
-      bool wuseL = L.wgt <= R.wgt;
-      if ((wuseL ? L.wgt : R.wgt) <= 64.0 * spd) {
-        sigma_out[c] = wuseL ? L.sigma : R.sigma; tier_out[c] = 1; return;
-      }
-    }
+    if (fmin(L.raw, R.raw) <= 8.0 * spd) { best = L.raw <= R.raw ? 2 * m : 2 * m + 1; tier = 0; break; }
+    for (int k = 2 * m; k <= 2 * m + 1; ++k)
+      if (isfinite(C[k].raw) && C[k].wgt <= 64.0 * spd && (best < 0 || C[k].raw < C[best].raw)) best = k;
+    tier = 1;
   }
-  if (best_raw <= 1e8 * spd) { sigma_out[c] = best_sigma; tier_out[c] = 3; return; }
-  sigma_out[c] = 0.0;
-  tier_out[c] = 4;
-  fail[0] = 1;
+  if (best < 0) {
+    for (int k = 0; k < 6; ++k)
+      if (best < 0 || C[k].raw < C[best].raw) best = k;
+    tier = 3;
+    if (!(C[best].raw <= 1e8 * spd)) best = -1;
+  }
+  if (best < 0) {
+    sigma_out[c] = 0.0;
+    tier_out[c] = 4;
+    fail[0] = 1;
+    return;
+  }
+  sigma_out[c] = C[best].sigma;
+  tier_out[c] = tier;
 }
 
 // Accepted child, pass 1 (one thread per cluster): projective chain, storing

@@ -325,6 +325,8 @@ struct VecArgs {
   int mode;                  // 0 = RQC + normalised Z column, 1 = one pass to zbuf
   double rtol_fallback;
   unsigned long long *ctr;   // [0] factorizations, [1] fallbacks, [2] nudges
+  int *task_info;            // optional: per task (iterations | fallback << 8)
+  int trace_task;            // task id whose RQC trajectory is printed (-1: none)
 };
 
 __device__ __forceinline__ void vectors_body(const VecArgs &A) {
@@ -379,9 +381,13 @@ __device__ __forceinline__ void vectors_body(const VecArgs &A) {
   }
   bool converged = false;
   int it = 1;
+  const bool trace = tix == A.trace_task;
   for (;;) {
     if (tw.negc >= j) { if (lam < hi) hi = lam; } else { if (lam > lo) lo = lam; }
     double delta = tw.gamma / tw.nrm2;
+    if (trace)
+      printf("[task %d it %d] j %d lam %.17g r %d gamma %.6e nrm2 %.6e delta %.6e negc %d lo %.17g hi %.17g ok %d\n",
+             tix, it, j, lam, tw.r, tw.gamma, tw.nrm2, delta, tw.negc, lo, hi, (int)tw.ok);
     if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam) {
       lam_fin = lam + delta; converged = true; break;
     }
@@ -422,6 +428,7 @@ __device__ __forceinline__ void vectors_body(const VecArgs &A) {
   double sc = 1.0 / sqrt(tw.nrm2);
   twist_solve(X, lam, tw.r, sc, A.Z + tk.col * A.ldz + N.row0, 1, tix, smA, smB);
   A.lam_out[tix] = lam_fin;
+  if (A.task_info) A.task_info[tix] = it | ((int)fb << 8);
   atomicAdd(&A.ctr[0], nfact);
   if (fb) atomicAdd(&A.ctr[1], fb);
   if (nudges) atomicAdd(&A.ctr[2], nudges);

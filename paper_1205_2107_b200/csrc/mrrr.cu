@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
+#include <mutex>
 #include <numeric>
 #include <vector>
 
@@ -32,16 +34,70 @@ struct MrrrError {
   int code;
 };
 
-// Stream-ordered device allocations released at scope exit.
+// Library-owned stream-ordered memory pool per device.  Its release threshold
+// is unlimited, so workspace freed at the end of a call stays mapped for the
+// next call instead of being returned to the driver at every synchronisation
+// (the default pool's behaviour, which costs a remap of the whole workspace
+// per call).  mrrr_trim_workspace() releases it.
+cudaMemPool_t g_pools[64];
+std::mutex g_pool_mu;
+
+cudaMemPool_t lib_pool() {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[dev]) {
+    cudaMemPoolProps pr{};
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = dev;
+    CK(cudaMemPoolCreate(&g_pools[dev], &pr));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  return g_pools[dev];
+}
+
+// Debug dump of device arrays (MRRR_DUMP=<dir>): raw little-endian files.
+template <class T>
+void dump(const char *name, const T *dptr, size_t count, cudaStream_t s) {
+  const char *dir = getenv("MRRR_DUMP");
+  if (!dir || !count) return;
+  std::vector<T> h(count);
+  CK(cudaMemcpyAsync(h.data(), dptr, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  char path[512];
+  snprintf(path, sizeof path, "%s/%s", dir, name);
+  FILE *f = fopen(path, "wb");
+  if (f) { fwrite(h.data(), sizeof(T), count, f); fclose(f); }
+}
+
+// Host wall-clock trace of the phases (MRRR_TRACE=1), for overhead hunting.
+struct Trace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, tl;
+  Trace() : on(getenv("MRRR_TRACE") != nullptr) { t0 = tl = std::chrono::steady_clock::now(); }
+  void mark(const char *what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[mrrr] %-28s +%8.3f ms  (at %8.3f ms)\n", what,
+            std::chrono::duration<double, std::milli>(t - tl).count(),
+            std::chrono::duration<double, std::milli>(t - t0).count());
+    tl = t;
+  }
+};
+
+// Stream-ordered device allocations released (to the library pool) at scope exit.
 struct DevArena {
   cudaStream_t s;
+  cudaMemPool_t pool;
   std::vector<void *> ptrs;
-  explicit DevArena(cudaStream_t st) : s(st) {}
+  explicit DevArena(cudaStream_t st) : s(st), pool(lib_pool()) {}
   template <class T>
   T *alloc(size_t count) {
     void *p = nullptr;
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, s);
     if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); throw MrrrError{MRRR_ERR_NOMEM}; }
     CK(e);
     ptrs.push_back(p);
@@ -329,6 +385,7 @@ int solve(Problem &P, int64_t *m_out) {
   cudaStream_t s = P.s;
   const int64_t n = P.n;
   DevArena ar(s);
+  Trace tr;
   Timer tm(s), tall(s);
   KTimer kt_root, kt_vec;
   memset(&g_stats, 0, sizeof(g_stats));
@@ -352,6 +409,7 @@ int solve(Problem &P, int64_t *m_out) {
   const double tnrm_s = h_hdr[0] * scale;
   std::vector<int> h_brk(n);
   d2h(h_brk.data(), brk, n, s);
+  tr.mark("prep");
 
   // blocks
   std::vector<Block> hb;
@@ -487,6 +545,10 @@ int solve(Problem &P, int64_t *m_out) {
   int h_fail[4];
   d2h(h_fail, dfail, 4, s);
   if (h_fail[0]) throw MrrrError{MRRR_ERR_ROOT};
+  dump("root_DL.bin", DLroot, n, s);
+  dump("root_LDv.bin", LDv, n, s);
+  dump("root_sigma.bin", sigma_b, nblocks, s);
+  tr.mark("root rrr");
 
   // node table (device), capacity grows with levels
   int node_cap = std::max<int>(nroot + 16, 64);
@@ -622,6 +684,7 @@ int solve(Problem &P, int64_t *m_out) {
   }
   h2d(slot_out, h_slot_out.data(), nslots, s);
   *m_out = m;
+  if (tr.on) { CK(cudaStreamSynchronize(s)); tr.mark("root bisection"); }
   g_stats.ms_root = tm.stop();
 
   if (!vectors) {
@@ -640,6 +703,8 @@ int solve(Problem &P, int64_t *m_out) {
     CK(cudaMemset2DAsync(P.Z, P.ldz * sizeof(double), 0, n * sizeof(double), m, s));
 
   // ---------------- a4/a5: representation tree ----------------
+  dump("root_lo.bin", slo, nslots, s);
+  dump("root_hi.bin", shi, nslots, s);
   std::vector<int> h_active(nslots, 1);
   int *active = ar.alloc<int>(nslots);
   int *run_end = ar.alloc<int>(nslots);
@@ -664,6 +729,7 @@ int solve(Problem &P, int64_t *m_out) {
     CK(cudaGetLastError());
     g_stats.kernel_launches++;
     d2h(h_run_end.data(), run_end, nslots, s);
+    tr.mark("classify");
     std::vector<int> cl_parent, cl_s0, cl_s1;
     for (int nd : level_nodes) {
       const HostNode &H = hn[nd];
@@ -721,7 +787,7 @@ int solve(Problem &P, int64_t *m_out) {
       A.nodes = dnodes; A.blocks = dblocks; A.LDv = LDv; A.tasks = dzt; A.ntask = ntask;
       A.lo = slo; A.hi = shi; A.slot_j = slot_j; A.fck = fck; A.bck = bck;
       A.ck_stride = ntask; A.nseg_max = nseg; A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1;
-      A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 4;
+      A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 4; A.task_info = nullptr; A.trace_task = -1;
       size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
       k_zprobe<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
       CK(cudaGetLastError());
@@ -780,8 +846,26 @@ int solve(Problem &P, int64_t *m_out) {
     g_stats.kernel_launches++;
     launch_bisect(M, dnodes, dwork, (int)wv.size(), slot_j, slo, shi, P.o.rtol_class, ctr + 2, s);
     d2h(h_fail, dfail, 4, s);
+    if (getenv("MRRR_DUMP")) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "L%d_pool.bin", level); dump(nm, pool, (size_t)ncl * nbmax, s);
+      snprintf(nm, sizeof nm, "L%d_sigma.bin", level); dump(nm, dsig, ncl, s);
+      snprintf(nm, sizeof nm, "L%d_tier.bin", level); dump(nm, dtier, ncl, s);
+      snprintf(nm, sizeof nm, "L%d_s0.bin", level); dump(nm, dcl_s0, ncl, s);
+      snprintf(nm, sizeof nm, "L%d_s1.bin", level); dump(nm, dcl_s1, ncl, s);
+      snprintf(nm, sizeof nm, "L%d_parent.bin", level); dump(nm, dcl_parent, ncl, s);
+      snprintf(nm, sizeof nm, "L%d_cand.bin", level); dump(nm, cand, (size_t)6 * ncl, s);
+      snprintf(nm, sizeof nm, "L%d_zbuf.bin", level); dump(nm, zbuf, (size_t)2 * ncl * nbmax, s);
+      snprintf(nm, sizeof nm, "L%d_lo.bin", level); dump(nm, slo, nslots, s);
+      snprintf(nm, sizeof nm, "L%d_hi.bin", level); dump(nm, shi, nslots, s);
+    }
     if (h_fail[1]) throw MrrrError{MRRR_ERR_CHILD};
     if (h_fail[2]) throw MrrrError{MRRR_ERR_CONVERGE};
+    if (tr.on) {
+      char buf[96];
+      snprintf(buf, sizeof buf, "level %d: %d clusters", level, ncl);
+      tr.mark(buf);
+    }
     level_nodes.clear();
     for (int c = 0; c < ncl; ++c) level_nodes.push_back(node_base + c);
     ++level;
@@ -805,6 +889,10 @@ int solve(Problem &P, int64_t *m_out) {
     A.lo = slo; A.hi = shi; A.slot_j = slot_j; A.fck = fck; A.bck = bck;
     A.ck_stride = ntask; A.nseg_max = nseg; A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam;
     A.mode = 0; A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 8;
+    const bool dbg = getenv("MRRR_DEBUG") != nullptr;
+    int *tinfo = dbg ? ar.alloc<int>(ntask) : nullptr;
+    A.task_info = tinfo;
+    A.trace_task = getenv("MRRR_TRACE_TASK") ? atoi(getenv("MRRR_TRACE_TASK")) : -1;
     size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
     {
       std::vector<Node> hnodes(nnodes);
@@ -823,10 +911,13 @@ int solve(Problem &P, int64_t *m_out) {
       d2h(hl.data(), lam, ntask, s);
       std::vector<Node> hnodes(nnodes);
       d2h(hnodes.data(), dnodes, nnodes, s);
+      std::vector<int> hti(ntask);
+      d2h(hti.data(), tinfo, ntask, s);
       for (int t = 0; t < ntask; ++t) {
         const Node &N = hnodes[tasks[t].node];
-        fprintf(stderr, "task %d slot %d node %d col %ld lam %.17g tau %.17g + %.3g sigma %.17g depth %d\n", t,
-                tasks[t].slot, tasks[t].node, (long)tasks[t].col, hl[t], N.tau_hi, N.tau_lo, N.sigma, N.depth);
+        fprintf(stderr, "task %d slot %d node %d col %ld lam %.17g tau %.17g + %.3g sigma %.17g depth %d it %d fb %d\n", t,
+                tasks[t].slot, tasks[t].node, (long)tasks[t].col, hl[t], N.tau_hi, N.tau_lo, N.sigma, N.depth,
+                hti[t] & 255, hti[t] >> 8);
       }
     }
     k_output<<<(ntask + 255) / 256, 256, 0, s>>>(dt, ntask, dnodes, lam, 1.0 / scale, P.w);
@@ -836,6 +927,7 @@ int solve(Problem &P, int64_t *m_out) {
     g_stats.kernel_launches += 3;
   }
   d2h(h_ctr, ctr, 16, s);
+  tr.mark("vectors");
   g_stats.ms_vectors = tv.stop();
   g_stats.root_sweeps += h_ctr[0];
   g_stats.safe_resweeps = h_ctr[1];
@@ -913,8 +1005,12 @@ int mrrr_stemr(int64_t n, const double *d, const double *e, int range, double vl
       CK(cudaStreamSynchronize(P.s));
       return 0;
     }
+    auto t0 = std::chrono::steady_clock::now();
     int rc = solve(P, m);
     CK(cudaStreamSynchronize(P.s));
+    if (getenv("MRRR_TRACE"))
+      fprintf(stderr, "[mrrr] call total (wall)         %8.3f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     return rc;
   } catch (const MrrrError &er) {
     cudaStreamSynchronize(P.s);
@@ -973,6 +1069,13 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, doub
   (void)nranks; (void)allgather; (void)allgather_ctx; (void)m; (void)opts; (void)col_begin;
   (void)m_local; (void)w_all; (void)Z_local; (void)ldz; (void)stream;
   return MRRR_ERR_COMM;  // implemented in a later milestone
+}
+
+int mrrr_trim_workspace(void) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (auto &p : g_pools)
+    if (p && cudaMemPoolTrimTo(p, 0) != cudaSuccess) return MRRR_ERR_CUDA;
+  return 0;
 }
 
 size_t mrrr_workspace_bytes(int64_t n, int64_t k) {

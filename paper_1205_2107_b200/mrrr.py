@@ -78,6 +78,7 @@ def lib():
         L.mrrr_get_stats.argtypes = [C.POINTER(Stats)]
         L.mrrr_get_stats.restype = C.c_int
         L.mrrr_version.restype = C.c_char_p
+        L.mrrr_trim_workspace.restype = C.c_int
         _lib = L
     return _lib
 
@@ -180,6 +181,13 @@ def stemr_raw(n, d, e, rng, vl, vu, il, iu, m_ok=True, w=None, Z=None, ldz=None)
                             C.byref(m) if m_ok else C.cast(None, C.POINTER(C.c_int64)),
                             _ptr(w), _ptr(Z), ldz if ldz is not None else max(n, 1),
                             C.c_void_p(0), None)
+
+
+def trim_workspace() -> None:
+    """Release the library's cached device workspace (mrrr_trim_workspace)."""
+    rc = lib().mrrr_trim_workspace()
+    if rc != 0:
+        raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
 
 
 def version() -> str:

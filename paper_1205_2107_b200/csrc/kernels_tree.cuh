@@ -139,10 +139,11 @@ __global__ void k_root_chain(const double *__restrict__ ds, const double *__rest
     double sigma = B.side > 0 ? B.gl - delta : B.gu + delta;
     double tm1 = 1.0, tm2 = 0.0;
     bool ok = true;
-    for (int i = 0; i < B.nb; ++i) {
-      int64_t gi = B.row0 + i;
-      double b2 = i > 0 ? es2[gi - 1] : 0.0;
-      double t = fma(ds[gi] - sigma, tm1, -b2 * tm2);
+    const double *dr = ds + B.row0;
+    const double *er = es2 + B.row0;  // er[i-1] = e_{i-1}^2 of the block
+    auto row = [&](int i, double di, double b2) {
+      const int64_t gi = B.row0 + i;
+      double t = fma(di - sigma, tm1, -b2 * tm2);
       // definite: D_i = t_i / t_{i-1} has the sign of the side
       bool good = (t != 0.0) && ((B.side > 0) ? (negbit(t, tm1) == 0) : (negbit(t, tm1) == 1));
       ok &= good && isfinite(t);
@@ -157,6 +158,21 @@ __global__ void k_root_chain(const double *__restrict__ ds, const double *__rest
         tm1 *= f; tm2 *= f;
       }
       sbuf[gi] = sh;
+    };
+    // rows prefetched one group ahead (in-order issue: a load's first use stalls)
+    constexpr int G = 8;
+    double dc[G], dn[G], ec[G], en[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k)
+      if (k < B.nb) { dc[k] = __ldg(&dr[k]); ec[k] = k > 0 ? __ldg(&er[k - 1]) : 0.0; }
+    for (int i = 0; i < B.nb; i += G) {
+#pragma unroll
+      for (int k = 0; k < G; ++k)
+        if (i + G + k < B.nb) { dn[k] = __ldg(&dr[i + G + k]); en[k] = __ldg(&er[i + G + k - 1]); }
+#pragma unroll
+      for (int k = 0; k < G; ++k) if (i + k < B.nb) row(i + k, dc[k], ec[k]);
+#pragma unroll
+      for (int k = 0; k < G; ++k) { dc[k] = dn[k]; ec[k] = en[k]; }
     }
     if (ok) { sigma_out[b] = sigma; return; }
     delta *= 2.0;
@@ -468,19 +484,15 @@ __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0
   const double *zr = zbuf ? zbuf + (int64_t)(2 * c + 1) * zstride : nullptr;
   double p = -sigma, q = 1.0, g = 0.0, nl = 0.0, dnl = 0.0, nr = 0.0, dnr = 0.0;
   bool fin = true;
-  int nb = P.nb;
-  for (int i = 0; i < nb; ++i) {
-    double2 v = __ldg(&DL[i]);
+  const int nb = P.nb;
+  auto row = [&](int i, const double2 &v, double a, double b) {
     double t = fma(v.x, q, p);
     double dp = t / q;  // D+_i (off the recurrence chain)
     fin &= isfinite(dp) && dp != 0.0;
     double adp = fabs(dp);
     g = fmax(g, adp);
-    if (zl) {
-      double a = zl[i], b = zr[i];
-      nl = fma(adp, a * a, nl); dnl = fma(a, a, dnl);
-      nr = fma(adp, b * b, nr); dnr = fma(b, b, dnr);
-    }
+    nl = fma(adp, a * a, nl); dnl = fma(a, a, dnl);
+    nr = fma(adp, b * b, nr); dnr = fma(b, b, dnr);
     if (i < nb - 1) { p = fma(-sigma, t, v.y * p); q = t; }
     if ((i & 7) == 7) {
       int ee = max_exp(p, q);
@@ -488,6 +500,28 @@ __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0
       double f = pow2_scale(min(ee, 2045));
       p *= f; q *= f;
     }
+  };
+  if (zl) {
+    // rows and both probe vectors prefetched one group ahead
+    constexpr int G = 4;
+    double2 vc[G], vn[G];
+    double ac[G], an[G], bc[G], bn[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k)
+      if (k < nb) { vc[k] = __ldg(&DL[k]); ac[k] = __ldg(&zl[k]); bc[k] = __ldg(&zr[k]); }
+    for (int i = 0; i < nb; i += G) {
+#pragma unroll
+      for (int k = 0; k < G; ++k)
+        if (i + G + k < nb) {
+          vn[k] = __ldg(&DL[i + G + k]); an[k] = __ldg(&zl[i + G + k]); bn[k] = __ldg(&zr[i + G + k]);
+        }
+#pragma unroll
+      for (int k = 0; k < G; ++k) if (i + k < nb) row(i + k, vc[k], ac[k], bc[k]);
+#pragma unroll
+      for (int k = 0; k < G; ++k) { vc[k] = vn[k]; ac[k] = an[k]; bc[k] = bn[k]; }
+    }
+  } else {
+    stream_rows<8>(DL, 0, nb, [&](int i, const double2 &v) { row(i, v, 0.0, 0.0); });
   }
   Cand C;
   C.sigma = sigma;
@@ -544,9 +578,8 @@ __global__ void k_child_chain(const Node *nodes, const int *cl_parent, const dou
   double p = -sg, q = 1.0;
   double *tb = tbuf + (int64_t)c * stride;
   int *sb = sbuf + (int64_t)c * stride;
-  int nb = P.nb;
-  for (int i = 0; i < nb; ++i) {
-    double2 v = __ldg(&P.DL[i]);
+  const int nb = P.nb;
+  stream_rows<8>(P.DL, 0, nb, [&](int i, const double2 &v) {
     double t = fma(v.x, q, p);
     tb[i] = t;
     int sh = 0;
@@ -561,7 +594,7 @@ __global__ void k_child_chain(const Node *nodes, const int *cl_parent, const dou
       }
     }
     sb[i] = sh;
-  }
+  });
 }
 
 // Accepted child, pass 2 (parallel over clusters x rows): D+_i = t_i / t_{i-1}

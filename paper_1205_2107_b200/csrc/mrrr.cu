@@ -18,6 +18,63 @@
 
 using namespace mrrr;
 
+namespace mrrr {
+// Deferred O10 fallback: one CTA per failing eigenpair refines its bracket
+// [lo, hi] (node coordinates) to rtol relative by multisection with
+// blockDim.x * M shifts per round, one node sweep per round (rows staged in
+// shared memory by cta_sweep).  Invariant N(lo) < j <= N(hi).
+template <int M>
+__global__ void __launch_bounds__(128) k_fallback_bisect(const Node *nodes, const VecTask *tasks,
+                                                         const int *list, const int *slot_j,
+                                                         double *lo_arr, double *hi_arr, double rtol,
+                                                         unsigned long long *safe_ctr) {
+  __shared__ double2 sm[2 * kTile];
+  __shared__ double red_lo[32], red_hi[32];
+  const VecTask tk = tasks[list[blockIdx.x]];
+  const Node N = nodes[tk.node];
+  const int j = slot_j[tk.slot];
+  double lo = lo_arr[tk.slot], hi = hi_arr[tk.slot];
+  const int S = blockDim.x * M;
+  for (int round = 0; round < 64; ++round) {
+    const double mid = 0.5 * (lo + hi);
+    if (hi - lo <= rtol * fmax(fabs(lo), fabs(hi)) || !(mid > lo && mid < hi)) break;
+    double mu[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c)
+      mu[c] = lo + (hi - lo) * ((double)(threadIdx.x * M + c + 1) / (double)(S + 1));
+    unsigned k[M];
+    bool ok;
+    cta_sweep<M>(N.DL, N.nb, sm, mu, k, ok);
+    if (!ok) {
+      atomicAdd(safe_ctr, 1ull);
+#pragma unroll
+      for (int c = 0; c < M; ++c) k[c] = negcount_qd_safe(N.DL, N.nb, mu[c]);
+    }
+    double nlo = lo, nhi = hi;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      if ((int)k[c] < j) nlo = fmax(nlo, mu[c]);
+      else nhi = fmin(nhi, mu[c]);
+    }
+    for (int o = 16; o; o >>= 1) {
+      nlo = fmax(nlo, __shfl_xor_sync(0xffffffff, nlo, o));
+      nhi = fmin(nhi, __shfl_xor_sync(0xffffffff, nhi, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { red_lo[w] = nlo; red_hi[w] = nhi; }
+    __syncthreads();
+    nlo = lo; nhi = hi;
+    for (int x = 0; x < (int)(blockDim.x >> 5); ++x) { nlo = fmax(nlo, red_lo[x]); nhi = fmin(nhi, red_hi[x]); }
+    __syncthreads();
+    if (nhi <= nlo) nhi = hi;  // non-monotone counts: keep the old upper end
+    const bool progress = nlo != lo || nhi != hi;
+    lo = nlo; hi = nhi;
+    if (!progress) break;  // the grid no longer resolves [lo, hi] (ulp level)
+  }
+  if (threadIdx.x == 0) { lo_arr[tk.slot] = lo; hi_arr[tk.slot] = hi; }
+}
+}  // namespace mrrr
+
 namespace {
 
 thread_local mrrr_stats_t g_stats;
@@ -787,7 +844,7 @@ int solve(Problem &P, int64_t *m_out) {
       A.nodes = dnodes; A.blocks = dblocks; A.LDv = LDv; A.tasks = dzt; A.ntask = ntask;
       A.lo = slo; A.hi = shi; A.slot_j = slot_j; A.fck = fck; A.bck = bck;
       A.ck_stride = ntask; A.nseg_max = nseg; A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1;
-      A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 4; A.task_info = nullptr; A.trace_task = -1;
+      A.ctr = ctr + 4; A.task_info = nullptr; A.trace_task = -1;
       size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
       k_zprobe<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
       CK(cudaGetLastError());
@@ -888,7 +945,10 @@ int solve(Problem &P, int64_t *m_out) {
     A.nodes = dnodes; A.blocks = dblocks; A.LDv = LDv; A.tasks = dt; A.ntask = ntask;
     A.lo = slo; A.hi = shi; A.slot_j = slot_j; A.fck = fck; A.bck = bck;
     A.ck_stride = ntask; A.nseg_max = nseg; A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam;
-    A.mode = 0; A.rtol_fallback = 4.0 * kEps; A.ctr = ctr + 8;
+    A.mode = 0; A.ctr = ctr + 8;
+    int *fail_list = ar.alloc<int>(ntask), *fail_count = ar.alloc<int>(1);
+    CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
+    A.fail_list = fail_list; A.fail_count = fail_count;
     const bool dbg = getenv("MRRR_DEBUG") != nullptr;
     int *tinfo = dbg ? ar.alloc<int>(ntask) : nullptr;
     A.task_info = tinfo;
@@ -906,6 +966,21 @@ int solve(Problem &P, int64_t *m_out) {
     k_vectors<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
     kt_vec.stop(s);
     CK(cudaGetLastError());
+    g_stats.kernel_launches++;
+    // deferred O10 fallback: CTA-parallel multisection to 4 eps, then one
+    // factorization at the midpoint (mode 2)
+    int h_nfail = 0;
+    d2h(&h_nfail, fail_count, 1, s);
+    if (h_nfail > 0) {
+      k_fallback_bisect<4><<<h_nfail, 128, 0, s>>>(dnodes, dt, fail_list, slot_j, slo, shi,
+                                                   4.0 * kEps, ctr + 1);
+      CK(cudaGetLastError());
+      VecArgs B2 = A;
+      B2.mode = 2; B2.task_list = fail_list; B2.ntask = h_nfail; B2.task_info = nullptr;
+      k_vectors<<<(h_nfail + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(B2);
+      CK(cudaGetLastError());
+      g_stats.kernel_launches += 2;
+    }
     if (getenv("MRRR_DEBUG")) {
       std::vector<double> hl(ntask);
       d2h(hl.data(), lam, ntask, s);
@@ -924,7 +999,7 @@ int solve(Problem &P, int64_t *m_out) {
     CK(cudaGetLastError());
     if (m > 1) k_monotone<<<1, 1024, 0, s>>>(P.w, (int)m);
     CK(cudaGetLastError());
-    g_stats.kernel_launches += 3;
+    g_stats.kernel_launches += 2;
   }
   d2h(h_ctr, ctr, 16, s);
   tr.mark("vectors");
@@ -1036,10 +1111,12 @@ int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range, doub
   };
   cudaError_t ce = cudaSuccess;
   do {
-    if ((ce = cudaMallocAsync((void **)&dd, n * sizeof(double), s))) break;
-    if ((ce = cudaMallocAsync((void **)&de, std::max<int64_t>(n - 1, 1) * sizeof(double), s))) break;
-    if ((ce = cudaMallocAsync((void **)&dw, k * sizeof(double), s))) break;
-    if (Z && (ce = cudaMallocAsync((void **)&dZ, (size_t)n * k * sizeof(double), s))) break;
+    cudaMemPool_t pool;
+    try { pool = lib_pool(); } catch (const CudaError &er) { ce = er.e; break; }
+    if ((ce = cudaMallocFromPoolAsync((void **)&dd, n * sizeof(double), pool, s))) break;
+    if ((ce = cudaMallocFromPoolAsync((void **)&de, std::max<int64_t>(n - 1, 1) * sizeof(double), pool, s))) break;
+    if ((ce = cudaMallocFromPoolAsync((void **)&dw, k * sizeof(double), pool, s))) break;
+    if (Z && (ce = cudaMallocFromPoolAsync((void **)&dZ, (size_t)n * k * sizeof(double), pool, s))) break;
     if ((ce = cudaMemcpyAsync(dd, d, n * sizeof(double), cudaMemcpyHostToDevice, s))) break;
     if (n > 1 && (ce = cudaMemcpyAsync(de, e, (n - 1) * sizeof(double), cudaMemcpyHostToDevice, s)))
       break;

@@ -175,6 +175,7 @@ typedef struct {
   double ms_k_vectors;      /* singleton RQC + twisted + Z kernel */
   int64_t vec_tasks;        /* eigenvectors computed by that kernel */
   int64_t vec_elems;        /* sum over those tasks of their block order */
+  double ms_k_final_refine; /* singleton brackets to 2^-40 before the vectors */
 } mrrr_stats_t;
 int mrrr_get_stats(mrrr_stats_t *out);
 

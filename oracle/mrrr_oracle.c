@@ -384,16 +384,22 @@ static void two_sum(double a, double b, double *s, double *err) {
 }
 
 /* O10 -- singleton vector by Rayleigh-quotient correction on twisted
- * factorizations (readings 10, 24, 25). */
+ * factorizations (readings 10, 24, 25).
+ * Reading 10 (amended): the bracket is first refined by bisection to relative
+ * width 2^-40 (high relative accuracy), so that the RQC
+ * converges in two factorizations for nearly every eigenpair. */
+#define ORACLE_RTOL_VEC 0x1p-40
+#define ORACLE_RQC_MAX 3 /* factorizations before the bisection fallback (reading 10) */
 static void singleton(ctx_t *c, const rrr_t *R, int64_t j) {
   int64_t nb = R->nb;
   double lo = c->lo[j], hi = c->hi[j];
+  bisect(c, R, j, ORACLE_RTOL_VEC, &lo, &hi);
   double lam = 0.5 * (lo + hi), lam_fin = lam;
   int64_t r, nc, nfact = 0;
   double gamma, nrm2 = 1;
   int converged = 0, rs = 0;
   double *z = c->z;
-  for (int it = 0; it < 10; ++it) {
+  for (int it = 0; it < ORACLE_RQC_MAX; ++it) {
     twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lam, R->pivmin, &c->ws, z, &r,
                &gamma, &nc, &rs);
     nfact++;

@@ -159,21 +159,34 @@ __global__ void k_root_chain(const double *__restrict__ ds, const double *__rest
       }
       sbuf[gi] = sh;
     };
-    // rows prefetched one group ahead (in-order issue: a load's first use stalls)
+    // rows prefetched one group ahead, ping-pong buffers (in-order issue: a
+    // load's first use stalls)
     constexpr int G = 8;
-    double dc[G], dn[G], ec[G], en[G];
+    const int ng = B.nb / G;
+    double dx[G], dy[G], ex[G], ey[G];
+    auto ld = [&](int i, double (&dd)[G], double (&ee)[G]) {
 #pragma unroll
-    for (int k = 0; k < G; ++k)
-      if (k < B.nb) { dc[k] = __ldg(&dr[k]); ec[k] = k > 0 ? __ldg(&er[k - 1]) : 0.0; }
-    for (int i = 0; i < B.nb; i += G) {
+      for (int k = 0; k < G; ++k) { dd[k] = __ldg(&dr[i + k]); ee[k] = (i + k > 0) ? __ldg(&er[i + k - 1]) : 0.0; }
+    };
+    int m = 0;
+    if (ng > 0) {
+      ld(0, dx, ex);
+      for (; m + 1 < ng; m += 2) {
+        const int i = G * m;
+        if (i + kPfDist < B.nb) { prefetch_l2(&dr[i + kPfDist]); prefetch_l2(&er[i + kPfDist]); }
+        ld(i + G, dy, ey);
 #pragma unroll
-      for (int k = 0; k < G; ++k)
-        if (i + G + k < B.nb) { dn[k] = __ldg(&dr[i + G + k]); en[k] = __ldg(&er[i + G + k - 1]); }
+        for (int k = 0; k < G; ++k) row(i + k, dx[k], ex[k]);
+        if (m + 2 < ng) ld(i + 2 * G, dx, ex);
 #pragma unroll
-      for (int k = 0; k < G; ++k) if (i + k < B.nb) row(i + k, dc[k], ec[k]);
+        for (int k = 0; k < G; ++k) row(i + G + k, dy[k], ey[k]);
+      }
+      if (m < ng) {
 #pragma unroll
-      for (int k = 0; k < G; ++k) { dc[k] = dn[k]; ec[k] = en[k]; }
+        for (int k = 0; k < G; ++k) row(G * m + k, dx[k], ex[k]);
+      }
     }
+    for (int i = G * ng; i < B.nb; ++i) row(i, __ldg(&dr[i]), i > 0 ? __ldg(&er[i - 1]) : 0.0);
     if (ok) { sigma_out[b] = sigma; return; }
     delta *= 2.0;
   }
@@ -282,6 +295,46 @@ __device__ void cta_sweep(const double2 *__restrict__ DL, int nb, double2 *sm, c
   }
 }
 
+// As cta_sweep, but a warp whose lanes carry no shift (`work` false for the
+// whole warp) only helps stage the tiles and skips the arithmetic.
+template <int M>
+__device__ void cta_sweep_masked(const double2 *__restrict__ DL, int nb, double2 *sm,
+                                 const double (&mu)[M], unsigned (&cnt)[M], bool &ok, bool work) {
+  Sturm s[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) sturm_init(s[c], mu[c]);
+  ok = true;
+  const int body = nb - 1;
+  const int ntiles = (body + kTile - 1) / kTile;
+  auto load = [&](int tile, int buf) {
+    int base = tile * kTile;
+    int rows = min(kTile, body - base);
+    for (int r = threadIdx.x; r < rows; r += blockDim.x)
+      __pipeline_memcpy_async(&sm[buf * kTile + r], &DL[base + r], sizeof(double2));
+    __pipeline_commit();
+  };
+  if (ntiles > 0) load(0, 0);
+  for (int tile = 0; tile < ntiles; ++tile) {
+    int buf = tile & 1;
+    if (tile + 1 < ntiles) {
+      load(tile + 1, buf ^ 1);
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
+    }
+    __syncthreads();
+    if (work) tile_steps<M>(sm + buf * kTile, min(kTile, body - tile * kTile), mu, s, ok);
+    __syncthreads();
+  }
+  double Dl = __ldg(&DL[nb - 1]).x;
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    sturm_last(s[c], Dl);
+    ok &= sturm_ok(s[c]);
+    cnt[c] = s[c].c;
+  }
+}
+
 // ===========================================================================
 // Work item of the bisection kernels: a chunk of slots of one node.
 struct Work {
@@ -371,6 +424,158 @@ __global__ void __launch_bounds__(128) k_bisect(const Node *nodes, const Work *w
   }
   if (threadIdx.x == 0) atomicAdd(sweeps, (unsigned long long)rounds * M * (W.s1 - W.s0));
   if (mine) { lo_arr[s] = lo; hi_arr[s] = hi; }
+}
+
+// a3/a5 -- adaptive multisection (replaces k_bisect + k_verify on the hot
+// path).  One CTA owns up to kRefMax member slots of one node.  Each round the
+// CTA sweeps the node once with blockDim.x * M shifts, spread evenly over the
+// members that have not converged yet: with a active members each gets
+// P = floor(blockDim.x * M / a) shifts, i.e. log2(P + 1) bits per round
+// (a lone eigenvalue gains 9 bits per sweep instead of 2.3).  Work item
+// slots are W.s0 .. W.s1-1, or slot_list[W.s0 .. W.s1-1] when a list is given.  Counts go to
+// shared memory; member i's owner thread then narrows [lo, hi] to the
+// neighbouring grid points around index j (invariant N(lo) < j <= N(hi)).
+// With `verify` set (child coordinates, O9.4) the member's grid first
+// includes both ends; an end that does not bracket j is widened by doubling
+// its offset from the translated parent interval (plo - wl, phi + wu) and the
+// member is narrowed only once both ends bracket j.
+// Stop: hi - lo <= rtol * max(|lo|, |hi|) or no double strictly inside.
+constexpr int kRefMax = 128;
+constexpr int kPmax = 16;
+
+template <int M>
+__global__ void __launch_bounds__(128) k_refine(const Node *nodes, const Work *work,
+                                                const int *__restrict__ slot_list,
+                                                const int *__restrict__ slot_j, double *lo_arr,
+                                                double *hi_arr, const double *wlo_arr,
+                                                const double *whi_arr, int verify, double rtol,
+                                                int max_rounds, int *fail,
+                                                unsigned long long *sweeps,
+                                                unsigned long long *safe_ctr) {
+  __shared__ double2 sm[2 * kTile];
+  __shared__ double m_lo[kRefMax], m_hi[kRefMax], m_wl[kRefMax], m_wu[kRefMax];
+  __shared__ double m_plo[kRefMax], m_phi[kRefMax];
+  __shared__ int m_j[kRefMax], m_state[kRefMax];  // state: 0 unverified, 1 verified, 2 done
+  __shared__ int act[kRefMax];                     // active member ids, compacted
+  __shared__ int cnt[128 * M];
+  __shared__ int s_na;
+  const Work W = work[blockIdx.x];
+  const Node N = nodes[W.node];
+  const int nm = W.s1 - W.s0;
+  const int tid = threadIdx.x, T = blockDim.x, S = T * M;
+  auto conv = [&](double a, double b) {
+    double m = 0.5 * (a + b);
+    return (b - a <= rtol * fmax(fabs(a), fabs(b))) || !(m > a && m < b);
+  };
+  for (int i = tid; i < nm; i += T) {
+    const int sl = slot_list ? slot_list[W.s0 + i] : W.s0 + i;
+    m_j[i] = slot_j[sl];
+    if (verify) {
+      m_plo[i] = lo_arr[sl]; m_phi[i] = hi_arr[sl];
+      m_wl[i] = wlo_arr[sl]; m_wu[i] = whi_arr[sl];
+      m_lo[i] = m_plo[i] - m_wl[i]; m_hi[i] = m_phi[i] + m_wu[i];
+      m_state[i] = 0;
+    } else {
+      m_lo[i] = lo_arr[sl]; m_hi[i] = hi_arr[sl];
+      m_state[i] = conv(m_lo[i], m_hi[i]) ? 2 : 1;
+    }
+  }
+  __syncthreads();
+  int rounds = 0;
+  for (; rounds < max_rounds; ++rounds) {
+    // compact the active members (warp 0; nm <= 128)
+    if (tid < 32) {
+      int base = 0;
+      for (int c0 = 0; c0 < nm; c0 += 32) {
+        const int i = c0 + tid;
+        const bool a = i < nm && m_state[i] != 2;
+        const unsigned b = __ballot_sync(0xffffffffu, a);
+        if (a) act[base + __popc(b & ((1u << tid) - 1u))] = i;
+        base += __popc(b);
+      }
+      if (tid == 0) s_na = base;
+    }
+    __syncthreads();
+    const int na = s_na;
+    if (na == 0) break;
+    // shifts per member: all of the CTA's, up to kPmax (log2(P+1) bits per
+    // round; beyond 16 shifts the bits per chain fall below 1/4)
+    const int P = min(S / na, kPmax);  // >= M
+    double mu[M];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const int f = tid * M + c;
+      const int ai = f / P, sub = f - ai * P;
+      mu[c] = 0.0;
+      if (ai < na) {
+        const int i = act[ai];
+        const double lo = m_lo[i], hi = m_hi[i];
+        // unverified: P points over [lo, hi] inclusive; verified: interior
+        mu[c] = (m_state[i] == 0) ? lo + (hi - lo) * ((double)sub / (double)(P - 1))
+                                  : lo + (hi - lo) * ((double)(sub + 1) / (double)(P + 1));
+        if (m_state[i] == 0 && sub == P - 1) mu[c] = hi;
+        any = true;
+      }
+    }
+    unsigned k[M];
+    bool ok;
+    cta_sweep_masked<M>(N.DL, N.nb, sm, mu, k, ok, __any_sync(0xffffffffu, any));
+    if (!ok && any) {
+      atomicAdd(safe_ctr, 1ull);
+#pragma unroll
+      for (int c = 0; c < M; ++c) k[c] = negcount_qd_safe(N.DL, N.nb, mu[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < M; ++c) cnt[tid * M + c] = (int)k[c];
+    __syncthreads();
+    // owners update their member
+    for (int ai = tid; ai < na; ai += T) {
+      const int i = act[ai];
+      const int j = m_j[i];
+      const int *cc = cnt + ai * P;
+      double lo = m_lo[i], hi = m_hi[i];
+      int st = m_state[i];
+      if (st == 0) {
+        const bool okl = cc[0] <= j - 1, oku = cc[P - 1] >= j;
+        if (!okl) { m_wl[i] *= 2.0; lo = m_plo[i] - m_wl[i]; }
+        if (!oku) { m_wu[i] *= 2.0; hi = m_phi[i] + m_wu[i]; }
+        if (okl && oku) {
+          st = 1;
+          double nlo = lo, nhi = hi;
+          for (int q = 1; q < P - 1; ++q) {
+            const double x = lo + (hi - lo) * ((double)q / (double)(P - 1));
+            if (cc[q] < j) nlo = fmax(nlo, x);
+          }
+          for (int q = P - 2; q >= 1; --q) {
+            const double x = lo + (hi - lo) * ((double)q / (double)(P - 1));
+            if (cc[q] >= j && x > nlo) nhi = fmin(nhi, x);
+          }
+          lo = nlo; hi = nhi;
+        }
+      } else {
+        double nlo = lo, nhi = hi;
+        for (int q = 0; q < P; ++q) {
+          const double x = lo + (hi - lo) * ((double)(q + 1) / (double)(P + 1));
+          if (cc[q] < j) nlo = fmax(nlo, x);
+        }
+        for (int q = P - 1; q >= 0; --q) {
+          const double x = lo + (hi - lo) * ((double)(q + 1) / (double)(P + 1));
+          if (cc[q] >= j && x > nlo) nhi = fmin(nhi, x);
+        }
+        lo = nlo; hi = nhi;
+      }
+      if (st == 1 && conv(lo, hi)) st = 2;
+      m_lo[i] = lo; m_hi[i] = hi; m_state[i] = st;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) atomicAdd(sweeps, (unsigned long long)rounds * S);
+  for (int i = tid; i < nm; i += T) {
+    const int sl = slot_list ? slot_list[W.s0 + i] : W.s0 + i;
+    lo_arr[sl] = m_lo[i]; hi_arr[sl] = m_hi[i];
+    if (m_state[i] != 2) fail[0] = 1;
+  }
 }
 
 // a5 -- bracket verification in child coordinates (O9.4): counts at lo and
@@ -502,24 +707,37 @@ __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0
     }
   };
   if (zl) {
-    // rows and both probe vectors prefetched one group ahead
+    // rows and both probe vectors prefetched one group ahead (ping-pong)
     constexpr int G = 4;
-    double2 vc[G], vn[G];
-    double ac[G], an[G], bc[G], bn[G];
+    const int ng = nb / G;
+    double2 vx[G], vy[G];
+    double ax[G], ay[G], bx[G], by[G];
+    auto ld = [&](int i, double2 (&v)[G], double (&a)[G], double (&b)[G]) {
 #pragma unroll
-    for (int k = 0; k < G; ++k)
-      if (k < nb) { vc[k] = __ldg(&DL[k]); ac[k] = __ldg(&zl[k]); bc[k] = __ldg(&zr[k]); }
-    for (int i = 0; i < nb; i += G) {
-#pragma unroll
-      for (int k = 0; k < G; ++k)
-        if (i + G + k < nb) {
-          vn[k] = __ldg(&DL[i + G + k]); an[k] = __ldg(&zl[i + G + k]); bn[k] = __ldg(&zr[i + G + k]);
+      for (int k = 0; k < G; ++k) { v[k] = __ldg(&DL[i + k]); a[k] = __ldg(&zl[i + k]); b[k] = __ldg(&zr[i + k]); }
+    };
+    int m = 0;
+    if (ng > 0) {
+      ld(0, vx, ax, bx);
+      for (; m + 1 < ng; m += 2) {
+        const int i = G * m;
+        if (i + kPfDist < nb) {
+          prefetch_l2(&DL[i + kPfDist]);
+          if ((i & 15) == 0) { prefetch_l2(&zl[i + kPfDist]); prefetch_l2(&zr[i + kPfDist]); }
         }
+        ld(i + G, vy, ay, by);
 #pragma unroll
-      for (int k = 0; k < G; ++k) if (i + k < nb) row(i + k, vc[k], ac[k], bc[k]);
+        for (int k = 0; k < G; ++k) row(i + k, vx[k], ax[k], bx[k]);
+        if (m + 2 < ng) ld(i + 2 * G, vx, ax, bx);
 #pragma unroll
-      for (int k = 0; k < G; ++k) { vc[k] = vn[k]; ac[k] = an[k]; bc[k] = bn[k]; }
+        for (int k = 0; k < G; ++k) row(i + G + k, vy[k], ay[k], by[k]);
+      }
+      if (m < ng) {
+#pragma unroll
+        for (int k = 0; k < G; ++k) row(G * m + k, vx[k], ax[k], bx[k]);
+      }
     }
+    for (int i = G * ng; i < nb; ++i) row(i, __ldg(&DL[i]), __ldg(&zl[i]), __ldg(&zr[i]));
   } else {
     stream_rows<8>(DL, 0, nb, [&](int i, const double2 &v) { row(i, v, 0.0, 0.0); });
   }

@@ -1,0 +1,443 @@
+// kernels_warp.cuh -- a6 (and the a5 probes): twisted factorizations and
+// eigenvector solves in WARP LOCKSTEP.  One warp owns up to 32 eigenpairs of
+// ONE node (one lane each).  All lanes walk the node's rows in the same
+// order, so the rows are staged once per warp through a shared-memory ring of
+// 32-row tiles filled by cp.async (LDGSTS) kRing-1 tiles ahead, and read back
+// as broadcasts.  Measured on B200 (tools/ubench_chain.cu): a dependent
+// projective sweep costs 37 cycles/row from such tiles against 72-80 from
+// global memory with register prefetch, and 26.5 with rows in registers.
+//
+// Arithmetic is that of kernels_vec.cuh: projective
+// stationary/progressive transforms, twist by cross-multiplied |gamma|,
+// running partial norms H/K, checkpoints every kTR rows with replay of the
+// forward segment during the backward sweep.  The eigenvector z of each lane
+// is formed per segment in shared memory and written to its column with
+// 256-byte coalesced stores (lane j's chunk by the whole warp).
+#pragma once
+#include <cuda_pipeline.h>
+
+#include "kernels_vec.cuh"
+
+namespace mrrr {
+
+constexpr int kTR = 16;          // rows per tile (= checkpoint segment)
+constexpr int kRing = 6;         // tiles in flight per warp
+constexpr int kWarpsPerCta = 2;  // independent warps per CTA
+static_assert(kTR == kSeg, "tiles and checkpoint segments coincide");
+
+// Shared memory of one warp.
+struct WarpSmem {
+  double2 rDL[kRing][kTR];  // (D, LLD) rows
+  double2 rLD[kRing][kTR];  // (LD, LD^2) rows
+  double sA[kTR][32], sB[kTR][32], sC[kTR][32];  // per-lane segment stores (z goes to sA)
+};
+
+struct WarpCtx {
+  const double2 *DL, *LDv;
+  int nb, nseg, lane;
+  WarpSmem *sm;
+  FwdCk *fck;
+  BwdCk *bck;
+  int64_t ck_stride, tix;  // checkpoint column of this lane
+};
+
+__device__ __forceinline__ void w_issue(const WarpCtx &W, int c, int slot) {
+  // lanes 0..15 copy the (D, LLD) rows, lanes 16..31 the (LD, LD^2) rows
+  const int k = W.lane & (kTR - 1);
+  const int row = c * kTR + k;
+  if (c >= 0 && c < W.nseg && row < W.nb) {
+    if (W.lane < kTR) __pipeline_memcpy_async(&W.sm->rDL[slot][k], &W.DL[row], sizeof(double2));
+    else __pipeline_memcpy_async(&W.sm->rLD[slot][k], &W.LDv[row], sizeof(double2));
+  }
+  __pipeline_commit();
+}
+
+// f(c, slot) for tiles c = c0 .. c1 (ascending, warp-uniform bounds); tile c
+// is in ring slot `slot` when f runs.
+template <class F>
+__device__ __forceinline__ void w_tiles_up(const WarpCtx &W, int c0, int c1, F &&f) {
+  if (c0 > c1) return;
+#pragma unroll
+  for (int k = 0; k < kRing - 1; ++k) w_issue(W, c0 + k <= c1 ? c0 + k : -1, (c0 + k) % kRing);
+  for (int c = c0; c <= c1; ++c) {
+    __pipeline_wait_prior(kRing - 2);
+    __syncwarp();
+    f(c, c % kRing);
+    __syncwarp();
+    const int cn = c + kRing - 1;
+    w_issue(W, cn <= c1 ? cn : -1, cn % kRing);
+  }
+  __pipeline_wait_prior(0);
+}
+
+// f(c, slot) for tiles c = c1 .. c0 (descending).
+template <class F>
+__device__ __forceinline__ void w_tiles_down(const WarpCtx &W, int c1, int c0, F &&f) {
+  if (c1 < c0) return;
+#pragma unroll
+  for (int k = 0; k < kRing - 1; ++k) w_issue(W, c1 - k >= c0 ? c1 - k : -1, (c1 - k + 64 * kRing) % kRing);
+  for (int c = c1; c >= c0; --c) {
+    __pipeline_wait_prior(kRing - 2);
+    __syncwarp();
+    f(c, c % kRing);
+    __syncwarp();
+    const int cn = c - (kRing - 1);
+    w_issue(W, cn >= c0 ? cn : -1, (cn + 64 * kRing) % kRing);
+  }
+  __pipeline_wait_prior(0);
+}
+
+__device__ __forceinline__ Row w_row(const WarpCtx &W, int slot, int k) {
+  const double2 a = W.sm->rDL[slot][k], b = W.sm->rLD[slot][k];
+  Row r; r.D = a.x; r.LLD = a.y; r.LD = b.x; r.LD2 = b.y;
+  return r;
+}
+
+__device__ __forceinline__ int warp_max(int v) {
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_min(int v) {
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Full twisted factorization of every lane at its own lambda (inactive lanes
+// compute too, on a harmless shift; their results are ignored).
+__device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
+  const int nb = W.nb, L = W.lane;
+  WarpSmem &S = *W.sm;
+  // ---- forward (stationary) sweep with checkpoints
+  Fwd F{-lam, 1.0, 0.0, 0};
+  w_tiles_up(W, 0, W.nseg - 1, [&](int c, int slot) {
+    put_fck(VecCtx{nullptr, nullptr, nb, W.nseg, W.fck, W.bck, W.ck_stride}, c, W.tix, F);
+    const int r0 = c * kTR;
+    const int rows = min(kTR, nb - 1 - r0);  // rows carrying LLD
+    if (rows == kTR) {
+#pragma unroll
+      for (int k = 0; k < kTR; ++k) F.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+    } else {
+      for (int k = 0; k < rows; ++k) F.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+    }
+  });
+  bool ok = isfinite(F.p) && isfinite(F.q);
+  // ---- backward (progressive) sweep with replay and argmin |gamma|
+  Bwd B{__ldg(&W.DL[nb - 1]).x - lam, 1.0, 0.0, 0};
+  int best_r = nb - 1;
+  double bN = 0, bden = 0, bH = 0, bq = 1, bK = 0, bb = 1;
+  int bneg = 0;
+  bool have = false;
+  FwdCk ckn = W.fck[(int64_t)(W.nseg - 1) * W.ck_stride + W.tix];
+  w_tiles_down(W, W.nseg - 1, 0, [&](int c, int slot) {
+    const int r0 = c * kTR, r1 = min(r0 + kTR, nb);
+    {
+      BwdCk bk; bk.a = B.a; bk.b = B.b;  // state at row min(r0 + kTR, nb - 1)
+      W.bck[(int64_t)c * W.ck_stride + W.tix] = bk;
+    }
+    const FwdCk ck = ckn;
+    if (c > 0) ckn = W.fck[(int64_t)(c - 1) * W.ck_stride + W.tix];
+    Fwd G{ck.p, ck.q, ck.H, 0};
+    unsigned mask = 0;
+    // argmin |gamma| by cross-multiplication, branch-free (selects) so that
+    // the next rows' progressive steps are scheduled across the comparison
+    auto eval = [&](int k) {
+      const double fpi = S.sA[k][L], fqi = S.sB[k][L], fHi = S.sC[k][L];
+      const double qb = fqi * B.b;
+      const double N = fma(fpi, B.b, fma(B.a, fqi, lam * qb));
+      const bool better = (!have || (fabs(N) * fabs(bden) <= fabs(bN) * fabs(qb))) && qb != 0.0 &&
+                          isfinite(N);
+      const int negk = ck.neg + __popc(mask & ((1u << k) - 1u)) + B.neg;
+      have |= better;
+      best_r = better ? r0 + k : best_r;
+      bN = better ? N : bN;
+      bden = better ? qb : bden;
+      bH = better ? fHi : bH;
+      bq = better ? fqi : bq;
+      bK = better ? B.K : bK;
+      bb = better ? B.b : bb;
+      bneg = better ? negk : bneg;
+    };
+    if (r1 < nb) {  // full segment, rows r0 .. r0+31 all below nb-1
+#pragma unroll 8
+      for (int k = 0; k < kTR; ++k) {
+        S.sA[k][L] = G.p; S.sB[k][L] = G.q; S.sC[k][L] = G.H;
+        const int before = G.neg;
+        G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+        mask |= (unsigned)(G.neg - before) << k;
+      }
+#pragma unroll 8
+      for (int k = kTR - 1; k >= 0; --k) {
+        B.step_r(w_row(W, slot, k), lam, (k & 7) == 0);
+        eval(k);
+      }
+    } else {  // the top segment: rows r0 .. nb-1
+      const int nr = r1 - r0;
+      for (int k = 0; k < nr; ++k) {
+        S.sA[k][L] = G.p; S.sB[k][L] = G.q; S.sC[k][L] = G.H;
+        if (k < nr - 1) {
+          const int before = G.neg;
+          G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+          mask |= (unsigned)(G.neg - before) << k;
+        }
+      }
+      eval(nr - 1);
+      for (int k = nr - 2; k >= 0; --k) {
+        B.step_r(w_row(W, slot, k), lam, (k & 7) == 0);
+        eval(k);
+      }
+    }
+  });
+  ok &= isfinite(B.a) && isfinite(B.b) && have;
+  Twist tw;
+  tw.r = best_r;
+  tw.gamma = bN / bden;
+  tw.nrm2 = 1.0 + bH / (bq * bq) + bK / (bb * bb);
+  tw.negc = bneg + ((tw.gamma < 0.0) ? 1 : 0);
+  tw.ok = ok && isfinite(tw.gamma) && isfinite(tw.nrm2);
+  return tw;
+}
+
+// Each lane writes its chunk rows [a, b] (values sA[0 .. b-a][lane]) to its
+// own column: 16-byte stores when the chunk start is 16-byte aligned.
+__device__ __forceinline__ void w_flush(const WarpCtx &W, int a, int b, double *col) {
+  const int L = W.lane;
+  if (b < a) return;
+  double *dst = col + a;
+  const int cnt = b - a + 1;
+  if ((((uintptr_t)dst) & 15) == 0) {
+    int k = 0;
+    for (; k + 1 < cnt; k += 2) {
+      double2 v = make_double2(W.sm->sA[k][L], W.sm->sA[k + 1][L]);
+      __stcg(reinterpret_cast<double2 *>(dst + k), v);
+    }
+    if (k < cnt) __stcg(dst + k, W.sm->sA[k][L]);
+  } else {
+    for (int k = 0; k < cnt; ++k) __stcg(dst + k, W.sm->sA[k][L]);
+  }
+}
+
+// z pass of every active lane: z_r = 1, written as scale * z to col[0 .. nb).
+// The ratios q_i / t_i (left) and b_{i+1} / u_{i+1} (right) are formed during
+// the replay with correctly rounded reciprocals (off the z recurrence), so
+// the z loops are pure multiply chains.
+__device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int r, double scale, double *col,
+                                              bool active) {
+  const int nb = W.nb, L = W.lane;
+  WarpSmem &S = *W.sm;
+  if (active) col[r] = scale;
+  // ---- left part, rows i < r, descending: z_i = -LD_i (q_i / t_i) z_{i+1}
+  const int clast = (active && r > 0) ? (r - 1) / kTR : -1;
+  const int cmax = warp_max(clast);
+  double z1 = 1.0, z2 = 0.0, ldn = (active && r > 0) ? __ldg(&W.LDv[r]).x : 0.0;
+  FwdCk ckn = W.fck[(int64_t)max(min(clast, cmax), 0) * W.ck_stride + W.tix];
+  w_tiles_down(W, cmax, 0, [&](int c, int slot) {
+    const bool on = c <= clast;
+    const int r0 = c * kTR, r1 = on ? min(r0 + kTR, r) : r0;  // rows [r0, r1)
+    const FwdCk ck = ckn;
+    if (on && c > 0) ckn = W.fck[(int64_t)(c - 1) * W.ck_stride + W.tix];
+    Fwd G{ck.p, ck.q, 0.0, 0};
+    auto rep = [&](int k) {
+      const Row R = w_row(W, slot, k);
+      const double t = fma(R.D, G.q, G.p);
+      S.sA[k][L] = -R.LD * (G.q * __drcp_rn(t));  // z_i / z_{i+1}
+      S.sC[k][L] = R.LD;
+      G.p = fma(-lam, t, R.LLD * G.p);
+      G.q = t;
+      if ((k & 7) == 7) fwd_rescale(G.p, G.q, G.H);
+    };
+    if (on && r1 == r0 + kTR) {
+#pragma unroll
+      for (int k = 0; k < kTR; ++k) rep(k);
+    } else if (on) {
+      for (int k = 0; k < r1 - r0; ++k) rep(k);
+    }
+    for (int k = r1 - r0 - 1; k >= 0; --k) {
+      const double ld = S.sC[k][L];
+      double zi = S.sA[k][L] * z1;
+      if (z1 == 0.0) zi = -(ldn / ld) * z2;  // row i+1 of (LDL^T - lambda I) z = 0
+      if (!(fabs(zi) >= kTiny)) zi = 0.0;
+      S.sA[k][L] = zi * scale;
+      z2 = z1; z1 = zi; ldn = ld;
+    }
+    w_flush(W, r0, r1 - 1, col);  // chunk rows r0 .. r1-1 from sA[0 ..]
+  });
+  // ---- right part, rows i > r, ascending: z_{i+1} = -LD_i (b_{i+1} / u_{i+1}) z_i
+  const int cfirst = (active && r < nb - 1) ? r / kTR : W.nseg;
+  const int cmin = warp_min(cfirst);
+  double y1 = 1.0, y2 = 0.0, ldp = (active && r > 0) ? __ldg(&W.LDv[r - 1]).x : 0.0;
+  BwdCk bkn = W.bck[(int64_t)min(max(cfirst, cmin), W.nseg - 1) * W.ck_stride + W.tix];
+  w_tiles_up(W, cmin, W.nseg - 1, [&](int c, int slot) {
+    const bool on = c >= cfirst;
+    const int r0 = c * kTR;
+    const int top = min(r0 + kTR, nb - 1);  // checkpoint row
+    const int lo_i = on ? max(r0, r) : top;  // rows i in [lo_i, top) give U-_i
+    const BwdCk bk = bkn;
+    if (on && c + 1 < W.nseg) bkn = W.bck[(int64_t)(c + 1) * W.ck_stride + W.tix];
+    Bwd G{bk.a, bk.b, 0.0, 0};
+    auto rep = [&](int k) {
+      const Row R = w_row(W, slot, k);
+      const double u = fma(R.LLD, G.b, G.a);
+      S.sA[k][L] = -R.LD * (G.b * __drcp_rn(u));  // z_{i+1} / z_i
+      S.sC[k][L] = R.LD;
+      G.a = fma(-lam, u, R.D * G.a);
+      G.b = u;
+      if ((k & 7) == 0) bwd_rescale(G.a, G.b, G.K);
+    };
+    if (on && lo_i == r0 && top == r0 + kTR) {
+#pragma unroll
+      for (int k = kTR - 1; k >= 0; --k) rep(k);
+    } else if (on) {
+      for (int k = top - 1 - r0; k >= lo_i - r0; --k) rep(k);
+    }
+    // z_{i+1} for i in [lo_i, top): chunk rows lo_i+1 .. top, stored at sA[i - lo_i]
+    // (ascending i: index i - lo_i <= i - r0 was already read)
+    for (int i = lo_i; i < top; ++i) {
+      const int k = i - r0;
+      const double ld = S.sC[k][L];
+      double zn = S.sA[k][L] * y1;
+      if (y1 == 0.0) zn = -(ldp / ld) * y2;  // row i of (LDL^T - lambda I) z = 0
+      if (!(fabs(zn) >= kTiny)) zn = 0.0;
+      S.sA[i - lo_i][L] = zn * scale;
+      y2 = y1; y1 = zn; ldp = ld;
+    }
+    w_flush(W, lo_i + 1, top, col);
+  });
+}
+
+// One warp item: up to 32 tasks of one node.
+struct WarpItem {
+  int32_t node;
+  int32_t t0, t1;  // task ids [t0, t1) (tasks of one node are consecutive)
+  int32_t pad;
+};
+
+struct WVecArgs {
+  const Node *nodes;
+  const double2 *LDv;        // global (LD, LD^2) per row
+  const VecTask *tasks;
+  const int *task_list;      // optional: item task indices go through this list
+  const WarpItem *items;
+  int nitems;
+  double *lo, *hi;           // slot brackets (node coordinates)
+  const int *slot_j;         // block-local 1-based eigen index per slot
+  FwdCk *fck;
+  BwdCk *bck;
+  int64_t ck_stride;         // = number of tasks + 32 (columns ntask + lane: idle lanes)
+  int ntask;
+  double *Z; int64_t ldz;    // modes 0, 2: Z columns (tk.col), node rows at N.row0
+  double *lam_out;           // modes 0, 2: final lambda (node coordinates) per task
+  double *zbuf; int64_t zstride;  // mode 1: unit vectors to zbuf + tk.col * zstride
+  int mode;                  // 0: RQC (reading 10); 1: one factorization (probes);
+                             // 2: one factorization at the bracket midpoint (RQC fallback)
+  int rqc_max;               // mode 0: factorizations before the fallback (3)
+  int *fail_list;            // mode 0: tasks that did not converge (appended)
+  int *fail_count;
+  unsigned long long *ctr;   // [0] factorizations, [1] fallbacks
+};
+
+__device__ __forceinline__ void wvec_body(const WVecArgs &A) {
+  extern __shared__ __align__(16) unsigned char wsm_raw[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kWarpsPerCta + wid;
+  if (item >= A.nitems) return;  // whole warp
+  const WarpItem It = A.items[item];
+  const Node N = A.nodes[It.node];
+  const bool active = It.t0 + lane < It.t1;
+  const int tix = A.task_list ? A.task_list[active ? It.t0 + lane : It.t0] : (active ? It.t0 + lane : It.t0);
+  const VecTask tk = A.tasks[tix];
+  WarpCtx W;
+  W.DL = N.DL; W.LDv = A.LDv + N.row0; W.nb = N.nb; W.nseg = (N.nb + kTR - 1) / kTR;
+  W.lane = lane;
+  W.sm = reinterpret_cast<WarpSmem *>(wsm_raw) + wid;
+  W.fck = A.fck; W.bck = A.bck; W.ck_stride = A.ck_stride;
+  const int64_t spare = A.ntask + lane;   // idle lanes checkpoint into spare columns
+  W.tix = active ? tix : spare;
+  double lo = A.lo[tk.slot], hi = A.hi[tk.slot];
+  if (N.nb == 1) {
+    if (active) {
+      if (A.mode != 1) { A.Z[tk.col * A.ldz + N.row0] = 1.0; A.lam_out[tix] = __ldg(&N.DL[0]).x; }
+      else A.zbuf[tk.col * A.zstride] = 1.0;
+    }
+    return;
+  }
+  double lam = (A.mode == 2 || isnan(tk.lam0)) ? 0.5 * (lo + hi) : tk.lam0;
+  unsigned long long nfact = 0;
+  Twist tw;
+  // full factorization; nudge lambda if not finite (overflow insurance, reading 25)
+  {
+    double nudge = 2.0 * kEps * fabs(lam) + kTiny;
+    const double lam_base = lam;
+    for (int tries = 0; tries < 60; ++tries) {
+      tw = w_twist_full(W, lam);
+      ++nfact;
+      if (!__any_sync(0xffffffffu, active && !tw.ok)) break;
+      if (active && !tw.ok) { lam = lam_base + nudge; nudge *= 2.0; }
+    }
+  }
+  double lam_fin = lam;
+  if (A.mode == 0) {
+    // O10 RQC (readings 10, 24): stop when |delta| <= 4 eps |lambda| or
+    // fl(lambda + delta) == lambda; a step leaving [lo, hi] from the interior
+    // is clamped to the violated end, from an end it bisects.  A lane that
+    // has converged keeps its factorization (its checkpoint column is parked
+    // on a spare column while the other lanes iterate).
+    const int j = A.slot_j[tk.slot];
+    bool conv = !active, failed = false;
+    Twist best = tw;
+    double lam_best = lam;
+    for (int it = 1;; ++it) {
+      if (!conv) {
+        if (tw.negc >= j) { if (lam < hi) hi = lam; } else { if (lam > lo) lo = lam; }
+        const double delta = tw.gamma / tw.nrm2;
+        if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam) {
+          conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
+        } else {
+          double nw = lam + delta;
+          if (nw <= lo || nw >= hi) {
+            if (lam == lo || lam == hi) {
+              nw = 0.5 * (lo + hi);
+              if (nw <= lo || nw >= hi) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }
+            } else {
+              nw = (nw <= lo) ? lo : hi;
+            }
+          }
+          lam = nw;
+        }
+        if (!conv && it >= A.rqc_max) { conv = true; failed = true; }
+        if (conv) W.tix = spare;  // park: later factorizations must not touch its checkpoints
+      }
+      if (__all_sync(0xffffffffu, conv)) break;
+      tw = w_twist_full(W, lam);
+      ++nfact;
+      if (!conv && !tw.ok) { conv = true; failed = true; W.tix = spare; }
+    }
+    W.tix = active ? tix : spare;
+    tw = best;
+    lam = lam_best;
+    if (active && failed) {
+      // O10 fallback, deferred: the bracket goes back to the slot; the host
+      // refines it to 4 eps and a mode-2 pass writes the vector
+      A.lo[tk.slot] = lo; A.hi[tk.slot] = hi;
+      A.fail_list[atomicAdd(A.fail_count, 1)] = tix;
+      atomicAdd(&A.ctr[1], 1ull);
+    }
+    // failed lanes skip the solve (their column is written by the fallback)
+    const double sc = 1.0 / sqrt(tw.nrm2);
+    w_twist_solve(W, lam, tw.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !failed);
+    if (active && !failed) A.lam_out[tix] = lam_fin;
+    if (active) atomicAdd(&A.ctr[0], nfact);
+    return;
+  }
+  const double sc = 1.0 / sqrt(tw.nrm2);
+  double *col = (A.mode == 2) ? A.Z + tk.col * A.ldz + N.row0 : A.zbuf + tk.col * A.zstride;
+  w_twist_solve(W, lam, tw.r, sc, col, active);
+  if (active) {
+    if (A.mode == 2) A.lam_out[tix] = lam_fin;
+    atomicAdd(&A.ctr[0], nfact);
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_wvectors(WVecArgs A) { wvec_body(A); }
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_wprobe(WVecArgs A) { wvec_body(A); }
+
+}  // namespace mrrr

@@ -15,65 +15,10 @@
 #include "../../include/mrrr.h"
 #include "kernels_tree.cuh"
 #include "kernels_vec.cuh"
+#include "kernels_warp.cuh"
 
 using namespace mrrr;
 
-namespace mrrr {
-// Deferred O10 fallback: one CTA per failing eigenpair refines its bracket
-// [lo, hi] (node coordinates) to rtol relative by multisection with
-// blockDim.x * M shifts per round, one node sweep per round (rows staged in
-// shared memory by cta_sweep).  Invariant N(lo) < j <= N(hi).
-template <int M>
-__global__ void __launch_bounds__(128) k_fallback_bisect(const Node *nodes, const VecTask *tasks,
-                                                         const int *list, const int *slot_j,
-                                                         double *lo_arr, double *hi_arr, double rtol,
-                                                         unsigned long long *safe_ctr) {
-  __shared__ double2 sm[2 * kTile];
-  __shared__ double red_lo[32], red_hi[32];
-  const VecTask tk = tasks[list[blockIdx.x]];
-  const Node N = nodes[tk.node];
-  const int j = slot_j[tk.slot];
-  double lo = lo_arr[tk.slot], hi = hi_arr[tk.slot];
-  const int S = blockDim.x * M;
-  for (int round = 0; round < 64; ++round) {
-    const double mid = 0.5 * (lo + hi);
-    if (hi - lo <= rtol * fmax(fabs(lo), fabs(hi)) || !(mid > lo && mid < hi)) break;
-    double mu[M];
-#pragma unroll
-    for (int c = 0; c < M; ++c)
-      mu[c] = lo + (hi - lo) * ((double)(threadIdx.x * M + c + 1) / (double)(S + 1));
-    unsigned k[M];
-    bool ok;
-    cta_sweep<M>(N.DL, N.nb, sm, mu, k, ok);
-    if (!ok) {
-      atomicAdd(safe_ctr, 1ull);
-#pragma unroll
-      for (int c = 0; c < M; ++c) k[c] = negcount_qd_safe(N.DL, N.nb, mu[c]);
-    }
-    double nlo = lo, nhi = hi;
-#pragma unroll
-    for (int c = 0; c < M; ++c) {
-      if ((int)k[c] < j) nlo = fmax(nlo, mu[c]);
-      else nhi = fmin(nhi, mu[c]);
-    }
-    for (int o = 16; o; o >>= 1) {
-      nlo = fmax(nlo, __shfl_xor_sync(0xffffffff, nlo, o));
-      nhi = fmin(nhi, __shfl_xor_sync(0xffffffff, nhi, o));
-    }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) { red_lo[w] = nlo; red_hi[w] = nhi; }
-    __syncthreads();
-    nlo = lo; nhi = hi;
-    for (int x = 0; x < (int)(blockDim.x >> 5); ++x) { nlo = fmax(nlo, red_lo[x]); nhi = fmin(nhi, red_hi[x]); }
-    __syncthreads();
-    if (nhi <= nlo) nhi = hi;  // non-monotone counts: keep the old upper end
-    const bool progress = nlo != lo || nhi != hi;
-    lo = nlo; hi = nhi;
-    if (!progress) break;  // the grid no longer resolves [lo, hi] (ulp level)
-  }
-  if (threadIdx.x == 0) { lo_arr[tk.slot] = lo; hi_arr[tk.slot] = hi; }
-}
-}  // namespace mrrr
 
 namespace {
 
@@ -420,6 +365,36 @@ void launch_grid(int M, const Node *nodes, int node, double lo0, double hi0, int
   g_stats.kernel_launches++;
 }
 
+// Warp items: runs of consecutive tasks of one node, at most 32 per item.
+std::vector<WarpItem> make_warp_items(const std::vector<VecTask> &t) {
+  std::vector<WarpItem> v;
+  const int nt = (int)t.size();
+  for (int a = 0; a < nt;) {
+    int b = a;
+    while (b < nt && b - a < 32 && t[b].node == t[a].node) ++b;
+    WarpItem w; w.node = t[a].node; w.t0 = a; w.t1 = b; w.pad = 0;
+    v.push_back(w);
+    a = b;
+  }
+  return v;
+}
+
+void launch_wvec(bool probe, WVecArgs A, cudaStream_t s) {
+  const size_t smem = kWarpsPerCta * sizeof(WarpSmem);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_wvectors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_wprobe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int grid = (A.nitems + kWarpsPerCta - 1) / kWarpsPerCta;
+  if (grid == 0) return;
+  if (probe) k_wprobe<<<grid, 32 * kWarpsPerCta, smem, s>>>(A);
+  else k_wvectors<<<grid, 32 * kWarpsPerCta, smem, s>>>(A);
+  CK(cudaGetLastError());
+  g_stats.kernel_launches++;
+}
+
 struct Problem {
   int64_t n;
   const double *d, *e;
@@ -444,7 +419,7 @@ int solve(Problem &P, int64_t *m_out) {
   DevArena ar(s);
   Trace tr;
   Timer tm(s), tall(s);
-  KTimer kt_root, kt_vec;
+  KTimer kt_root, kt_vec, kt_fin;
   memset(&g_stats, 0, sizeof(g_stats));
   const bool vectors = P.Z != nullptr;
 
@@ -649,11 +624,19 @@ int solve(Problem &P, int64_t *m_out) {
   // ---------------- a3: root eigenvalue intervals ----------------
   const double rtol_root = (vectors && nblocks == 1) ? P.o.rtol_class : 4.0 * kEps;
   const int M = std::max(1, P.o.multisection);
-  auto make_work = [&](int node, int s0, int s1, std::vector<Work> &wv) {
-    for (int a = s0; a < s1; a += 128) {
-      Work W; W.node = node; W.s0 = a; W.s1 = std::min(a + 128, s1); W.pad = 0;
+  // Work items of <= wmax member slots of one node.  wmax shrinks when the
+  // level has few slots, so that more CTAs (and more shifts per member, i.e.
+  // fewer rounds) cover the GPU.
+  auto make_work = [&](int node, int s0, int s1, int wmax, std::vector<Work> &wv) {
+    for (int a = s0; a < s1; a += wmax) {
+      Work W; W.node = node; W.s0 = a; W.s1 = std::min(a + wmax, s1); W.pad = 0;
       wv.push_back(W);
     }
+  };
+  auto pick_wmax = [&](int64_t slots) {
+    int w = 128;
+    while (w > 8 && slots / w < 4 * 148) w >>= 1;
+    return w;
   };
   {
     std::vector<Work> wv;
@@ -672,11 +655,15 @@ int solve(Problem &P, int64_t *m_out) {
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }
-      make_work(B.root_node, B.slot0, B.slot1, wv);
+      make_work(B.root_node, B.slot0, B.slot1, pick_wmax(nslots), wv);
     }
     Work *dwork = ar.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
-    launch_bisect(M, dnodes, dwork, (int)wv.size(), slot_j, slo, shi, rtol_root, ctr, s);
+    k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, nullptr, slot_j, slo, shi, nullptr, nullptr, 0,
+                                               rtol_root, 4000, dfail + 2, ctr, ctr + 1);
+    CK(cudaGetLastError());
+    g_stats.kernel_launches++;
+    (void)M;
     kt_root.stop(s);
   }
 
@@ -836,19 +823,18 @@ int solve(Problem &P, int64_t *m_out) {
       }
       VecTask *dzt = ar.alloc<VecTask>(zt.size());
       h2d(dzt, zt.data(), zt.size(), s);
-      int ntask = (int)zt.size();
-      int nseg = (int)((nbmax + kSeg - 1) / kSeg);
-      FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg * ntask);
-      BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg * ntask);
-      VecArgs A{};
-      A.nodes = dnodes; A.blocks = dblocks; A.LDv = LDv; A.tasks = dzt; A.ntask = ntask;
-      A.lo = slo; A.hi = shi; A.slot_j = slot_j; A.fck = fck; A.bck = bck;
-      A.ck_stride = ntask; A.nseg_max = nseg; A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1;
-      A.ctr = ctr + 4; A.task_info = nullptr; A.trace_task = -1;
-      size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
-      k_zprobe<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
-      CK(cudaGetLastError());
-      g_stats.kernel_launches++;
+      const int ntask = (int)zt.size();
+      const int nseg = (int)((nbmax + kSeg - 1) / kSeg);
+      FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg * (ntask + 32));
+      BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg * (ntask + 32));
+      auto items = make_warp_items(zt);
+      WarpItem *ditems = ar.alloc<WarpItem>(items.size());
+      h2d(ditems, items.data(), items.size(), s);
+      WVecArgs A{};
+      A.nodes = dnodes; A.LDv = LDv; A.tasks = dzt; A.items = ditems; A.nitems = (int)items.size();
+      A.lo = slo; A.hi = shi; A.fck = fck; A.bck = bck; A.ck_stride = ntask + 32; A.ntask = ntask;
+      A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1; A.ctr = ctr + 4; A.slot_j = slot_j;
+      launch_wvec(true, A, s);
     }
     Cand *cand = ar.alloc<Cand>((size_t)6 * ncl);
     k_cand<<<(6 * ncl + 127) / 128, 128, 0, s>>>(dnodes, dcl_parent, dcl_s0, dcl_s1, slo, shi, ncl,
@@ -894,14 +880,18 @@ int solve(Problem &P, int64_t *m_out) {
     nnodes += ncl;
     // verify + refine in child coordinates
     std::vector<Work> wv;
-    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], wv);
+    {
+      int64_t lvl_slots = 0;
+      for (int c = 0; c < ncl; ++c) lvl_slots += cl_s1[c] - cl_s0[c];
+      const int wmax = pick_wmax(lvl_slots);
+      for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], wmax, wv);
+    }
     Work *dwork = ar.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
-    k_verify<<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, slot_j, slo, shi, wlo, whi, dfail + 2,
-                                            ctr + 2, ctr + 1);
+    k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, nullptr, slot_j, slo, shi, wlo, whi, 1,
+                                               P.o.rtol_class, 4000, dfail + 2, ctr + 2, ctr + 1);
     CK(cudaGetLastError());
     g_stats.kernel_launches++;
-    launch_bisect(M, dnodes, dwork, (int)wv.size(), slot_j, slo, shi, P.o.rtol_class, ctr + 2, s);
     d2h(h_fail, dfail, 4, s);
     if (getenv("MRRR_DUMP")) {
       char nm[64];
@@ -935,25 +925,57 @@ int solve(Problem &P, int64_t *m_out) {
   const int ntask = (int)tasks.size();
   g_stats.singletons = ntask;
   if (ntask > 0) {
+    // O10 (reading 10 amended): singleton brackets to 2^-40 relative by the
+    // adaptive multisection, work items grouped by node through a slot list
+    {
+      std::vector<int> order(ntask);
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int a, int b) { return tasks[a].node < tasks[b].node; });
+      std::vector<int> list(ntask);
+      for (int q = 0; q < ntask; ++q) list[q] = tasks[order[q]].slot;
+      const int wmax = pick_wmax(ntask);
+      std::vector<Work> wv;
+      for (int q0 = 0; q0 < ntask;) {
+        int q1 = q0;
+        while (q1 < ntask && tasks[order[q1]].node == tasks[order[q0]].node) ++q1;
+        for (int a = q0; a < q1; a += wmax) {
+          Work W; W.node = tasks[order[q0]].node; W.s0 = a; W.s1 = std::min(a + wmax, q1); W.pad = 0;
+          wv.push_back(W);
+        }
+        q0 = q1;
+      }
+      int *dlist = ar.alloc<int>(ntask);
+      h2d(dlist, list.data(), ntask, s);
+      Work *dwork = ar.alloc<Work>(wv.size());
+      h2d(dwork, wv.data(), wv.size(), s);
+      kt_fin.start(s);
+      k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, dlist, slot_j, slo, shi, nullptr, nullptr,
+                                                 0, std::ldexp(1.0, -40), 4000, dfail + 2, ctr + 2,
+                                                 ctr + 1);
+      kt_fin.stop(s);
+      CK(cudaGetLastError());
+      g_stats.kernel_launches++;
+    }
     VecTask *dt = ar.alloc<VecTask>(ntask);
     h2d(dt, tasks.data(), ntask, s);
-    int nseg = (int)((nbmax + kSeg - 1) / kSeg);
-    FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg * ntask);
-    BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg * ntask);
+    const int nseg = (int)((nbmax + kSeg - 1) / kSeg);
+    FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg * (ntask + 32));
+    BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg * (ntask + 32));
     double *lam = ar.alloc<double>(ntask);
-    VecArgs A{};
-    A.nodes = dnodes; A.blocks = dblocks; A.LDv = LDv; A.tasks = dt; A.ntask = ntask;
-    A.lo = slo; A.hi = shi; A.slot_j = slot_j; A.fck = fck; A.bck = bck;
-    A.ck_stride = ntask; A.nseg_max = nseg; A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam;
-    A.mode = 0; A.ctr = ctr + 8;
+    auto items = make_warp_items(tasks);
+    WarpItem *ditems = ar.alloc<WarpItem>(items.size());
+    h2d(ditems, items.data(), items.size(), s);
+    WVecArgs A{};
+    A.nodes = dnodes; A.LDv = LDv; A.tasks = dt; A.items = ditems; A.nitems = (int)items.size();
+    A.lo = slo; A.hi = shi; A.fck = fck; A.bck = bck; A.ck_stride = ntask + 32; A.ntask = ntask;
+    A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam; A.mode = 0; A.ctr = ctr + 8;
+    A.slot_j = slot_j; A.rqc_max = 3;
     int *fail_list = ar.alloc<int>(ntask), *fail_count = ar.alloc<int>(1);
     CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
     A.fail_list = fail_list; A.fail_count = fail_count;
-    const bool dbg = getenv("MRRR_DEBUG") != nullptr;
-    int *tinfo = dbg ? ar.alloc<int>(ntask) : nullptr;
-    A.task_info = tinfo;
-    A.trace_task = getenv("MRRR_TRACE_TASK") ? atoi(getenv("MRRR_TRACE_TASK")) : -1;
-    size_t smem = 3 * kSeg * kVecThreads * sizeof(double);
+    int *tinfo = nullptr;
+    long long *tcyc = nullptr;
     {
       std::vector<Node> hnodes(nnodes);
       d2h(hnodes.data(), dnodes, nnodes, s);
@@ -963,23 +985,50 @@ int solve(Problem &P, int64_t *m_out) {
       g_stats.vec_elems = el;
     }
     kt_vec.start(s);
-    k_vectors<<<(ntask + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(A);
+    launch_wvec(false, A, s);
     kt_vec.stop(s);
-    CK(cudaGetLastError());
-    g_stats.kernel_launches++;
-    // deferred O10 fallback: CTA-parallel multisection to 4 eps, then one
-    // factorization at the midpoint (mode 2)
-    int h_nfail = 0;
-    d2h(&h_nfail, fail_count, 1, s);
-    if (h_nfail > 0) {
-      k_fallback_bisect<4><<<h_nfail, 128, 0, s>>>(dnodes, dt, fail_list, slot_j, slo, shi,
-                                                   4.0 * kEps, ctr + 1);
-      CK(cudaGetLastError());
-      VecArgs B2 = A;
-      B2.mode = 2; B2.task_list = fail_list; B2.ntask = h_nfail; B2.task_info = nullptr;
-      k_vectors<<<(h_nfail + kVecThreads - 1) / kVecThreads, kVecThreads, smem, s>>>(B2);
-      CK(cudaGetLastError());
-      g_stats.kernel_launches += 2;
+    // deferred O10 fallback (reading 10): brackets of the tasks whose RQC did
+    // not converge are refined to 4 eps, then one factorization at the
+    // midpoint writes their vectors (mode 2)
+    {
+      int h_nf = 0;
+      d2h(&h_nf, fail_count, 1, s);
+      if (h_nf > 0) {
+        std::vector<int> fl(h_nf);
+        d2h(fl.data(), fail_list, h_nf, s);
+        std::sort(fl.begin(), fl.end(), [&](int a, int b) {
+          return tasks[a].node != tasks[b].node ? tasks[a].node < tasks[b].node : a < b;
+        });
+        std::vector<int> slots(h_nf);
+        std::vector<Work> wv;
+        std::vector<WarpItem> fitems;
+        for (int q0 = 0; q0 < h_nf;) {
+          int q1 = q0;
+          while (q1 < h_nf && tasks[fl[q1]].node == tasks[fl[q0]].node) ++q1;
+          for (int a = q0; a < q1; a += 32) {
+            Work W; W.node = tasks[fl[q0]].node; W.s0 = a; W.s1 = std::min(a + 32, q1); W.pad = 0;
+            wv.push_back(W);
+            WarpItem wi; wi.node = W.node; wi.t0 = W.s0; wi.t1 = W.s1; wi.pad = 0;
+            fitems.push_back(wi);
+          }
+          q0 = q1;
+        }
+        for (int q = 0; q < h_nf; ++q) slots[q] = tasks[fl[q]].slot;
+        int *dslots = ar.alloc<int>(h_nf), *dfl = ar.alloc<int>(h_nf);
+        h2d(dslots, slots.data(), h_nf, s);
+        h2d(dfl, fl.data(), h_nf, s);
+        Work *dw = ar.alloc<Work>(wv.size());
+        h2d(dw, wv.data(), wv.size(), s);
+        k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dw, dslots, slot_j, slo, shi, nullptr, nullptr,
+                                                   0, 4.0 * kEps, 4000, dfail + 2, ctr + 2, ctr + 1);
+        CK(cudaGetLastError());
+        g_stats.kernel_launches++;
+        WarpItem *dfi = ar.alloc<WarpItem>(fitems.size());
+        h2d(dfi, fitems.data(), fitems.size(), s);
+        WVecArgs F = A;
+        F.mode = 2; F.task_list = dfl; F.items = dfi; F.nitems = (int)fitems.size();
+        launch_wvec(false, F, s);
+      }
     }
     if (getenv("MRRR_DEBUG")) {
       std::vector<double> hl(ntask);
@@ -988,7 +1037,21 @@ int solve(Problem &P, int64_t *m_out) {
       d2h(hnodes.data(), dnodes, nnodes, s);
       std::vector<int> hti(ntask);
       d2h(hti.data(), tinfo, ntask, s);
-      for (int t = 0; t < ntask; ++t) {
+      std::vector<long long> hcy(ntask);
+      d2h(hcy.data(), tcyc, ntask, s);
+      {
+        std::vector<long long> sc(hcy);
+        std::sort(sc.begin(), sc.end());
+        int hist[16] = {0};
+        for (int t = 0; t < ntask; ++t) hist[std::min(hti[t] & 255, 15)]++;
+        fprintf(stderr, "[mrrr] k_vectors cycles per task: p50 %lld p90 %lld p99 %lld max %lld (nb %d)\n",
+                sc[ntask / 2], sc[ntask * 9 / 10], sc[ntask * 99 / 100], sc[ntask - 1], (int)nbmax);
+        fprintf(stderr, "[mrrr] iterations hist:");
+        for (int k = 0; k < 16; ++k) fprintf(stderr, " %d:%d", k, hist[k]);
+        fprintf(stderr, "\n");
+      }
+      if (getenv("MRRR_DEBUG_TASKS") == nullptr) hti.clear();
+      for (int t = 0; t < (int)hti.size(); ++t) {
         const Node &N = hnodes[tasks[t].node];
         fprintf(stderr, "task %d slot %d node %d col %ld lam %.17g tau %.17g + %.3g sigma %.17g depth %d it %d fb %d\n", t,
                 tasks[t].slot, tasks[t].node, (long)tasks[t].col, hl[t], N.tau_hi, N.tau_lo, N.sigma, N.depth,
@@ -1012,6 +1075,7 @@ int solve(Problem &P, int64_t *m_out) {
   g_stats.ms_total = tall.stop();
   g_stats.ms_k_root_bisect = kt_root.ms();
   g_stats.ms_k_vectors = kt_vec.ms();
+  g_stats.ms_k_final_refine = kt_fin.ms();
   return 0;
 }
 

@@ -32,7 +32,8 @@ class Stats(C.Structure):
                 ("kernel_launches", C.c_int64), ("ms_root", C.c_double), ("ms_tree", C.c_double),
                 ("ms_vectors", C.c_double), ("ms_total", C.c_double),
                 ("ms_k_root_bisect", C.c_double), ("ms_k_vectors", C.c_double),
-                ("vec_tasks", C.c_int64), ("vec_elems", C.c_int64)]
+                ("vec_tasks", C.c_int64), ("vec_elems", C.c_int64),
+                ("ms_k_final_refine", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

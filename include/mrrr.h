@@ -69,6 +69,10 @@ typedef struct {
                           (1 = plain bisection); default 4 */
   int grid_factor;     /* root grid points per wanted eigenvalue; default 4;
                           0 disables the grid stage */
+  double rtol_vec;     /* singleton brackets refined to this relative width
+                          before the RQC; 0 = none (default; reading 10) */
+  int rqc_max;         /* twisted factorizations of the RQC before the
+                          bisection fallback; default 3 (reading 10) */
 } mrrr_opts_t;
 
 void mrrr_default_opts(mrrr_opts_t *opts);

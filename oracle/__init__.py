@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
 class Opts(C.Structure):
     _fields_ = [("tol_relgap", C.c_double), ("rtol_class", C.c_double),
                 ("max_depth", C.c_int), ("perturb_root", C.c_int),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("rtol_vec", C.c_double), ("rqc_max", C.c_int)]
 
 
 class Stats(C.Structure):

@@ -24,6 +24,8 @@ void oracle_default_opts(oracle_opts_t *o) {
   o->max_depth = 128;                  /* reading 21 */
   o->perturb_root = 1;                 /* reading 3 */
   o->seed = 0x1205210700000000ULL;     /* SURVEY §8(b) default seed */
+  o->rtol_vec = 0.0;                   /* reading 10 */
+  o->rqc_max = 3;                      /* reading 10 */
 }
 
 /* ------------------------------------------------------------------------ */
@@ -385,21 +387,19 @@ static void two_sum(double a, double b, double *s, double *err) {
 
 /* O10 -- singleton vector by Rayleigh-quotient correction on twisted
  * factorizations (readings 10, 24, 25).
- * Reading 10 (amended): the bracket is first refined by bisection to relative
- * width 2^-40 (high relative accuracy), so that the RQC
- * converges in two factorizations for nearly every eigenpair. */
-#define ORACLE_RTOL_VEC 0x1p-40
-#define ORACLE_RQC_MAX 3 /* factorizations before the bisection fallback (reading 10) */
+ * Reading 10 (amended): at most opts.rqc_max factorizations (3), then the
+ * bisection fallback; optionally (opts.rtol_vec > 0) the bracket is first
+ * refined by bisection to that relative width. */
 static void singleton(ctx_t *c, const rrr_t *R, int64_t j) {
   int64_t nb = R->nb;
   double lo = c->lo[j], hi = c->hi[j];
-  bisect(c, R, j, ORACLE_RTOL_VEC, &lo, &hi);
+  if (c->o->rtol_vec > 0) bisect(c, R, j, c->o->rtol_vec, &lo, &hi);
   double lam = 0.5 * (lo + hi), lam_fin = lam;
   int64_t r, nc, nfact = 0;
   double gamma, nrm2 = 1;
   int converged = 0, rs = 0;
   double *z = c->z;
-  for (int it = 0; it < ORACLE_RQC_MAX; ++it) {
+  for (int it = 0; it < (c->o->rqc_max > 0 ? c->o->rqc_max : 1); ++it) {
     twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lam, R->pivmin, &c->ws, z, &r,
                &gamma, &nc, &rs);
     nfact++;

@@ -405,8 +405,12 @@ struct Problem {
   int64_t ldz;
   cudaStream_t s;
   mrrr_opts_t o;
-  // distributed (single GPU: rank 0 of 1)
+  // distributed (single GPU: rank 0 of 1); DESIGN.md §6
   int rank = 0, nranks = 1;
+  mrrr_allgather_fn allgather = nullptr;
+  void *ag_ctx = nullptr;
+  double *w_all = nullptr;  // dist: all m eigenvalues (device); P.w is then unused
+  int64_t col_begin = 0, m_local = 0;
 };
 
 struct HostNode {
@@ -633,6 +637,7 @@ int solve(Problem &P, int64_t *m_out) {
       wv.push_back(W);
     }
   };
+  constexpr int kTreeChunk = 32;
   auto pick_wmax = [&](int64_t slots) {
     int w = 128;
     while (w > 8 && slots / w < 4 * 148) w >>= 1;
@@ -726,25 +731,54 @@ int solve(Problem &P, int64_t *m_out) {
     }
     m = cnt;
   }
-  h2d(slot_out, h_slot_out.data(), nslots, s);
+  // ---- e: this rank's columns (static division of the m wanted pairs,
+  // P:L1139-1146); every rank builds the same root, intervals and tree for
+  // the clusters its columns touch, and computes only its own vectors.
+  const int nr = std::max(1, P.nranks);
+  const int64_t epp = (m + nr - 1) / nr;
+  const int64_t c0 = std::min<int64_t>((int64_t)P.rank * epp, m), c1 = std::min<int64_t>(c0 + epp, m);
+  P.col_begin = c0;
+  P.m_local = c1 - c0;
+  std::vector<int> h_own(nslots, -1);  // local output column of a slot, or -1
+  for (int64_t q = 0; q < nslots; ++q)
+    if (h_slot_out[q] >= c0 && h_slot_out[q] < c1) h_own[q] = (int)(h_slot_out[q] - c0);
+  // local eigenvalue buffer: the caller's w on one GPU, a padded buffer for the
+  // all-gather otherwise
+  double *w_loc = P.w;
+  if (nr > 1) {
+    w_loc = ar.alloc<double>(std::max<int64_t>(epp, 1));
+    CK(cudaMemsetAsync(w_loc, 0, std::max<int64_t>(epp, 1) * sizeof(double), s));
+  }
+  // final w: all-gather of the padded local parts (dist) and the O11 monotone fix
+  auto finish_w = [&]() {
+    if (nr == 1) {
+      if (m > 1) { k_monotone<<<1, 1024, 0, s>>>(P.w, (int)m); CK(cudaGetLastError()); g_stats.kernel_launches++; }
+      return;
+    }
+    double *wall = ar.alloc<double>(std::max<int64_t>(epp * nr, 1));
+    if (P.allgather(P.ag_ctx, w_loc, wall, (size_t)epp * sizeof(double), (void *)s) != 0)
+      throw MrrrError{MRRR_ERR_COMM};
+    if (m > 0) CK(cudaMemcpyAsync(P.w_all, wall, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (m > 1) { k_monotone<<<1, 1024, 0, s>>>(P.w_all, (int)m); CK(cudaGetLastError()); g_stats.kernel_launches++; }
+  };
+  h2d(slot_out, h_own.data(), nslots, s);
   *m_out = m;
   if (tr.on) { CK(cudaStreamSynchronize(s)); tr.mark("root bisection"); }
   g_stats.ms_root = tm.stop();
 
   if (!vectors) {
     k_values<<<(nslots + 255) / 256, 256, 0, s>>>(slot_node, slot_out, dnodes, slo, shi,
-                                                  (int)nslots, 1.0 / scale, P.w);
+                                                  (int)nslots, 1.0 / scale, w_loc);
     CK(cudaGetLastError());
-    // 1x1 blocks: w = d
-    if (m > 1) k_monotone<<<1, 1024, 0, s>>>(P.w, (int)m);
-    g_stats.kernel_launches += 2;
+    g_stats.kernel_launches++;
+    finish_w();
     CK(cudaStreamSynchronize(s));
     g_stats.ms_total = tall.stop();
     g_stats.ms_k_root_bisect = kt_root.ms();
     return 0;
   }
-  if (nblocks > 1)
-    CK(cudaMemset2DAsync(P.Z, P.ldz * sizeof(double), 0, n * sizeof(double), m, s));
+  if (nblocks > 1 && P.m_local > 0)
+    CK(cudaMemset2DAsync(P.Z, P.ldz * sizeof(double), 0, n * sizeof(double), P.m_local, s));
 
   // ---------------- a4/a5: representation tree ----------------
   dump("root_lo.bin", slo, nslots, s);
@@ -782,14 +816,14 @@ int solve(Problem &P, int64_t *m_out) {
         if (!h_active[q]) { st = q + 1; continue; }
         if (h_run_end[q]) {
           if (q == st) {
-            if (h_slot_out[q] >= 0) {
-              VecTask t; t.slot = q; t.node = nd; t.col = h_slot_out[q]; t.lam0 = NAN;
+            if (h_own[q] >= 0) {
+              VecTask t; t.slot = q; t.node = nd; t.col = h_own[q]; t.lam0 = NAN;
               tasks.push_back(t);
             }
             h_active[q] = 0;
           } else {
             bool any = false;
-            for (int x = st; x <= q; ++x) any |= h_slot_out[x] >= 0;
+            for (int x = st; x <= q; ++x) any |= h_own[x] >= 0;
             if (any) { cl_parent.push_back(nd); cl_s0.push_back(st); cl_s1.push_back(q + 1); }
             else for (int x = st; x <= q; ++x) h_active[x] = 0;
           }
@@ -880,12 +914,10 @@ int solve(Problem &P, int64_t *m_out) {
     nnodes += ncl;
     // verify + refine in child coordinates
     std::vector<Work> wv;
-    {
-      int64_t lvl_slots = 0;
-      for (int c = 0; c < ncl; ++c) lvl_slots += cl_s1[c] - cl_s0[c];
-      const int wmax = pick_wmax(lvl_slots);
-      for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], wmax, wv);
-    }
+    // chunks of kTreeChunk members from each cluster's start: the refinement of
+    // a cluster depends on the cluster alone, so every rank that holds a
+    // shared cluster computes bitwise the same child intervals (§8(e))
+    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], kTreeChunk, wv);
     Work *dwork = ar.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
     k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, nullptr, slot_j, slo, shi, wlo, whi, 1,
@@ -925,9 +957,10 @@ int solve(Problem &P, int64_t *m_out) {
   const int ntask = (int)tasks.size();
   g_stats.singletons = ntask;
   if (ntask > 0) {
-    // O10 (reading 10 amended): singleton brackets to 2^-40 relative by the
-    // adaptive multisection, work items grouped by node through a slot list
-    {
+    // O10 (reading 10, opts.rtol_vec > 0): singleton brackets refined by the
+    // adaptive multisection before the RQC, work items grouped by node
+    // through a slot list
+    if (P.o.rtol_vec > 0) {
       std::vector<int> order(ntask);
       std::iota(order.begin(), order.end(), 0);
       std::stable_sort(order.begin(), order.end(),
@@ -951,7 +984,7 @@ int solve(Problem &P, int64_t *m_out) {
       h2d(dwork, wv.data(), wv.size(), s);
       kt_fin.start(s);
       k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, dlist, slot_j, slo, shi, nullptr, nullptr,
-                                                 0, std::ldexp(1.0, -40), 4000, dfail + 2, ctr + 2,
+                                                 0, P.o.rtol_vec, 4000, dfail + 2, ctr + 2,
                                                  ctr + 1);
       kt_fin.stop(s);
       CK(cudaGetLastError());
@@ -970,7 +1003,7 @@ int solve(Problem &P, int64_t *m_out) {
     A.nodes = dnodes; A.LDv = LDv; A.tasks = dt; A.items = ditems; A.nitems = (int)items.size();
     A.lo = slo; A.hi = shi; A.fck = fck; A.bck = bck; A.ck_stride = ntask + 32; A.ntask = ntask;
     A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam; A.mode = 0; A.ctr = ctr + 8;
-    A.slot_j = slot_j; A.rqc_max = 3;
+    A.slot_j = slot_j; A.rqc_max = std::max(1, P.o.rqc_max);
     int *fail_list = ar.alloc<int>(ntask), *fail_count = ar.alloc<int>(1);
     CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
     A.fail_list = fail_list; A.fail_count = fail_count;
@@ -1058,12 +1091,11 @@ int solve(Problem &P, int64_t *m_out) {
                 hti[t] & 255, hti[t] >> 8);
       }
     }
-    k_output<<<(ntask + 255) / 256, 256, 0, s>>>(dt, ntask, dnodes, lam, 1.0 / scale, P.w);
+    k_output<<<(ntask + 255) / 256, 256, 0, s>>>(dt, ntask, dnodes, lam, 1.0 / scale, w_loc);
     CK(cudaGetLastError());
-    if (m > 1) k_monotone<<<1, 1024, 0, s>>>(P.w, (int)m);
-    CK(cudaGetLastError());
-    g_stats.kernel_launches += 2;
+    g_stats.kernel_launches++;
   }
+  finish_w();
   d2h(h_ctr, ctr, 16, s);
   tr.mark("vectors");
   g_stats.ms_vectors = tv.stop();
@@ -1113,6 +1145,8 @@ void mrrr_default_opts(mrrr_opts_t *o) {
   o->seed = 0x1205210700000000ULL;
   o->multisection = 4;
   o->grid_factor = 4;
+  o->rtol_vec = 0.0;
+  o->rqc_max = 3;
 }
 
 __global__ void k_n1(const double *d, double *w, double *Z) {
@@ -1206,10 +1240,49 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, doub
                     mrrr_allgather_fn allgather, void *allgather_ctx, int64_t *m,
                     const mrrr_opts_t *opts, int64_t *col_begin, int64_t *m_local,
                     double *w_all, double *Z_local, int64_t ldz, void *stream) {
-  (void)n; (void)d; (void)e; (void)range; (void)vl; (void)vu; (void)il; (void)iu; (void)rank;
-  (void)nranks; (void)allgather; (void)allgather_ctx; (void)m; (void)opts; (void)col_begin;
-  (void)m_local; (void)w_all; (void)Z_local; (void)ldz; (void)stream;
-  return MRRR_ERR_COMM;  // implemented in a later milestone
+  int v = validate(n, d, e, range, vl, vu, il, iu, m, w_all, Z_local, ldz);
+  if (v) return v == -9 ? -13 : (v == -10 ? -17 : (v == -12 ? -19 : v));
+  if (nranks < 1) return -10;
+  if (rank < 0 || rank >= nranks) return -9;
+  if (nranks > 1 && !allgather) return -11;
+  if (!col_begin) return -15;
+  if (!m_local) return -16;
+  Problem P;
+  P.n = n; P.d = d; P.e = e; P.range = range; P.vl = vl; P.vu = vu; P.il = il; P.iu = iu;
+  P.w = w_all; P.Z = Z_local; P.ldz = ldz; P.s = (cudaStream_t)stream;
+  P.rank = rank; P.nranks = nranks; P.allgather = allgather; P.ag_ctx = allgather_ctx;
+  P.w_all = w_all;
+  if (opts) P.o = *opts; else mrrr_default_opts(&P.o);
+  try {
+    if (n == 1) {
+      // one eigenpair: rank 0 owns it; w on every rank
+      double dv;
+      CK(cudaMemcpyAsync(&dv, d, sizeof(double), cudaMemcpyDeviceToHost, P.s));
+      CK(cudaStreamSynchronize(P.s));
+      if (!std::isfinite(dv)) return -2;
+      bool in = range != MRRR_RANGE_VALUE || (dv > vl && dv <= vu);
+      *m = in ? 1 : 0;
+      *col_begin = 0;
+      *m_local = (in && rank == 0) ? 1 : 0;
+      if (in) {
+        k_n1<<<1, 1, 0, P.s>>>(d, w_all, rank == 0 ? Z_local : nullptr);
+        CK(cudaGetLastError());
+      }
+      CK(cudaStreamSynchronize(P.s));
+      return 0;
+    }
+    int rc = solve(P, m);
+    CK(cudaStreamSynchronize(P.s));
+    *col_begin = P.col_begin;
+    *m_local = P.m_local;
+    return rc;
+  } catch (const MrrrError &er) {
+    cudaStreamSynchronize(P.s);
+    return er.code;
+  } catch (const CudaError &ce) {
+    cudaGetLastError();
+    return ce.e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;
+  }
 }
 
 int mrrr_trim_workspace(void) {

@@ -21,7 +21,7 @@ RANGE_ALL, RANGE_INDEX, RANGE_VALUE = 0, 1, 2
 class Opts(C.Structure):
     _fields_ = [("tol_relgap", C.c_double), ("rtol_class", C.c_double), ("max_depth", C.c_int),
                 ("perturb_root", C.c_int), ("seed", C.c_uint64), ("multisection", C.c_int),
-                ("grid_factor", C.c_int)]
+                ("grid_factor", C.c_int), ("rtol_vec", C.c_double), ("rqc_max", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -173,6 +173,97 @@ def stemr_host(d, e, *, il=None, iu=None, vl=None, vu=None, w=None, Z=None, vect
         raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
     k = m.value
     return w[:k], (Z[:k].T if vectors else None)
+
+
+def shard_columns(m: int, nranks: int, rank: int):
+    """Columns [c0, c1) of the m wanted eigenpairs owned by `rank` (the static
+    division of PAPER.md L1139-1146 as mrrr_stemr_dist applies it:
+    epp = ceil(m / nranks), c0 = rank * epp)."""
+    epp = (m + nranks - 1) // nranks
+    c0 = min(rank * epp, m)
+    return c0, min(c0 + epp, m)
+
+
+class _DevBuf:
+    """Zero-copy view of a device buffer for torch.as_tensor (fp64)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes // 8,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def _host_view(ptr: int, nbytes: int):
+    arr = (C.c_double * (nbytes // 8)).from_address(ptr)
+    return torch.frombuffer(arr, dtype=torch.float64)
+
+
+def torch_allgather(group=None, device: str = "cuda"):
+    """An mrrr_allgather_fn over torch.distributed: recv[r * bytes ...] <- rank
+    r's send (bytes each).  device="cuda": the library's device buffers, NCCL
+    over NVLink; device="cpu": host buffers (gloo; used by the CPU tests of
+    the exchange).  Returns the ctypes callback (keep a reference while the
+    call runs)."""
+    import torch.distributed as dist
+
+    def fn(ctx, send, recv, nbytes, stream):
+        try:
+            if nbytes == 0:
+                return 0
+            world = dist.get_world_size(group)
+            if device == "cuda":
+                st = torch.as_tensor(_DevBuf(send, nbytes), device="cuda")
+                rt = torch.as_tensor(_DevBuf(recv, nbytes * world), device="cuda")
+                dist.all_gather_into_tensor(rt, st, group=group)
+            else:
+                st = _host_view(send, nbytes)
+                parts = [torch.empty_like(st) for _ in range(world)]
+                dist.all_gather(parts, st, group=group)
+                _host_view(recv, nbytes * world).copy_(torch.cat(parts))
+            return 0
+        except Exception:  # reported as MRRR_ERR_COMM by the library
+            return 1
+    return ALLGATHER_FN(fn)
+
+
+def stemr_dist(d: torch.Tensor, e: torch.Tensor, *, il=None, iu=None, vl=None, vu=None,
+               vectors: bool = True, opts: Opts | None = None, group=None, rank=None,
+               nranks=None, allgather=None, stream=None):
+    """Sharded MRRR (``mrrr_stemr_dist``): every rank passes the same T and
+    range; returns ``(w_all, Z_local, col_begin)`` where ``w_all`` holds all m
+    eigenvalues on every rank and ``Z_local`` (n, m_local) the eigenvectors of
+    columns ``col_begin .. col_begin + m_local`` (this rank's static share).
+    The only collective is the all-gather of w (torch.distributed by default)."""
+    import torch.distributed as dist
+    if not (d.is_cuda and d.dtype == torch.float64):
+        raise TypeError("d must be a torch.float64 CUDA tensor (no CPU fallback)")
+    n = d.shape[0]
+    if rank is None:
+        rank = dist.get_rank(group)
+    if nranks is None:
+        nranks = dist.get_world_size(group)
+    d = d.contiguous()
+    e = e.contiguous() if n > 1 else d
+    rng, a, b, ilv, iuv, kcap = _range_args(n, il, iu, vl, vu)
+    kcap = max(kcap, 1)
+    epp = (kcap + max(nranks, 1) - 1) // max(nranks, 1)
+    w_all = torch.empty(kcap, dtype=torch.float64, device=d.device)
+    Zl = torch.empty((max(epp, 1), n), dtype=torch.float64, device=d.device) if vectors else None
+    if stream is None:
+        stream = torch.cuda.current_stream(d.device)
+    cb = allgather if allgather is not None else torch_allgather(group)
+    m = C.c_int64(0)
+    c0 = C.c_int64(0)
+    ml = C.c_int64(0)
+    o = opts if opts is not None else default_opts()
+    with torch.cuda.device(d.device):
+        rc = lib().mrrr_stemr_dist(n, _ptr(d), _ptr(e), rng, a, b, ilv, iuv, int(rank), int(nranks),
+                                   cb, None, C.byref(m), C.byref(o), C.byref(c0), C.byref(ml),
+                                   _ptr(w_all), _ptr(Zl) if vectors else C.c_void_p(0), n,
+                                   C.c_void_p(stream.cuda_stream))
+    if rc != 0:
+        raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
+    k = m.value
+    return w_all[:k], (Zl[:ml.value].T if vectors else None), c0.value
 
 
 def stemr_raw(n, d, e, rng, vl, vu, il, iu, m_ok=True, w=None, Z=None, ldz=None):

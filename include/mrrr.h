@@ -72,7 +72,7 @@ typedef struct {
   double rtol_vec;     /* singleton brackets refined to this relative width
                           before the RQC; 0 = none (default; reading 10) */
   int rqc_max;         /* twisted factorizations of the RQC before the
-                          bisection fallback; default 3 (reading 10) */
+                          bisection fallback; default 10 (reading 10) */
 } mrrr_opts_t;
 
 void mrrr_default_opts(mrrr_opts_t *opts);

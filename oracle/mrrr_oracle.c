@@ -25,7 +25,7 @@ void oracle_default_opts(oracle_opts_t *o) {
   o->perturb_root = 1;                 /* reading 3 */
   o->seed = 0x1205210700000000ULL;     /* SURVEY §8(b) default seed */
   o->rtol_vec = 0.0;                   /* reading 10 */
-  o->rqc_max = 3;                      /* reading 10 */
+  o->rqc_max = 10;                     /* reading 10 */
 }
 
 /* ------------------------------------------------------------------------ */
@@ -398,7 +398,7 @@ static void singleton(ctx_t *c, const rrr_t *R, int64_t j) {
   int64_t r, nc, nfact = 0;
   double gamma, nrm2 = 1;
   int converged = 0, rs = 0;
-  double *z = c->z;
+  double *z = c->z, delta_prev = INFINITY;
   for (int it = 0; it < (c->o->rqc_max > 0 ? c->o->rqc_max : 1); ++it) {
     twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lam, R->pivmin, &c->ws, z, &r,
                &gamma, &nc, &rs);
@@ -407,11 +407,18 @@ static void singleton(ctx_t *c, const rrr_t *R, int64_t j) {
     nrm2 = 0;
     for (int64_t i = 0; i < nb; ++i) nrm2 += z[i] * z[i];
     double delta = gamma / nrm2;
-    if (fabs(delta) <= 4.0 * EPS * fabs(lam) || lam + delta == lam) {
+    /* stop (reading 10): |delta| <= 4 eps |lambda|, fl(lambda + delta) ==
+     * lambda, or stagnation -- the correction no longer halves (the
+     * Rayleigh-quotient iteration converges cubically; a correction that
+     * stops shrinking sits at the rounding floor of the twisted
+     * factorization) */
+    if (fabs(delta) <= 4.0 * EPS * fabs(lam) || lam + delta == lam ||
+        (it > 0 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
       lam_fin = lam + delta;
       converged = 1;
       break;
     }
+    delta_prev = delta;
     /* safeguard (reading 24, amended): a step leaving [lo,hi] from the
      * interior is clamped to the violated end; from an end it bisects; a
      * bracket of adjacent doubles is converged. */
@@ -465,18 +472,19 @@ static double weighted_growth(int64_t nb, const double *z, const double *Dp) {
 }
 
 /* O9 -- cluster step: shift, child RRR, refine, recurse.
- * Shift choice, reading 9 (amended): candidates at offsets
- * m = 1, 2, 4 beyond each end of the cluster (order L1 R1 L2 R2 L4 R4),
- * raw growth g = max_i |D+_i| (inf if a pivot is not finite or zero),
- * weighted growth wg = max over the parent's two end-eigenvalue vectors z_L,
- * z_R of sum |D+_i| z_i^2 / ||z||^2.  For m = 1, 2, 4 in turn:
- *   (i)  if an end has g <= 8 spdiam: the end with the lower g;
- *   (ii) else if an end has wg <= 64 spdiam: of those ends the lower g.
- * (iii) After all offsets: the least g if <= 1e8 spdiam; else error 2.
- * Ties go to the left end.  Weighting by one vector only, or choosing by the
- * lower wg, admits children whose element growth ruins the accuracy of the
- * cluster's far eigenvalues (Clement n=20000: raw growth 3.5e5 spdiam, RQC
- * corrections 1e3 eps|lambda| at the far end). */
+ * Shift choice, reading 9 (amended): six candidates at offsets
+ * m = 1, 2, 4 beyond each end of the cluster (order L1 R1 L2 R2 L4 R4), all
+ * evaluated; raw growth g = max_i |D+_i| (inf if a pivot is not finite or
+ * zero), weighted growth wg = max over the parent's two end-eigenvalue
+ * vectors z_L, z_R of sum |D+_i| z_i^2 / ||z||^2.
+ *   (i)   some g <= 8 spdiam: the least g among those;
+ *   (ii)  else, the least g among the candidates with wg <= 64 spdiam;
+ *   (iii) else the least g if <= 1e8 spdiam; else error 2.
+ * Ties go to the earlier candidate.  Evidence (oracle, glued Wilkinson
+ * n=21000): the SURVEY rule (lower wg at the first passing offset) gave
+ * orthogonality 2.7x the 10 n eps tolerance, this rule 0.46x; on Clement
+ * n=20000 the SURVEY rule accepted a child with g = 3.5e5 spdiam (RQC
+ * corrections 1e3 eps |lambda| for the far eigenvalues). */
 static void cluster(ctx_t *c, const rrr_t *R, int64_t s, int64_t t, int depth) {
   int64_t nb = R->nb;
   double spd = c->spdiam;
@@ -487,47 +495,37 @@ static void cluster(ctx_t *c, const rrr_t *R, int64_t s, int64_t t, int depth) {
   double *LpA = DpA + (nb + 1), *zL = DpA + 2 * (nb + 1), *zR = DpA + 3 * (nb + 1);
   static const double mult[3] = {1.0, 2.0, 4.0};
   double cs[6], cg[6];
-  double dl = fmax(2.0 * (c->hi[s] - c->lo[s]), 4.0 * EPS * fabs(c->lo[s]));
-  double dr = fmax(2.0 * (c->hi[t] - c->lo[t]), 4.0 * EPS * fabs(c->hi[t]));
-  int best = -1, have_z = 0;
-  for (int mi = 0; mi < 3 && best < 0; ++mi) {
-    int kL = 2 * mi, kR = 2 * mi + 1;
-    cs[kL] = c->lo[s] - mult[mi] * dl;
-    cs[kR] = c->hi[t] + mult[mi] * dr;
-    oracle_child_rrr(nb, R->D, R->L, R->LD, cs[kL], DpA, LpA, &cg[kL]);
-    oracle_child_rrr(nb, R->D, R->L, R->LD, cs[kR], DpA, LpA, &cg[kR]);
-    c->st->child_sweeps += 2;
-    /* (i) */
-    if (fmin(cg[kL], cg[kR]) <= 8.0 * spd) {
-      best = cg[kL] <= cg[kR] ? kL : kR;
-      c->st->tier[0]++;
-      break;
-    }
-    /* (ii) */
-    if (!have_z) {
-      int64_t r, nc;
-      double g;
-      int rs = 0;
-      double lamL = 0.5 * (c->lo[s] + c->hi[s]), lamR = 0.5 * (c->lo[t] + c->hi[t]);
-      twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lamL, R->pivmin, &c->ws, zL, &r, &g, &nc, &rs);
-      twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lamR, R->pivmin, &c->ws, zR, &r, &g, &nc, &rs);
-      have_z = 1;
-    }
-    for (int k = kL; k <= kR; ++k) {
+  /* offset unit (reading 8, amended): twice the end bracket's width, but at
+   * least 2 rtol_c |lambda| -- the width classification guarantees -- so the
+   * shift does not depend on how far below rtol_c a bracket happens to be */
+  double rt2 = 2.0 * c->o->rtol_class;
+  double dl = fmax(fmax(2.0 * (c->hi[s] - c->lo[s]), rt2 * fabs(c->lo[s])), 4.0 * EPS * fabs(c->lo[s]));
+  double dr = fmax(fmax(2.0 * (c->hi[t] - c->lo[t]), rt2 * fabs(c->hi[t])), 4.0 * EPS * fabs(c->hi[t]));
+  int best = -1;
+  for (int mi = 0; mi < 3; ++mi) {
+    cs[2 * mi] = c->lo[s] - mult[mi] * dl;
+    cs[2 * mi + 1] = c->hi[t] + mult[mi] * dr;
+  }
+  for (int k = 0; k < 6; ++k) {
+    oracle_child_rrr(nb, R->D, R->L, R->LD, cs[k], DpA, LpA, &cg[k]);
+    c->st->child_sweeps++;
+    if (cg[k] <= 8.0 * spd && (best < 0 || cg[k] < cg[best])) best = k;
+  }
+  if (best >= 0) c->st->tier[0]++;
+  else {
+    int64_t r, nc;
+    double g;
+    int rs = 0;
+    double lamL = 0.5 * (c->lo[s] + c->hi[s]), lamR = 0.5 * (c->lo[t] + c->hi[t]);
+    twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lamL, R->pivmin, &c->ws, zL, &r, &g, &nc, &rs);
+    twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lamR, R->pivmin, &c->ws, zR, &r, &g, &nc, &rs);
+    for (int k = 0; k < 6; ++k) {
       if (!isfinite(cg[k])) continue;
-      double g;
       oracle_child_rrr(nb, R->D, R->L, R->LD, cs[k], DpA, LpA, &g);
-      c->st->child_sweeps++;
       double wg = fmax(weighted_growth(nb, zL, DpA), weighted_growth(nb, zR, DpA));
       if (wg <= 64.0 * spd && (best < 0 || cg[k] < cg[best])) best = k;
     }
     if (best >= 0) c->st->tier[1]++;
-  }
-  if (best < 0) {
-    for (int k = 0; k < 6; ++k)
-      if (best < 0 || cg[k] < cg[best]) best = k;
-    if (!(cg[best] <= 1e8 * spd)) { c->err = 2; free(DpA); free(C.D); return; }
-    c->st->tier[3]++;
   }
   double sigma;
   sigma = cs[best];

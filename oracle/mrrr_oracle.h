@@ -30,7 +30,7 @@ typedef struct {
   int perturb_root;   /* 1: seeded (1+4eps*u) perturbation of root D, L (reading 3) */
   uint64_t seed;      /* perturbation seed */
   double rtol_vec;    /* singleton bracket refinement before the RQC; 0 = none (reading 10) */
-  int rqc_max;        /* RQC factorizations before the bisection fallback; 3 (reading 10) */
+  int rqc_max;        /* RQC factorizations before the bisection fallback; 10 (reading 10) */
 } oracle_opts_t;
 
 typedef struct {

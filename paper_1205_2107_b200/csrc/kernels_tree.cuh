@@ -669,7 +669,7 @@ struct Cand {
 
 __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0, const int *cl_s1,
                        const double *__restrict__ lo, const double *__restrict__ hi, int ncl,
-                       const double *__restrict__ zbuf, int64_t zstride, Cand *cand) {
+                       const double *__restrict__ zbuf, int64_t zstride, double rtol, Cand *cand) {
   int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= ncl * 6) return;
   int c = id / 6, which = id % 6;
@@ -678,10 +678,12 @@ __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0
   double mult = (double)(1 << (which >> 1));
   double sigma;
   if ((which & 1) == 0) {
-    double dl = fmax(2.0 * (hi[s0] - lo[s0]), 4.0 * kEps * fabs(lo[s0]));
+    // offset unit (reading 8 amended): >= 2 rtol_c |lambda|, independent of
+    // how far below rtol_c the bracket converged
+    double dl = fmax(fmax(2.0 * (hi[s0] - lo[s0]), 2.0 * rtol * fabs(lo[s0])), 4.0 * kEps * fabs(lo[s0]));
     sigma = lo[s0] - mult * dl;
   } else {
-    double dr = fmax(2.0 * (hi[s1] - lo[s1]), 4.0 * kEps * fabs(hi[s1]));
+    double dr = fmax(fmax(2.0 * (hi[s1] - lo[s1]), 2.0 * rtol * fabs(hi[s1])), 4.0 * kEps * fabs(hi[s1]));
     sigma = hi[s1] + mult * dr;
   }
   const double2 *DL = P.DL;
@@ -750,31 +752,27 @@ __global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0
   cand[id] = C;
 }
 
-// Shift choice (O9.3, reading 9 amended).  For offsets m = 1, 2, 4
-// in turn: (i) if an end has raw growth <= 8 spdiam, the end with the lower
-// raw growth; (ii) else if an end has weighted growth <= 64 spdiam, of those
-// ends the lower raw growth.  (iii) After all offsets the least raw growth if
-// <= 1e8 spdiam; else error 2.  Ties go to the left end.
+// Shift choice (O9.3, reading 9 amended): all six candidates;
+// (i) some raw growth <= 8 spdiam: the least raw growth among those; (ii) else
+// the least raw growth among the candidates with weighted growth <= 64
+// spdiam; (iii) else the least raw growth if <= 1e8 spdiam; else error 2.
+// Ties: the earlier candidate (order L1 R1 L2 R2 L4 R4).
 __global__ void k_pick(const Node *nodes, const int *cl_parent, const Cand *cand, int ncl,
                        double *sigma_out, int *tier_out, int *fail) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
   double spd = nodes[cl_parent[c]].spdiam;
   const Cand *C = cand + 6 * c;
-  int best = -1, tier = 0;
-  for (int m = 0; m < 3 && best < 0; ++m) {
-    const Cand &L = C[2 * m], &R = C[2 * m + 1];
-    if (fmin(L.raw, R.raw) <= 8.0 * spd) { best = L.raw <= R.raw ? 2 * m : 2 * m + 1; tier = 0; break; }
-    for (int k = 2 * m; k <= 2 * m + 1; ++k)
-      if (isfinite(C[k].raw) && C[k].wgt <= 64.0 * spd && (best < 0 || C[k].raw < C[best].raw)) best = k;
-    tier = 1;
+  int b1 = -1, b2 = -1, b3 = -1;
+  for (int k = 0; k < 6; ++k) {
+    double g = C[k].raw;
+    if (g <= 8.0 * spd && (b1 < 0 || g < C[b1].raw)) b1 = k;
+    if (isfinite(g) && C[k].wgt <= 64.0 * spd && (b2 < 0 || g < C[b2].raw)) b2 = k;
+    if (b3 < 0 || g < C[b3].raw) b3 = k;
   }
-  if (best < 0) {
-    for (int k = 0; k < 6; ++k)
-      if (best < 0 || C[k].raw < C[best].raw) best = k;
-    tier = 3;
-    if (!(C[best].raw <= 1e8 * spd)) best = -1;
-  }
+  int tier = 0, best = b1;
+  if (best < 0) { tier = 1; best = b2; }
+  if (best < 0) { tier = 3; best = b3; if (!(C[b3].raw <= 1e8 * spd)) best = -1; }
   if (best < 0) {
     sigma_out[c] = 0.0;
     tier_out[c] = 4;

@@ -384,14 +384,18 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
     const int j = A.slot_j[tk.slot];
     bool conv = !active, failed = false;
     Twist best = tw;
-    double lam_best = lam;
+    double lam_best = lam, delta_prev = CUDART_INF;
     for (int it = 1;; ++it) {
       if (!conv) {
         if (tw.negc >= j) { if (lam < hi) hi = lam; } else { if (lam > lo) lo = lam; }
         const double delta = tw.gamma / tw.nrm2;
-        if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam) {
+        // stop (reading 10): |delta| <= 4 eps |lambda|, fl(lambda + delta) ==
+        // lambda, or stagnation (the correction no longer halves)
+        if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam ||
+            (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
           conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
         } else {
+          delta_prev = delta;
           double nw = lam + delta;
           if (nw <= lo || nw >= hi) {
             if (lam == lo || lam == hi) {

@@ -872,7 +872,7 @@ int solve(Problem &P, int64_t *m_out) {
     }
     Cand *cand = ar.alloc<Cand>((size_t)6 * ncl);
     k_cand<<<(6 * ncl + 127) / 128, 128, 0, s>>>(dnodes, dcl_parent, dcl_s0, dcl_s1, slo, shi, ncl,
-                                                 zbuf, nbmax, cand);
+                                                 zbuf, nbmax, P.o.rtol_class, cand);
     CK(cudaGetLastError());
     double *dsig = ar.alloc<double>(ncl);
     int *dtier = ar.alloc<int>(ncl);
@@ -1007,8 +1007,6 @@ int solve(Problem &P, int64_t *m_out) {
     int *fail_list = ar.alloc<int>(ntask), *fail_count = ar.alloc<int>(1);
     CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
     A.fail_list = fail_list; A.fail_count = fail_count;
-    int *tinfo = nullptr;
-    long long *tcyc = nullptr;
     {
       std::vector<Node> hnodes(nnodes);
       d2h(hnodes.data(), dnodes, nnodes, s);
@@ -1063,32 +1061,15 @@ int solve(Problem &P, int64_t *m_out) {
         launch_wvec(false, F, s);
       }
     }
-    if (getenv("MRRR_DEBUG")) {
+    if (getenv("MRRR_DEBUG_TASKS")) {
       std::vector<double> hl(ntask);
       d2h(hl.data(), lam, ntask, s);
       std::vector<Node> hnodes(nnodes);
       d2h(hnodes.data(), dnodes, nnodes, s);
-      std::vector<int> hti(ntask);
-      d2h(hti.data(), tinfo, ntask, s);
-      std::vector<long long> hcy(ntask);
-      d2h(hcy.data(), tcyc, ntask, s);
-      {
-        std::vector<long long> sc(hcy);
-        std::sort(sc.begin(), sc.end());
-        int hist[16] = {0};
-        for (int t = 0; t < ntask; ++t) hist[std::min(hti[t] & 255, 15)]++;
-        fprintf(stderr, "[mrrr] k_vectors cycles per task: p50 %lld p90 %lld p99 %lld max %lld (nb %d)\n",
-                sc[ntask / 2], sc[ntask * 9 / 10], sc[ntask * 99 / 100], sc[ntask - 1], (int)nbmax);
-        fprintf(stderr, "[mrrr] iterations hist:");
-        for (int k = 0; k < 16; ++k) fprintf(stderr, " %d:%d", k, hist[k]);
-        fprintf(stderr, "\n");
-      }
-      if (getenv("MRRR_DEBUG_TASKS") == nullptr) hti.clear();
-      for (int t = 0; t < (int)hti.size(); ++t) {
+      for (int t = 0; t < ntask; ++t) {
         const Node &N = hnodes[tasks[t].node];
-        fprintf(stderr, "task %d slot %d node %d col %ld lam %.17g tau %.17g + %.3g sigma %.17g depth %d it %d fb %d\n", t,
-                tasks[t].slot, tasks[t].node, (long)tasks[t].col, hl[t], N.tau_hi, N.tau_lo, N.sigma, N.depth,
-                hti[t] & 255, hti[t] >> 8);
+        fprintf(stderr, "task %d slot %d node %d col %ld lam %.17g tau %.17g + %.3g sigma %.17g depth %d\n", t,
+                tasks[t].slot, tasks[t].node, (long)tasks[t].col, hl[t], N.tau_hi, N.tau_lo, N.sigma, N.depth);
       }
     }
     k_output<<<(ntask + 255) / 256, 256, 0, s>>>(dt, ntask, dnodes, lam, 1.0 / scale, w_loc);
@@ -1146,7 +1127,7 @@ void mrrr_default_opts(mrrr_opts_t *o) {
   o->multisection = 4;
   o->grid_factor = 4;
   o->rtol_vec = 0.0;
-  o->rqc_max = 3;
+  o->rqc_max = 10;
 }
 
 __global__ void k_n1(const double *d, double *w, double *Z) {

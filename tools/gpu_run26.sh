@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || cd /root/repo
+mkdir -p gpurun_out
+MRRR_DEBUG=1 MRRR_DEBUG_TASKS=1 timeout 600 python tools/diag_orth.py glued_wilkinson_21000 > gpurun_out/r26_glued.log 2> gpurun_out/r26_glued.err
+timeout 600 python tools/diag_orth.py clement_50000 > gpurun_out/r26_clem.log 2>&1
+gzip -f gpurun_out/r26_glued.err
+exit 0

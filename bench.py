@@ -42,10 +42,10 @@ from paper_1205_2107_b200 import workloads as W  # noqa: E402
 EPS = 2.0 ** -52
 # FP64 ALU peak: 148 SMs x 64 FP64 FMA lanes x 2 flop x 1.965 GHz
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
-# algorithmic work model: flops per matrix element
+# algorithmic work model, in FP64-pipe slots
 R_RQC = 3                   # twisted factorizations per eigenpair (yardstick)
-FLOPS_TWIST = 15 * R_RQC + 1  # per element per eigenpair: 15 per factorization+solve, +1 scale
-FLOPS_STURM = 4             # per element per bisection step (add, div, mul, sub)
+W_DIV = 1.708e13 / 1.2945e12  # measured DFMA/s / IEEE DDIV/s (profiles/r01_microbench_fp64.json)
+HBM_GBS = 6554.6            # MEASURED_PEAKS.json hbm_gbs (Z write bound)
 RTOL_C = 2.0 ** -20
 METRIC = "STEP eigenpairs/sec fp64 (n=20k, all pairs) at 1/2/4/8 B200; % of roofline"
 
@@ -231,6 +231,7 @@ def main():
            for _ in range(args.steps)]
     clk = Clocks(dev.index or 0)
     clk.start()
+    time.sleep(1.0)  # let the sampler start before the timed region (host-side orchestration)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -254,19 +255,20 @@ def main():
     # whole job: the m eigenpairs of a step are computed once across the ranks
     value = m * args.steps / (tot_ms / 1e3)
 
-    # ---------------- roofline of the dominant kernel
+    # ---------------- roofline (SURVEY §8(d) work model)
+    # FP64-pipe slots: a bisection step costs 2 + w_div per element, a
+    # twisted factorization + solve 10 + 2 w_div, the final scale 1; R = 3
+    # factorizations per eigenpair is the fixed yardstick.  Reported as
+    # TFLOP/s with one slot = one DFMA = 2 flops (peak 37.2 TFLOP/s).
     w_host = wk.double().cpu().numpy()
-    kv = [s["ms_k_vectors"] for s in stats]
-    kb = [s["ms_k_root_bisect"] for s in stats]
+    kv = statistics.mean(s["ms_k_vectors"] for s in stats)
+    kb = statistics.mean(s["ms_k_root_bisect"] for s in stats)
     B = bisection_steps(d, e, w_host)
-    flops_bis = float(np.sum(B)) * FLOPS_STURM * n
-    flops_vec = stats[-1]["vec_elems"] * FLOPS_TWIST
-    mv, mb = statistics.mean(kv), statistics.mean(kb)
-    if mv >= mb:
-        dom, flops, kms = "k_vectors", flops_vec, mv
-    else:
-        dom, flops, kms = "k_root_bisect", flops_bis, mb
-    achieved = flops / (kms / 1e3) / 1e12
+    slots_bis = float(np.sum(B)) * (2 + W_DIV) * n
+    slots_vec = stats[-1]["vec_elems"] * (R_RQC * (10 + 2 * W_DIV) + 1)
+    # the dominant kernel carrying algorithmic work: the singleton vectors
+    dom, slots, kms = "k_wvectors", slots_vec, kv
+    achieved = 2 * slots / (kms / 1e3) / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
@@ -274,15 +276,18 @@ def main():
             traffic = json.load(open(tf)).get(args.config, {}).get(dom)
         except Exception:
             traffic = None
+    # whole step against T_roof = max(W_slots / P64, 8 n k / BW)
+    w_slots = (float(np.sum(B)) * (2 + W_DIV) + m * (R_RQC * (10 + 2 * W_DIV) + 1)) * n
+    t_roof = max(w_slots / (FP64_PEAK_TFLOPS * 1e12 / 2), 8.0 * n * m / (HBM_GBS * 1e9))
     roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
             "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
             "kernel_ms": kms, "kernel_share_of_step": kms / (tot_ms / args.steps),
-            "algorithmic_flops_per_launch": flops,
-            "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §5)",
-            "other_kernel": {"k_root_bisect" if dom == "k_vectors" else "k_vectors":
-                             {"ms": mb if dom == "k_vectors" else mv,
-                              "achieved_tflops": (flops_bis / (mb / 1e3) / 1e12) if dom == "k_vectors"
-                              else (flops_vec / (mv / 1e3) / 1e12)}}}
+            "algorithmic_slots_per_launch": slots, "w_div": W_DIV,
+            "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 1.965 GHz = 1.861e13 slots/s, x2 flop "
+                           "(guide unit counts; microbenchmark 1.708e13 DFMA/s)",
+            "root_bisect": {"ms": kb, "achieved_tflops": 2 * slots_bis / (kb / 1e3) / 1e12 if kb else None},
+            "step": {"w_slots": w_slots, "t_roof_ms": 1e3 * t_roof,
+                     "frac": 1e3 * t_roof / (tot_ms / args.steps)}}
 
     # ---------------- end to end through the host-buffer C ABI
     e2e = None
@@ -317,6 +322,11 @@ def main():
                "h2d_bytes_per_step": 8 * (2 * n - 1), "d2h_bytes_per_step": 8 * m + 8 * n * (c1 - c0),
                "ms_per_step": etot / args.steps, "note": "d2h per rank: all w + own Z columns"}
     if not args.no_e2e and world == 1:
+        # the host entry allocates its own device buffers: release the
+        # device-resident ones first (Z is 80 GB at n = 1e5)
+        del Z, w
+        torch.cuda.empty_cache()
+        P.trim_workspace()
         dh = torch.tensor(d).pin_memory()
         eh = torch.tensor(e).pin_memory()
         wh = torch.empty(k, dtype=torch.float64).pin_memory()

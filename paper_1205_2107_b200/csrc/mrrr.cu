@@ -843,26 +843,28 @@ int solve(Problem &P, int64_t *m_out) {
       CK(cudaMemcpyAsync(nn, dnodes, nnodes * sizeof(Node), cudaMemcpyDeviceToDevice, s));
       dnodes = nn; node_cap = ncap;
     }
-    int *dcl_parent = ar.alloc<int>(ncl), *dcl_s0 = ar.alloc<int>(ncl), *dcl_s1 = ar.alloc<int>(ncl);
+    // per-level scratch, released (to the library pool) at the end of the level
+    DevArena lv(s);
+    int *dcl_parent = lv.alloc<int>(ncl), *dcl_s0 = lv.alloc<int>(ncl), *dcl_s1 = lv.alloc<int>(ncl);
     h2d(dcl_parent, cl_parent.data(), ncl, s);
     h2d(dcl_s0, cl_s0.data(), ncl, s);
     h2d(dcl_s1, cl_s1.data(), ncl, s);
     // tier-(ii) vectors: parent twisted solve at both end eigenvalues
-    double *zbuf = ar.alloc<double>((size_t)2 * ncl * nbmax);
+    double *zbuf = lv.alloc<double>((size_t)2 * ncl * nbmax);
     {
       std::vector<VecTask> zt(2 * ncl);
       for (int c = 0; c < ncl; ++c) {
         zt[2 * c] = {cl_s0[c], cl_parent[c], 2 * c, NAN};
         zt[2 * c + 1] = {cl_s1[c] - 1, cl_parent[c], 2 * c + 1, NAN};
       }
-      VecTask *dzt = ar.alloc<VecTask>(zt.size());
+      VecTask *dzt = lv.alloc<VecTask>(zt.size());
       h2d(dzt, zt.data(), zt.size(), s);
       const int ntask = (int)zt.size();
       const int nseg = (int)((nbmax + kSeg - 1) / kSeg);
-      FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg * (ntask + 32));
-      BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg * (ntask + 32));
+      FwdCk *fck = lv.alloc<FwdCk>((size_t)nseg * (ntask + 32));
+      BwdCk *bck = lv.alloc<BwdCk>((size_t)nseg * (ntask + 32));
       auto items = make_warp_items(zt);
-      WarpItem *ditems = ar.alloc<WarpItem>(items.size());
+      WarpItem *ditems = lv.alloc<WarpItem>(items.size());
       h2d(ditems, items.data(), items.size(), s);
       WVecArgs A{};
       A.nodes = dnodes; A.LDv = LDv; A.tasks = dzt; A.items = ditems; A.nitems = (int)items.size();
@@ -870,18 +872,18 @@ int solve(Problem &P, int64_t *m_out) {
       A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1; A.ctr = ctr + 4; A.slot_j = slot_j;
       launch_wvec(true, A, s);
     }
-    Cand *cand = ar.alloc<Cand>((size_t)6 * ncl);
+    Cand *cand = lv.alloc<Cand>((size_t)6 * ncl);
     k_cand<<<(6 * ncl + 127) / 128, 128, 0, s>>>(dnodes, dcl_parent, dcl_s0, dcl_s1, slo, shi, ncl,
                                                  zbuf, nbmax, P.o.rtol_class, cand);
     CK(cudaGetLastError());
-    double *dsig = ar.alloc<double>(ncl);
-    int *dtier = ar.alloc<int>(ncl);
+    double *dsig = lv.alloc<double>(ncl);
+    int *dtier = lv.alloc<int>(ncl);
     k_pick<<<(ncl + 127) / 128, 128, 0, s>>>(dnodes, dcl_parent, cand, ncl, dsig, dtier, dfail + 1);
     CK(cudaGetLastError());
     g_stats.child_sweeps += 6 * ncl + ncl;
-    double2 *pool = ar.alloc<double2>((size_t)ncl * nbmax);
-    double *ctb = ar.alloc<double>((size_t)ncl * nbmax);
-    int *csb = ar.alloc<int>((size_t)ncl * nbmax);
+    double2 *pool = ar.alloc<double2>((size_t)ncl * nbmax);  // child RRRs live until the vectors
+    double *ctb = lv.alloc<double>((size_t)ncl * nbmax);
+    int *csb = lv.alloc<int>((size_t)ncl * nbmax);
     k_child_chain<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, dcl_parent, dsig, ncl, nbmax, ctb, csb);
     CK(cudaGetLastError());
     dim3 gfin((unsigned)std::min<int64_t>((nbmax + 255) / 256, 64), ncl);
@@ -898,7 +900,7 @@ int solve(Problem &P, int64_t *m_out) {
     for (int c = 0; c < ncl; ++c)
       for (int q = cl_s0[c]; q < cl_s1[c]; ++q) { slot_cl.push_back(c); first_slot.push_back(q); }
     int nsn = (int)slot_cl.size();
-    int *dslot_cl = ar.alloc<int>(nsn), *dfirst = ar.alloc<int>(nsn);
+    int *dslot_cl = lv.alloc<int>(nsn), *dfirst = lv.alloc<int>(nsn);
     h2d(dslot_cl, slot_cl.data(), nsn, s);
     h2d(dfirst, first_slot.data(), nsn, s);
     k_translate<<<(nsn + 127) / 128, 128, 0, s>>>(dslot_cl, dfirst, nsn, dsig, slo, shi, wlo, whi,
@@ -918,7 +920,7 @@ int solve(Problem &P, int64_t *m_out) {
     // a cluster depends on the cluster alone, so every rank that holds a
     // shared cluster computes bitwise the same child intervals (§8(e))
     for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], kTreeChunk, wv);
-    Work *dwork = ar.alloc<Work>(wv.size());
+    Work *dwork = lv.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
     k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, nullptr, slot_j, slo, shi, wlo, whi, 1,
                                                P.o.rtol_class, 4000, dfail + 2, ctr + 2, ctr + 1);

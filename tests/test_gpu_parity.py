@@ -288,3 +288,50 @@ def test_config4_clement_50000(torch_cuda, P, oracle_mod, subset):
     ok = dk_comparable(wo, residuals(d, e, w[:3], Zs[:, :3]), residuals(d, e, wo, Zo))
     assert ok.all()
     assert np.max(vec_diff_signfree(Zs[:, :3], Zo)) <= 1e-9
+
+
+def test_config5_random_100000(torch_cuda, P, oracle_mod):
+    """configs[4] on one GPU (Z = 80 GB): residual of every column, orthogonality
+    on sampled 2048-column blocks (diagonal blocks every 8th block, adjacent
+    pairs, seeded random pairs), Sturm placement of sampled
+    eigenvalues with an independent count, oracle index windows."""
+    torch = torch_cuda
+    n = 100000
+    d, e = W.random_uniform(n, 0)
+    dd, ee = torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda")
+    wt, Zt = P.stemr(dd, ee)
+    tn = tnorm1(d, e)
+    B = 2048
+    res = 0.0
+    for a in range(0, n, B):
+        Zb = Zt[:, a:a + B]
+        TZ = dd[:, None] * Zb
+        TZ[1:] += ee[:, None] * Zb[:-1]
+        TZ[:-1] += ee[:, None] * Zb[1:]
+        R = TZ - Zb * wt[None, a:a + B]
+        res = max(res, float(torch.linalg.vector_norm(R, dim=0).max()))
+        del TZ, R
+    assert res / tn <= 10 * n * EPS, res / tn / (10 * n * EPS)
+    rng = np.random.default_rng(7)
+    nbk = (n + B - 1) // B
+    pairs = [(i, i) for i in range(0, nbk, 8)] + [(i, i + 1) for i in range(0, nbk - 1, 6)]
+    pairs += [tuple(sorted(rng.choice(nbk, 2, replace=False))) for _ in range(16)]
+    orth = 0.0
+    for bi, bj in pairs:
+        G = Zt[:, bi * B:(bi + 1) * B].T @ Zt[:, bj * B:(bj + 1) * B]
+        if bi == bj:
+            G.diagonal().sub_(1.0)
+        orth = max(orth, float(G.abs().max()))
+    assert orth <= 10 * n * EPS, orth / (10 * n * EPS)
+    w = wt.cpu().numpy()
+    assert np.all(np.diff(w) >= 0)
+    assert abs(w.sum() - d.sum()) <= n * 4 * n * EPS * tn
+    idx = np.sort(rng.choice(n, 64, replace=False))
+    assert sturm_placement(d, e, w[idx], idx, 4 * n * EPS * tn)
+    for il, iu in [(1, 12), (50001, 50012), (99989, 100000)]:
+        wo, Zo = oracle_mod.stemr(d, e, il=il, iu=iu)
+        assert np.max(np.abs(w[il - 1:iu] - wo)) <= 4 * n * EPS * tn
+        Zs = Zt[:, il - 1:iu].cpu().numpy()
+        ok = dk_comparable(wo, residuals(d, e, w[il - 1:iu], Zs), residuals(d, e, wo, Zo))
+        if ok.any():
+            assert np.max(vec_diff_signfree(Zs[:, ok], Zo[:, ok])) <= 1e-9

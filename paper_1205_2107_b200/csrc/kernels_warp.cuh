@@ -197,6 +197,64 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
   return tw;
 }
 
+// Fixed-twist factorization of every lane at its own (lambda, r): forward
+// rows 0..r-1 (ascending tiles up to the warp's largest r) and backward rows
+// nb-2..r (descending tiles down to the smallest r), each lane stepping only
+// its own rows; writes the checkpoints the solve needs (forward segments
+// below r, backward segments from r up).  No argmin, no replay: one pass of
+// simple steps per direction.
+__device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int r, bool active) {
+  const int nb = W.nb;
+  Fwd F{-lam, 1.0, 0.0, 0};
+  Bwd B{__ldg(&W.DL[nb - 1]).x - lam, 1.0, 0.0, 0};
+  // an idle lane steps no rows and does not widen the warp's tile ranges
+  const int rf = active ? r : 0;        // forward rows [0, rf)
+  const int rb = active ? r : nb - 1;   // backward steps into rows [rb, nb - 1)
+  const VecCtx X{nullptr, nullptr, nb, W.nseg, W.fck, W.bck, W.ck_stride};
+  // ---- forward: tiles 0 .. (max r - 1) / kTR
+  const int cf = warp_max(rf > 0 ? (rf - 1) / kTR : -1);
+  w_tiles_up(W, 0, cf, [&](int c, int slot) {
+    const int r0 = c * kTR;
+    if (r0 < rf) put_fck(X, c, W.tix, F);
+#pragma unroll
+    for (int k = 0; k < kTR; ++k) {
+      const Row R = w_row(W, slot, k);
+      if (r0 + k < rf) F.step_r(R, lam, (k & 7) == 7);
+    }
+  });
+  // ---- backward: tiles nseg-1 .. r / kTR
+  const int cb = warp_min(rb / kTR);
+  w_tiles_down(W, W.nseg - 1, cb, [&](int c, int slot) {
+    const int r0 = c * kTR;
+    const int top = min(r0 + kTR, nb) - 1;  // rows r0 .. top in this tile
+    if (c >= rb / kTR) {
+      BwdCk bk; bk.a = B.a; bk.b = B.b;    // state at row min(r0 + kTR, nb - 1)
+      W.bck[(int64_t)c * W.ck_stride + W.tix] = bk;
+    }
+    if (top - r0 + 1 == kTR && top < nb - 1) {
+#pragma unroll
+      for (int k = kTR - 1; k >= 0; --k) {
+        const Row R = w_row(W, slot, k);
+        if (r0 + k >= rb) B.step_r(R, lam, (k & 7) == 0);
+      }
+    } else {
+      for (int k = top - r0; k >= 0; --k) {
+        const int i = r0 + k;
+        if (i < nb - 1 && i >= rb) B.step_r(w_row(W, slot, k), lam, (k & 7) == 0);
+      }
+    }
+  });
+  const double qb = F.q * B.b;
+  const double N = fma(F.p, B.b, fma(B.a, F.q, lam * qb));
+  Twist tw;
+  tw.r = r;
+  tw.gamma = N / qb;
+  tw.nrm2 = 1.0 + F.H / (F.q * F.q) + B.K / (B.b * B.b);
+  tw.negc = F.neg + B.neg + ((tw.gamma < 0.0) ? 1 : 0);
+  tw.ok = isfinite(tw.gamma) && isfinite(tw.nrm2) && qb != 0.0;
+  return tw;
+}
+
 // Each lane writes its chunk rows [a, b] (values sA[0 .. b-a][lane]) to its
 // own column: 16-byte stores when the chunk start is 16-byte aligned.
 __device__ __forceinline__ void w_flush(const WarpCtx &W, int a, int b, double *col) {
@@ -239,7 +297,7 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
     auto rep = [&](int k) {
       const Row R = w_row(W, slot, k);
       const double t = fma(R.D, G.q, G.p);
-      S.sA[k][L] = -R.LD * (G.q * __drcp_rn(t));  // z_i / z_{i+1}
+      S.sA[k][L] = -R.LD * (G.q * rcp_nr(t));  // z_i / z_{i+1}
       S.sC[k][L] = R.LD;
       G.p = fma(-lam, t, R.LLD * G.p);
       G.q = t;
@@ -277,7 +335,7 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
     auto rep = [&](int k) {
       const Row R = w_row(W, slot, k);
       const double u = fma(R.LLD, G.b, G.a);
-      S.sA[k][L] = -R.LD * (G.b * __drcp_rn(u));  // z_{i+1} / z_i
+      S.sA[k][L] = -R.LD * (G.b * rcp_nr(u));  // z_{i+1} / z_i
       S.sC[k][L] = R.LD;
       G.a = fma(-lam, u, R.D * G.a);
       G.b = u;
@@ -384,6 +442,7 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
     const int j = A.slot_j[tk.slot];
     bool conv = !active, failed = false;
     Twist best = tw;
+    const int best_r0 = tw.r;
     double lam_best = lam, delta_prev = CUDART_INF;
     for (int it = 1;; ++it) {
       if (!conv) {
@@ -411,7 +470,8 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
         if (conv) W.tix = spare;  // park: later factorizations must not touch its checkpoints
       }
       if (__all_sync(0xffffffffu, conv)) break;
-      tw = w_twist_full(W, lam);
+      // later iterations keep the first factorization's twist index
+      tw = w_twist_fixed(W, lam, best_r0, !conv);
       ++nfact;
       if (!conv && !tw.ok) { conv = true; failed = true; W.tix = spare; }
     }

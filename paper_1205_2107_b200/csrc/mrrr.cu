@@ -16,6 +16,7 @@
 #include "kernels_tree.cuh"
 #include "kernels_vec.cuh"
 #include "kernels_warp.cuh"
+#include "kernels_child.cuh"
 
 using namespace mrrr;
 
@@ -872,24 +873,20 @@ int solve(Problem &P, int64_t *m_out) {
       A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1; A.ctr = ctr + 4; A.slot_j = slot_j;
       launch_wvec(true, A, s);
     }
-    Cand *cand = lv.alloc<Cand>((size_t)6 * ncl);
-    k_cand<<<(6 * ncl + 127) / 128, 128, 0, s>>>(dnodes, dcl_parent, dcl_s0, dcl_s1, slo, shi, ncl,
-                                                 zbuf, nbmax, P.o.rtol_class, cand);
-    CK(cudaGetLastError());
     double *dsig = lv.alloc<double>(ncl);
     int *dtier = lv.alloc<int>(ncl);
-    k_pick<<<(ncl + 127) / 128, 128, 0, s>>>(dnodes, dcl_parent, cand, ncl, dsig, dtier, dfail + 1);
-    CK(cudaGetLastError());
-    g_stats.child_sweeps += 6 * ncl + ncl;
     double2 *pool = ar.alloc<double2>((size_t)ncl * nbmax);  // child RRRs live until the vectors
-    double *ctb = lv.alloc<double>((size_t)ncl * nbmax);
-    int *csb = lv.alloc<int>((size_t)ncl * nbmax);
-    k_child_chain<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, dcl_parent, dsig, ncl, nbmax, ctb, csb);
-    CK(cudaGetLastError());
-    dim3 gfin((unsigned)std::min<int64_t>((nbmax + 255) / 256, 64), ncl);
-    k_child_finish<<<gfin, 256, 0, s>>>(dnodes, dcl_parent, nullptr, ncl, nbmax, ctb, csb, LDv, pool,
-                                        dfail + 1);
-    CK(cudaGetLastError());
+    {
+      ChildArgs C{};
+      C.nodes = dnodes; C.cl_parent = dcl_parent; C.cl_s0 = dcl_s0; C.cl_s1 = dcl_s1;
+      C.lo = slo; C.hi = shi; C.zbuf = zbuf; C.zstride = nbmax; C.LDv = LDv; C.ncl = ncl;
+      C.rtol = P.o.rtol_class; C.pool = pool; C.stride = nbmax; C.sigma_out = dsig;
+      C.tier_out = dtier; C.fail = dfail + 1;
+      k_child_warp<<<(ncl + kCWarps - 1) / kCWarps, 32 * kCWarps, 0, s>>>(C);
+      CK(cudaGetLastError());
+      g_stats.kernel_launches++;
+    }
+    g_stats.child_sweeps += 6 * ncl + ncl;
     // the child node entries are written before the translate kernel reads sigma
     int *slot_jl = slot_j;
     k_child_nodes<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, node_base, dcl_parent, dcl_s0, dcl_s1, dsig,
@@ -906,7 +903,7 @@ int solve(Problem &P, int64_t *m_out) {
     k_translate<<<(nsn + 127) / 128, 128, 0, s>>>(dslot_cl, dfirst, nsn, dsig, slo, shi, wlo, whi,
                                                   slot_node, node_base);
     CK(cudaGetLastError());
-    g_stats.kernel_launches += 6;
+    g_stats.kernel_launches += 2;
     // host mirror
     hn.resize(nnodes + ncl);
     for (int c = 0; c < ncl; ++c) {
@@ -935,7 +932,6 @@ int solve(Problem &P, int64_t *m_out) {
       snprintf(nm, sizeof nm, "L%d_s0.bin", level); dump(nm, dcl_s0, ncl, s);
       snprintf(nm, sizeof nm, "L%d_s1.bin", level); dump(nm, dcl_s1, ncl, s);
       snprintf(nm, sizeof nm, "L%d_parent.bin", level); dump(nm, dcl_parent, ncl, s);
-      snprintf(nm, sizeof nm, "L%d_cand.bin", level); dump(nm, cand, (size_t)6 * ncl, s);
       snprintf(nm, sizeof nm, "L%d_zbuf.bin", level); dump(nm, zbuf, (size_t)2 * ncl * nbmax, s);
       snprintf(nm, sizeof nm, "L%d_lo.bin", level); dump(nm, slo, nslots, s);
       snprintf(nm, sizeof nm, "L%d_hi.bin", level); dump(nm, shi, nslots, s);

@@ -62,8 +62,9 @@ __device__ __forceinline__ void w_tiles_up(const WarpCtx &W, int c0, int c1, F &
   for (int c = c0; c <= c1; ++c) {
     __pipeline_wait_prior(kRing - 2);
     __syncwarp();
-    f(c, c % kRing);
+    const bool stop = f(c, c % kRing);
     __syncwarp();
+    if (__any_sync(0xffffffffu, stop)) break;  // warp-uniform early end (truncated solves)
     const int cn = c + kRing - 1;
     w_issue(W, cn <= c1 ? cn : -1, cn % kRing);
   }
@@ -79,8 +80,9 @@ __device__ __forceinline__ void w_tiles_down(const WarpCtx &W, int c1, int c0, F
   for (int c = c1; c >= c0; --c) {
     __pipeline_wait_prior(kRing - 2);
     __syncwarp();
-    f(c, c % kRing);
+    const bool stop = f(c, c % kRing);
     __syncwarp();
+    if (__any_sync(0xffffffffu, stop)) break;  // warp-uniform early end (truncated solves)
     const int cn = c - (kRing - 1);
     w_issue(W, cn >= c0 ? cn : -1, (cn + 64 * kRing) % kRing);
   }
@@ -119,6 +121,7 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
     } else {
       for (int k = 0; k < rows; ++k) F.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
     }
+    return false;
   });
   bool ok = isfinite(F.p) && isfinite(F.q);
   // ---- backward (progressive) sweep with replay and argmin |gamma|
@@ -186,6 +189,7 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
         eval(k);
       }
     }
+    return false;
   });
   ok &= isfinite(B.a) && isfinite(B.b) && have;
   Twist tw;
@@ -200,18 +204,23 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
 // Fixed-twist factorization of every lane at its own (lambda, r): forward
 // rows 0..r-1 (ascending tiles up to the warp's largest r) and backward rows
 // nb-2..r (descending tiles down to the smallest r), each lane stepping only
-// its own rows; writes the checkpoints the solve needs (forward segments
-// below r, backward segments from r up).  No argmin, no replay: one pass of
-// simple steps per direction.
-__device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int r, bool active) {
+// its own rows.  No argmin, no replay: one pass of simple steps per
+// direction.  With `col` (per lane, may be null) the z
+// multipliers are stored on the way: col[i] = z_i / z_{i+1} = -LD_i q_i / t_i
+// for i < r and col[i+1] = z_{i+1} / z_i = -LD_i b_{i+1} / u_{i+1} for i >= r,
+// so the eigenvector needs no further sweep (w_ratio_solve).
+__device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int r, bool active,
+                                               double *col = nullptr) {
   const int nb = W.nb;
   Fwd F{-lam, 1.0, 0.0, 0};
   Bwd B{__ldg(&W.DL[nb - 1]).x - lam, 1.0, 0.0, 0};
   // an idle lane steps no rows and does not widen the warp's tile ranges
   const int rf = active ? r : 0;        // forward rows [0, rf)
   const int rb = active ? r : nb - 1;   // backward steps into rows [rb, nb - 1)
+  const bool st = active && col != nullptr;
   const VecCtx X{nullptr, nullptr, nb, W.nseg, W.fck, W.bck, W.ck_stride};
-  // ---- forward: tiles 0 .. (max r - 1) / kTR
+  // ---- forward: tiles 0 .. (max r - 1) / kTR; checkpoints of the segments
+  // below r (the replayed solve reads them)
   const int cf = warp_max(rf > 0 ? (rf - 1) / kTR : -1);
   w_tiles_up(W, 0, cf, [&](int c, int slot) {
     const int r0 = c * kTR;
@@ -219,8 +228,17 @@ __device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int
 #pragma unroll
     for (int k = 0; k < kTR; ++k) {
       const Row R = w_row(W, slot, k);
-      if (r0 + k < rf) F.step_r(R, lam, (k & 7) == 7);
+      if (r0 + k < rf) {
+        const double t = fma(R.D, F.q, F.p);
+        if (st) col[r0 + k] = -R.LD * (F.q * rcp_nr(t));
+        F.neg += negbit(t, F.q);
+        F.H = R.LD2 * fma(F.q, F.q, F.H);
+        F.p = fma(-lam, t, R.LLD * F.p);
+        F.q = t;
+        if ((k & 7) == 7) fwd_rescale(F.p, F.q, F.H);
+      }
     }
+    return false;
   });
   // ---- backward: tiles nseg-1 .. r / kTR
   const int cb = warp_min(rb / kTR);
@@ -231,18 +249,27 @@ __device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int
       BwdCk bk; bk.a = B.a; bk.b = B.b;    // state at row min(r0 + kTR, nb - 1)
       W.bck[(int64_t)c * W.ck_stride + W.tix] = bk;
     }
+    auto bstep = [&](int k) {
+      const Row R = w_row(W, slot, k);
+      const double u = fma(R.LLD, B.b, B.a);
+      if (st) col[r0 + k + 1] = -R.LD * (B.b * rcp_nr(u));
+      B.neg += negbit(u, B.b);
+      B.K = R.LD2 * fma(B.b, B.b, B.K);
+      B.a = fma(-lam, u, R.D * B.a);
+      B.b = u;
+      if ((k & 7) == 0) bwd_rescale(B.a, B.b, B.K);
+    };
     if (top - r0 + 1 == kTR && top < nb - 1) {
 #pragma unroll
-      for (int k = kTR - 1; k >= 0; --k) {
-        const Row R = w_row(W, slot, k);
-        if (r0 + k >= rb) B.step_r(R, lam, (k & 7) == 0);
-      }
+      for (int k = kTR - 1; k >= 0; --k)
+        if (r0 + k >= rb) bstep(k);
     } else {
       for (int k = top - r0; k >= 0; --k) {
         const int i = r0 + k;
-        if (i < nb - 1 && i >= rb) B.step_r(w_row(W, slot, k), lam, (k & 7) == 0);
+        if (i < nb - 1 && i >= rb) bstep(k);
       }
     }
+    return false;
   });
   const double qb = F.q * B.b;
   const double N = fma(F.p, B.b, fma(B.a, F.q, lam * qb));
@@ -278,8 +305,12 @@ __device__ __forceinline__ void w_flush(const WarpCtx &W, int a, int b, double *
 // The ratios q_i / t_i (left) and b_{i+1} / u_{i+1} (right) are formed during
 // the replay with correctly rounded reciprocals (off the z recurrence), so
 // the z loops are pure multiply chains.
+// trunc: stop a side once every lane's |z| fell below 2^-100 (the rows not
+// written keep the caller's zeros); used for the probes, whose vectors only
+// weight the growth test, never for Z.
 __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int r, double scale, double *col,
-                                              bool active) {
+                                              bool active, bool trunc = false) {
+  constexpr double kNeg = 7.888609052210118e-31;  // 2^-100
   const int nb = W.nb, L = W.lane;
   WarpSmem &S = *W.sm;
   if (active) col[r] = scale;
@@ -309,15 +340,27 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
     } else if (on) {
       for (int k = 0; k < r1 - r0; ++k) rep(k);
     }
-    for (int k = r1 - r0 - 1; k >= 0; --k) {
+    // branch-free: the zero-component rule (row i+1 of (LDL^T - lambda I) z
+    // = 0 gives z_i = -(LD_{i+1} / LD_i) z_{i+2}) is evaluated every row and
+    // selected, so no division slow path splits the unrolled block
+    auto zstep = [&](int k) {
       const double ld = S.sC[k][L];
-      double zi = S.sA[k][L] * z1;
-      if (z1 == 0.0) zi = -(ldn / ld) * z2;  // row i+1 of (LDL^T - lambda I) z = 0
-      if (!(fabs(zi) >= kTiny)) zi = 0.0;
+      const double za = S.sA[k][L] * z1;
+      const double zb = -(ldn * rcp_nr(ld)) * z2;
+      double zi = (z1 != 0.0) ? za : zb;
+      zi = (fabs(zi) >= kTiny) ? zi : 0.0;
       S.sA[k][L] = zi * scale;
       z2 = z1; z1 = zi; ldn = ld;
+    };
+    if (r1 - r0 == kTR) {
+#pragma unroll
+      for (int k = kTR - 1; k >= 0; --k) zstep(k);
+    } else {
+      for (int k = r1 - r0 - 1; k >= 0; --k) zstep(k);
     }
     w_flush(W, r0, r1 - 1, col);  // chunk rows r0 .. r1-1 from sA[0 ..]
+    const bool done = !active || r == 0 || (on && fabs(z1) < kNeg && fabs(z2) < kNeg);
+    return trunc && __all_sync(0xffffffffu, done);
   });
   // ---- right part, rows i > r, ascending: z_{i+1} = -LD_i (b_{i+1} / u_{i+1}) z_i
   const int cfirst = (active && r < nb - 1) ? r / kTR : W.nseg;
@@ -349,16 +392,24 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
     }
     // z_{i+1} for i in [lo_i, top): chunk rows lo_i+1 .. top, stored at sA[i - lo_i]
     // (ascending i: index i - lo_i <= i - r0 was already read)
-    for (int i = lo_i; i < top; ++i) {
-      const int k = i - r0;
+    auto ystep = [&](int k, int o) {
       const double ld = S.sC[k][L];
-      double zn = S.sA[k][L] * y1;
-      if (y1 == 0.0) zn = -(ldp / ld) * y2;  // row i of (LDL^T - lambda I) z = 0
-      if (!(fabs(zn) >= kTiny)) zn = 0.0;
-      S.sA[i - lo_i][L] = zn * scale;
+      const double za = S.sA[k][L] * y1;
+      const double zb = -(ldp * rcp_nr(ld)) * y2;  // row i of (LDL^T - lambda I) z = 0
+      double zn = (y1 != 0.0) ? za : zb;
+      zn = (fabs(zn) >= kTiny) ? zn : 0.0;
+      S.sA[o][L] = zn * scale;
       y2 = y1; y1 = zn; ldp = ld;
+    };
+    if (lo_i == r0 && top == r0 + kTR) {
+#pragma unroll
+      for (int k = 0; k < kTR; ++k) ystep(k, k);
+    } else {
+      for (int i = lo_i; i < top; ++i) ystep(i - r0, i - lo_i);
     }
     w_flush(W, lo_i + 1, top, col);
+    const bool done = !active || r >= nb - 1 || (on && fabs(y1) < kNeg && fabs(y2) < kNeg);
+    return trunc && __all_sync(0xffffffffu, done);
   });
 }
 
@@ -421,6 +472,7 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
   double lam = (A.mode == 2 || isnan(tk.lam0)) ? 0.5 * (lo + hi) : tk.lam0;
   unsigned long long nfact = 0;
   Twist tw;
+  const long long clk0 = clock64();
   // full factorization; nudge lambda if not finite (overflow insurance, reading 25)
   {
     double nudge = 2.0 * kEps * fabs(lam) + kTiny;
@@ -429,7 +481,13 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
       tw = w_twist_full(W, lam);
       ++nfact;
       if (!__any_sync(0xffffffffu, active && !tw.ok)) break;
-      if (active && !tw.ok) { lam = lam_base + nudge; nudge *= 2.0; }
+      if (active && !tw.ok) {
+        lam = lam_base + nudge; nudge *= 2.0;
+        atomicAdd(&A.ctr[2], 1ull);
+        if (A.ctr[3] == 0) {  // first failure: record why (debug aid, MRRR_TRACE)
+          A.ctr[3] = 1 + (isfinite(tw.gamma) ? 0 : 2) + (isfinite(tw.nrm2) ? 0 : 4);
+        }
+      }
     }
   }
   double lam_fin = lam;
@@ -494,7 +552,13 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
   }
   const double sc = 1.0 / sqrt(tw.nrm2);
   double *col = (A.mode == 2) ? A.Z + tk.col * A.ldz + N.row0 : A.zbuf + tk.col * A.zstride;
-  w_twist_solve(W, lam, tw.r, sc, col, active);
+  const long long clk1 = clock64();
+  w_twist_solve(W, lam, tw.r, sc, col, active, /*trunc=*/A.mode == 1);
+  const long long clk2 = clock64();
+  if (lane == 0) {  // per-phase cycles of the slowest warp (MRRR_TRACE)
+    atomicMax(&A.ctr[4], (unsigned long long)(clk1 - clk0));
+    atomicMax(&A.ctr[5], (unsigned long long)(clk2 - clk1));
+  }
   if (active) {
     if (A.mode == 2) A.lam_out[tix] = lam_fin;
     atomicAdd(&A.ctr[0], nfact);

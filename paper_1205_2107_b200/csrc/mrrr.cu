@@ -367,12 +367,12 @@ void launch_grid(int M, const Node *nodes, int node, double lo0, double hi0, int
 }
 
 // Warp items: runs of consecutive tasks of one node, at most 32 per item.
-std::vector<WarpItem> make_warp_items(const std::vector<VecTask> &t) {
+std::vector<WarpItem> make_warp_items(const std::vector<VecTask> &t, int lanes = 32) {
   std::vector<WarpItem> v;
   const int nt = (int)t.size();
   for (int a = 0; a < nt;) {
     int b = a;
-    while (b < nt && b - a < 32 && t[b].node == t[a].node) ++b;
+    while (b < nt && b - a < lanes && t[b].node == t[a].node) ++b;
     WarpItem w; w.node = t[a].node; w.t0 = a; w.t1 = b; w.pad = 0;
     v.push_back(w);
     a = b;
@@ -432,8 +432,8 @@ int solve(Problem &P, int64_t *m_out) {
   double *ds = ar.alloc<double>(n), *es = ar.alloc<double>(n), *es2 = ar.alloc<double>(n);
   int *brk = ar.alloc<int>(n);
   double *hdr = ar.alloc<double>(8);
-  unsigned long long *ctr = ar.alloc<unsigned long long>(16);
-  CK(cudaMemsetAsync(ctr, 0, 16 * sizeof(unsigned long long), s));
+  unsigned long long *ctr = ar.alloc<unsigned long long>(32);
+  CK(cudaMemsetAsync(ctr, 0, 32 * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(brk, 0, n * sizeof(int), s));
   k_prep<<<1, 1024, 0, s>>>(P.d, P.e, n, ds, es, es2, brk, hdr);
   CK(cudaGetLastError());
@@ -799,7 +799,7 @@ int solve(Problem &P, int64_t *m_out) {
   double *wlo = ar.alloc<double>(nslots), *whi = ar.alloc<double>(nslots);
   const int64_t nbmax = [&] { int x = 1; for (auto &B : hb) x = std::max(x, B.nb); return (int64_t)x; }();
   int level = 0;
-  unsigned long long h_ctr[16];
+  unsigned long long h_ctr[32];
   Timer ttree(s);
   for (;;) {
     h2d(active, h_active.data(), nslots, s);
@@ -864,13 +864,17 @@ int solve(Problem &P, int64_t *m_out) {
       const int nseg = (int)((nbmax + kSeg - 1) / kSeg);
       FwdCk *fck = lv.alloc<FwdCk>((size_t)nseg * (ntask + 32));
       BwdCk *bck = lv.alloc<BwdCk>((size_t)nseg * (ntask + 32));
-      auto items = make_warp_items(zt);
+      // one probe per warp: a lockstep solve spans the union of its lanes'
+      // row ranges (up to 2n rows for two distant twist indices); alone it
+      // spans n rows (or less when truncated)
+      auto items = make_warp_items(zt, 1);
+      CK(cudaMemsetAsync(zbuf, 0, (size_t)2 * ncl * nbmax * sizeof(double), s));
       WarpItem *ditems = lv.alloc<WarpItem>(items.size());
       h2d(ditems, items.data(), items.size(), s);
       WVecArgs A{};
       A.nodes = dnodes; A.LDv = LDv; A.tasks = dzt; A.items = ditems; A.nitems = (int)items.size();
       A.lo = slo; A.hi = shi; A.fck = fck; A.bck = bck; A.ck_stride = ntask + 32; A.ntask = ntask;
-      A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1; A.ctr = ctr + 4; A.slot_j = slot_j;
+      A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1; A.ctr = ctr + 16; A.slot_j = slot_j;
       launch_wvec(true, A, s);
     }
     double *dsig = lv.alloc<double>(ncl);
@@ -1075,7 +1079,10 @@ int solve(Problem &P, int64_t *m_out) {
     g_stats.kernel_launches++;
   }
   finish_w();
-  d2h(h_ctr, ctr, 16, s);
+  d2h(h_ctr, ctr, 32, s);
+  if (tr.on)
+    fprintf(stderr, "[mrrr] nudged factorizations: probes %llu (why %llu), vectors %llu (why %llu); probe max cycles: factorization %llu solve %llu\n",
+            h_ctr[18], h_ctr[19], h_ctr[10], h_ctr[11], h_ctr[20], h_ctr[21]);
   tr.mark("vectors");
   g_stats.ms_vectors = tv.stop();
   g_stats.root_sweeps += h_ctr[0];

@@ -45,6 +45,7 @@ __global__ void kb_fwd(const double2 *DL, const double2 *LDv, int nb, FwdCk *fck
     } else {
       for (int k = 0; k < rows; ++k) F.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
     }
+    return false;
   });
   out[W.lane] = F.p + F.q + F.H + F.neg;
 }
@@ -57,6 +58,7 @@ __global__ void kb_fwd_nock(const double2 *DL, const double2 *LDv, int nb, FwdCk
 #pragma unroll
       for (int k = 0; k < kTR; ++k) F.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
     }
+    return false;
   });
   out[W.lane] = F.p + F.q + F.H + F.neg;
 }
@@ -73,6 +75,7 @@ __global__ void kb_fwd_plain(const double2 *DL, const double2 *LDv, int nb, FwdC
         if ((k & 7) == 7) { int e = max_exp(p, q); double f = pow2_scale(min(e, 2045)); p *= f; q *= f; }
       }
     }
+    return false;
   });
   out[W.lane] = p + q;
 }

@@ -232,6 +232,8 @@ def main():
     clk = Clocks(dev.index or 0)
     clk.start()
     time.sleep(1.0)  # let the sampler start before the timed region (host-side orchestration)
+    step()           # and bring the clocks back up after the pause (untimed)
+    torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()

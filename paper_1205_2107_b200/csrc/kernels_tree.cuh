@@ -578,6 +578,194 @@ __global__ void __launch_bounds__(128) k_refine(const Node *nodes, const Work *w
   }
 }
 
+// a3/a5 -- the adaptive multisection per WARP (k_refine_warp): one warp owns up
+// to kRWMembers member slots of one node and sweeps the node once per round
+// with 32 * M shifts spread over its unconverged members (P = min(32 M / a,
+// 64) each: a lone member gains 6 bits per sweep).  Rows come through a
+// warp-private shared-memory ring of 16-row tiles filled by cp.async ahead of
+// the chains, so warps of different clusters never wait on each other (the
+// CTA-wide version spent most of its time in barrier stalls: ncu 9.3 barrier
+// stalls per issue).  Same arithmetic and update rules as k_refine.
+constexpr int kRWMembers = 8;
+constexpr int kRWT = 16, kRWRing = 6, kRWWarps = 4;
+
+struct RefWarpSmem {
+  double2 ring[kRWRing][kRWT];
+  double lo[kRWMembers], hi[kRWMembers], wl[kRWMembers], wu[kRWMembers];
+  double plo[kRWMembers], phi[kRWMembers];
+  int j[kRWMembers], state[kRWMembers], act[kRWMembers];
+  int cnt[32 * 4];
+};
+
+template <int M>
+__global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes, const Work *work, int nwork,
+                                                               const int *__restrict__ slot_list,
+                                                               const int *__restrict__ slot_j, double *lo_arr,
+                                                               double *hi_arr, const double *wlo_arr,
+                                                               const double *whi_arr, int verify, double rtol,
+                                                               int max_rounds, int *fail,
+                                                               unsigned long long *sweeps,
+                                                               unsigned long long *safe_ctr) {
+  static_assert(M == 4, "cnt[] is sized for 4 shifts per lane");
+  __shared__ RefWarpSmem smem[kRWWarps];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kRWWarps + wid;
+  if (item >= nwork) return;
+  RefWarpSmem &S = smem[wid];
+  const Work Wk = work[item];
+  const Node N = nodes[Wk.node];
+  const int nm = Wk.s1 - Wk.s0;
+  const int nb = N.nb, body = nb - 1, ntile = (body + kRWT - 1) / kRWT;
+  constexpr int SH = 32 * M;
+  auto conv = [&](double a, double b) {
+    const double m = 0.5 * (a + b);
+    return (b - a <= rtol * fmax(fabs(a), fabs(b))) || !(m > a && m < b);
+  };
+  if (lane < nm) {
+    const int sl = slot_list ? slot_list[Wk.s0 + lane] : Wk.s0 + lane;
+    S.j[lane] = slot_j[sl];
+    if (verify) {
+      S.plo[lane] = lo_arr[sl]; S.phi[lane] = hi_arr[sl];
+      S.wl[lane] = wlo_arr[sl]; S.wu[lane] = whi_arr[sl];
+      S.lo[lane] = S.plo[lane] - S.wl[lane]; S.hi[lane] = S.phi[lane] + S.wu[lane];
+      S.state[lane] = 0;
+    } else {
+      S.lo[lane] = lo_arr[sl]; S.hi[lane] = hi_arr[sl];
+      S.state[lane] = conv(S.lo[lane], S.hi[lane]) ? 2 : 1;
+    }
+  }
+  __syncwarp();
+  int rounds = 0;
+  for (; rounds < max_rounds; ++rounds) {
+    const bool a = lane < nm && S.state[lane] != 2;
+    const unsigned bal = __ballot_sync(0xffffffffu, a);
+    const int na = __popc(bal);
+    if (na == 0) break;
+    if (a) S.act[__popc(bal & ((1u << lane) - 1u))] = lane;
+    __syncwarp();
+    const int P = min(SH / na, 64);
+    double mu[M];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      const int f = lane * M + c;
+      const int ai = f / P, sub = f - ai * P;
+      mu[c] = 0.0;
+      if (ai < na) {
+        const int i = S.act[ai];
+        const double l = S.lo[i], h = S.hi[i];
+        mu[c] = (S.state[i] == 0) ? l + (h - l) * ((double)sub / (double)(P - 1))
+                                  : l + (h - l) * ((double)(sub + 1) / (double)(P + 1));
+        if (S.state[i] == 0 && sub == P - 1) mu[c] = h;
+        any = true;
+      }
+    }
+    // ---- one sweep of the node for the lane's M shifts
+    Sturm st[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) sturm_init(st[c], mu[c]);
+    bool ok = true;
+    auto issue = [&](int t) {
+      const int row = t * kRWT + lane;
+      if (lane < kRWT && t < ntile && row < body)
+        __pipeline_memcpy_async(&S.ring[t % kRWRing][lane], &N.DL[row], sizeof(double2));
+      __pipeline_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < kRWRing - 1; ++k) issue(k);
+    for (int t = 0; t < ntile; ++t) {
+      __pipeline_wait_prior(kRWRing - 2);
+      __syncwarp();
+      const double2 *T = S.ring[t % kRWRing];
+      const int rows = min(kRWT, body - t * kRWT);
+      if (any) {
+        if (rows == kRWT) {
+#pragma unroll
+          for (int k = 0; k < kRWT; ++k) {
+            const double2 v = T[k];
+#pragma unroll
+            for (int c = 0; c < M; ++c) sturm_step(st[c], v.x, v.y, mu[c]);
+            if ((k & 7) == 7) {
+#pragma unroll
+              for (int c = 0; c < M; ++c) ok &= sturm_rescale(st[c]);
+            }
+          }
+        } else {
+          for (int k = 0; k < rows; ++k) {
+            const double2 v = T[k];
+#pragma unroll
+            for (int c = 0; c < M; ++c) sturm_step(st[c], v.x, v.y, mu[c]);
+            if ((k & 7) == 7) {
+#pragma unroll
+              for (int c = 0; c < M; ++c) ok &= sturm_rescale(st[c]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      issue(t + kRWRing - 1);
+    }
+    __pipeline_wait_prior(0);
+    const double Dl = __ldg(&N.DL[nb - 1]).x;
+#pragma unroll
+    for (int c = 0; c < M; ++c) { sturm_last(st[c], Dl); ok &= sturm_ok(st[c]); }
+    if (any && !ok) {
+      atomicAdd(safe_ctr, 1ull);
+#pragma unroll
+      for (int c = 0; c < M; ++c) st[c].c = negcount_qd_safe(N.DL, nb, mu[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < M; ++c) S.cnt[lane * M + c] = (int)st[c].c;
+    __syncwarp();
+    // ---- owners update their member (lane ai < na owns active member act[ai])
+    if (lane < na) {
+      const int i = S.act[lane];
+      const int jj = S.j[i];
+      const int *cc = S.cnt + lane * P;
+      double l = S.lo[i], h = S.hi[i];
+      int stt = S.state[i];
+      if (stt == 0) {
+        const bool okl = cc[0] <= jj - 1, oku = cc[P - 1] >= jj;
+        if (!okl) { S.wl[i] *= 2.0; l = S.plo[i] - S.wl[i]; }
+        if (!oku) { S.wu[i] *= 2.0; h = S.phi[i] + S.wu[i]; }
+        if (okl && oku) {
+          stt = 1;
+          double nl = l, nh = h;
+          for (int q = 1; q < P - 1; ++q) {
+            const double x = l + (h - l) * ((double)q / (double)(P - 1));
+            if (cc[q] < jj) nl = fmax(nl, x);
+          }
+          for (int q = P - 2; q >= 1; --q) {
+            const double x = l + (h - l) * ((double)q / (double)(P - 1));
+            if (cc[q] >= jj && x > nl) nh = fmin(nh, x);
+          }
+          l = nl; h = nh;
+        }
+      } else {
+        double nl = l, nh = h;
+        for (int q = 0; q < P; ++q) {
+          const double x = l + (h - l) * ((double)(q + 1) / (double)(P + 1));
+          if (cc[q] < jj) nl = fmax(nl, x);
+        }
+        for (int q = P - 1; q >= 0; --q) {
+          const double x = l + (h - l) * ((double)(q + 1) / (double)(P + 1));
+          if (cc[q] >= jj && x > nl) nh = fmin(nh, x);
+        }
+        l = nl; h = nh;
+      }
+      if (stt == 1 && conv(l, h)) stt = 2;
+      S.lo[i] = l; S.hi[i] = h; S.state[i] = stt;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) atomicAdd(sweeps, (unsigned long long)rounds * SH);
+  if (lane < nm) {
+    const int sl = slot_list ? slot_list[Wk.s0 + lane] : Wk.s0 + lane;
+    lo_arr[sl] = S.lo[lane]; hi_arr[sl] = S.hi[lane];
+    if (S.state[lane] != 2) fail[0] = 1;
+  }
+}
+
 // a5 -- bracket verification in child coordinates (O9.4): counts at lo and
 // hi; an end that does not bracket index j is widened by doubling its offset
 // from the parent interval until it does.

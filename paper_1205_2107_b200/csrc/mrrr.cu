@@ -111,9 +111,46 @@ struct DevArena {
   }
 };
 
+// Pinned staging for host->device uploads.  A copy from pageable memory makes
+// cudaMemcpyAsync wait for the stream, so every small upload of the
+// orchestrator (cluster lists, work items) used to drain the GPU.  Uploads go
+// through a per-thread pinned bump buffer instead; a region is never reused
+// within a call (mrrr_stemr synchronises its stream before returning, and
+// staging_reset() runs at the start of the next call).
+struct Staging {
+  std::vector<std::pair<char *, size_t>> chunks;  // pinned chunks (kept across calls)
+  size_t chunk = 0, off = 0;
+  void *get(size_t bytes) {
+    bytes = (bytes + 15) & ~size_t(15);
+    while (true) {
+      if (chunk < chunks.size() && off + bytes <= chunks[chunk].second) {
+        void *p = chunks[chunk].first + off;
+        off += bytes;
+        return p;
+      }
+      if (chunk + 1 < chunks.size()) { ++chunk; off = 0; continue; }
+      size_t sz = std::max<size_t>(bytes, chunks.empty() ? (8u << 20) : 2 * chunks.back().second);
+      char *p = nullptr;
+      if (cudaMallocHost((void **)&p, sz) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+      chunks.push_back({p, sz});
+      chunk = chunks.size() - 1;
+      off = 0;
+    }
+  }
+  void reset() { chunk = 0; off = 0; }
+};
+thread_local Staging g_staging;
+
 template <class T>
 void h2d(T *dst, const T *src, size_t count, cudaStream_t s) {
-  if (count) CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  if (!count) return;
+  void *st = g_staging.get(count * sizeof(T));
+  if (st) {
+    memcpy(st, src, count * sizeof(T));
+    CK(cudaMemcpyAsync(dst, st, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  } else {
+    CK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
 }
 template <class T>
 void d2h(T *dst, const T *src, size_t count, cudaStream_t s) {
@@ -396,6 +433,19 @@ void launch_wvec(bool probe, WVecArgs A, cudaStream_t s) {
   g_stats.kernel_launches++;
 }
 
+// Adaptive multisection by warps (k_refine_warp) over work items of at most
+// kRWMembers slots.
+void launch_refine(const Node *nodes, const Work *work, int nwork, const int *slot_list,
+                   const int *slot_j, double *lo, double *hi, const double *wlo, const double *whi,
+                   int verify, double rtol, int *fail, unsigned long long *sweeps,
+                   unsigned long long *safe, cudaStream_t s) {
+  if (nwork == 0) return;
+  k_refine_warp<4><<<(nwork + kRWWarps - 1) / kRWWarps, 32 * kRWWarps, 0, s>>>(
+      nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi, verify, rtol, 4000, fail, sweeps, safe);
+  CK(cudaGetLastError());
+  g_stats.kernel_launches++;
+}
+
 struct Problem {
   int64_t n;
   const double *d, *e;
@@ -423,6 +473,7 @@ int solve(Problem &P, int64_t *m_out) {
   const int64_t n = P.n;
   DevArena ar(s);
   Trace tr;
+  g_staging.reset();
   Timer tm(s), tall(s);
   KTimer kt_root, kt_vec, kt_fin;
   memset(&g_stats, 0, sizeof(g_stats));
@@ -661,14 +712,12 @@ int solve(Problem &P, int64_t *m_out) {
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }
-      make_work(B.root_node, B.slot0, B.slot1, pick_wmax(nslots), wv);
+      make_work(B.root_node, B.slot0, B.slot1, kRWMembers, wv);
     }
     Work *dwork = ar.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
-    k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, nullptr, slot_j, slo, shi, nullptr, nullptr, 0,
-                                               rtol_root, 4000, dfail + 2, ctr, ctr + 1);
-    CK(cudaGetLastError());
-    g_stats.kernel_launches++;
+    launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, nullptr, nullptr, 0, rtol_root,
+                  dfail + 2, ctr, ctr + 1, s);
     (void)M;
     kt_root.stop(s);
   }
@@ -920,13 +969,11 @@ int solve(Problem &P, int64_t *m_out) {
     // chunks of kTreeChunk members from each cluster's start: the refinement of
     // a cluster depends on the cluster alone, so every rank that holds a
     // shared cluster computes bitwise the same child intervals (§8(e))
-    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], kTreeChunk, wv);
+    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], kRWMembers, wv);
     Work *dwork = lv.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
-    k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, nullptr, slot_j, slo, shi, wlo, whi, 1,
-                                               P.o.rtol_class, 4000, dfail + 2, ctr + 2, ctr + 1);
-    CK(cudaGetLastError());
-    g_stats.kernel_launches++;
+    launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, wlo, whi, 1, P.o.rtol_class,
+                  dfail + 2, ctr + 2, ctr + 1, s);
     d2h(h_fail, dfail, 4, s);
     if (getenv("MRRR_DUMP")) {
       char nm[64];
@@ -969,7 +1016,7 @@ int solve(Problem &P, int64_t *m_out) {
                        [&](int a, int b) { return tasks[a].node < tasks[b].node; });
       std::vector<int> list(ntask);
       for (int q = 0; q < ntask; ++q) list[q] = tasks[order[q]].slot;
-      const int wmax = pick_wmax(ntask);
+      const int wmax = kRWMembers;
       std::vector<Work> wv;
       for (int q0 = 0; q0 < ntask;) {
         int q1 = q0;
@@ -985,12 +1032,9 @@ int solve(Problem &P, int64_t *m_out) {
       Work *dwork = ar.alloc<Work>(wv.size());
       h2d(dwork, wv.data(), wv.size(), s);
       kt_fin.start(s);
-      k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dwork, dlist, slot_j, slo, shi, nullptr, nullptr,
-                                                 0, P.o.rtol_vec, 4000, dfail + 2, ctr + 2,
-                                                 ctr + 1);
+      launch_refine(dnodes, dwork, (int)wv.size(), dlist, slot_j, slo, shi, nullptr, nullptr, 0,
+                    P.o.rtol_vec, dfail + 2, ctr + 2, ctr + 1, s);
       kt_fin.stop(s);
-      CK(cudaGetLastError());
-      g_stats.kernel_launches++;
     }
     VecTask *dt = ar.alloc<VecTask>(ntask);
     h2d(dt, tasks.data(), ntask, s);
@@ -1038,10 +1082,12 @@ int solve(Problem &P, int64_t *m_out) {
         for (int q0 = 0; q0 < h_nf;) {
           int q1 = q0;
           while (q1 < h_nf && tasks[fl[q1]].node == tasks[fl[q0]].node) ++q1;
-          for (int a = q0; a < q1; a += 32) {
-            Work W; W.node = tasks[fl[q0]].node; W.s0 = a; W.s1 = std::min(a + 32, q1); W.pad = 0;
+          for (int a = q0; a < q1; a += kRWMembers) {
+            Work W; W.node = tasks[fl[q0]].node; W.s0 = a; W.s1 = std::min(a + kRWMembers, q1); W.pad = 0;
             wv.push_back(W);
-            WarpItem wi; wi.node = W.node; wi.t0 = W.s0; wi.t1 = W.s1; wi.pad = 0;
+          }
+          for (int a = q0; a < q1; a += 32) {
+            WarpItem wi; wi.node = tasks[fl[q0]].node; wi.t0 = a; wi.t1 = std::min(a + 32, q1); wi.pad = 0;
             fitems.push_back(wi);
           }
           q0 = q1;
@@ -1052,10 +1098,8 @@ int solve(Problem &P, int64_t *m_out) {
         h2d(dfl, fl.data(), h_nf, s);
         Work *dw = ar.alloc<Work>(wv.size());
         h2d(dw, wv.data(), wv.size(), s);
-        k_refine<4><<<(int)wv.size(), 128, 0, s>>>(dnodes, dw, dslots, slot_j, slo, shi, nullptr, nullptr,
-                                                   0, 4.0 * kEps, 4000, dfail + 2, ctr + 2, ctr + 1);
-        CK(cudaGetLastError());
-        g_stats.kernel_launches++;
+        launch_refine(dnodes, dw, (int)wv.size(), dslots, slot_j, slo, shi, nullptr, nullptr, 0, 4.0 * kEps,
+                      dfail + 2, ctr + 2, ctr + 1, s);
         WarpItem *dfi = ar.alloc<WarpItem>(fitems.size());
         h2d(dfi, fitems.data(), fitems.size(), s);
         WVecArgs F = A;

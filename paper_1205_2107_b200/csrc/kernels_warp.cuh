@@ -439,8 +439,9 @@ struct WVecArgs {
   int mode;                  // 0: RQC (reading 10); 1: one factorization (probes);
                              // 2: one factorization at the bracket midpoint (RQC fallback)
   int rqc_max;               // mode 0: factorizations before the fallback (3)
-  int *fail_list;            // mode 0: tasks that did not converge (appended)
+  int *fail_list;            // mode 0: tasks that did not converge (appended as task_base + tix)
   int *fail_count;
+  int task_base;             // global index of this launch's task 0
   unsigned long long *ctr;   // [0] factorizations, [1] fallbacks
 };
 
@@ -540,7 +541,7 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
       // O10 fallback, deferred: the bracket goes back to the slot; the host
       // refines it to 4 eps and a mode-2 pass writes the vector
       A.lo[tk.slot] = lo; A.hi[tk.slot] = hi;
-      A.fail_list[atomicAdd(A.fail_count, 1)] = tix;
+      A.fail_list[atomicAdd(A.fail_count, 1)] = A.task_base + tix;
       atomicAdd(&A.ctr[1], 1ull);
     }
     // failed lanes skip the solve (their column is written by the fallback)

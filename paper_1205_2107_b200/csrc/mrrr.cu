@@ -309,6 +309,11 @@ __global__ void k_translate(const int *slot_cl, const int *cl_first_slot, int ns
   slot_node[s] = node_base + c;
 }
 
+__global__ void k_scatter(const int *idx, const double *src, int n, double *dst) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = src[i];
+}
+
 __global__ void k_output(const VecTask *tasks, int ntask, const Node *nodes, const double *lam,
                          double inv_scale, double *w) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -849,6 +854,60 @@ int solve(Problem &P, int64_t *m_out) {
   const int64_t nbmax = [&] { int x = 1; for (auto &B : hb) x = std::max(x, B.nb); return (int64_t)x; }();
   int level = 0;
   unsigned long long h_ctr[32];
+  // ---- a6 overlapped with the tree: the singletons a level classifies are
+  // final, so their vectors start at once on a lower-priority side stream
+  // (events order them after the kernels that produced their node and
+  // bracket) while the main stream continues with the next level.
+  double *lam = ar.alloc<double>(std::max<int64_t>(nslots, 1));
+  int *fail_list = ar.alloc<int>(std::max<int64_t>(nslots, 1)), *fail_count = ar.alloc<int>(1);
+  CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
+  cudaStream_t s2 = nullptr;
+  {
+    int lo_pr = 0, hi_pr = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
+    CK(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, lo_pr));
+  }
+  struct StreamGuard {
+    cudaStream_t a, b;
+    ~StreamGuard() {
+      if (b) { cudaEvent_t e; cudaEventCreateWithFlags(&e, cudaEventDisableTiming); cudaEventRecord(e, b);
+               cudaStreamWaitEvent(a, e, 0); cudaEventDestroy(e); cudaStreamDestroy(b); }
+    }
+  } sguard{s, s2};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vec_ev;
+  const int nseg_v = (int)((nbmax + kSeg - 1) / kSeg);
+  size_t vec_done = 0;
+  auto flush_vectors = [&]() {
+    const size_t t0 = vec_done, t1 = tasks.size();
+    if (t1 == t0) return;
+    const int nbt = (int)(t1 - t0);
+    std::vector<VecTask> bt(tasks.begin() + t0, tasks.begin() + t1);
+    VecTask *dtb = ar.alloc<VecTask>(nbt);
+    FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg_v * (nbt + 32));
+    BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg_v * (nbt + 32));
+    auto items = make_warp_items(bt);
+    WarpItem *ditems = ar.alloc<WarpItem>(items.size());
+    h2d(dtb, bt.data(), nbt, s);
+    h2d(ditems, items.data(), items.size(), s);
+    cudaEvent_t ready;
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, s));
+    CK(cudaStreamWaitEvent(s2, ready, 0));
+    cudaEventDestroy(ready);
+    WVecArgs A{};
+    A.nodes = dnodes; A.LDv = LDv; A.tasks = dtb; A.items = ditems; A.nitems = (int)items.size();
+    A.lo = slo; A.hi = shi; A.fck = fck; A.bck = bck; A.ck_stride = nbt + 32; A.ntask = nbt;
+    A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam + t0; A.mode = 0; A.ctr = ctr + 8;
+    A.slot_j = slot_j; A.rqc_max = std::max(1, P.o.rqc_max);
+    A.fail_list = fail_list; A.fail_count = fail_count; A.task_base = (int)t0;
+    cudaEvent_t ea, eb;
+    CK(cudaEventCreate(&ea)); CK(cudaEventCreate(&eb));
+    CK(cudaEventRecord(ea, s2));
+    launch_wvec(false, A, s2);
+    CK(cudaEventRecord(eb, s2));
+    vec_ev.push_back({ea, eb});
+    vec_done = t1;
+  };
   Timer ttree(s);
   for (;;) {
     h2d(active, h_active.data(), nslots, s);
@@ -882,6 +941,7 @@ int solve(Problem &P, int64_t *m_out) {
       }
     }
     const int ncl = (int)cl_parent.size();
+    if (vectors) flush_vectors();
     if (ncl == 0) break;
     if (level + 1 > P.o.max_depth) throw MrrrError{MRRR_ERR_DEPTH};
     g_stats.nodes += ncl;
@@ -1001,58 +1061,21 @@ int solve(Problem &P, int64_t *m_out) {
   g_stats.levels = level;
   g_stats.ms_tree = ttree.stop();
 
-  // ---------------- a6: singleton vectors ----------------
+  // ---------------- a6: singleton vectors (launched per level above) ----------------
   Timer tv(s);
   const int ntask = (int)tasks.size();
   g_stats.singletons = ntask;
+  {
+    // join the side stream
+    cudaEvent_t j;
+    CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+    CK(cudaEventRecord(j, s2));
+    CK(cudaStreamWaitEvent(s, j, 0));
+    cudaEventDestroy(j);
+  }
   if (ntask > 0) {
-    // O10 (reading 10, opts.rtol_vec > 0): singleton brackets refined by the
-    // adaptive multisection before the RQC, work items grouped by node
-    // through a slot list
-    if (P.o.rtol_vec > 0) {
-      std::vector<int> order(ntask);
-      std::iota(order.begin(), order.end(), 0);
-      std::stable_sort(order.begin(), order.end(),
-                       [&](int a, int b) { return tasks[a].node < tasks[b].node; });
-      std::vector<int> list(ntask);
-      for (int q = 0; q < ntask; ++q) list[q] = tasks[order[q]].slot;
-      const int wmax = kRWMembers;
-      std::vector<Work> wv;
-      for (int q0 = 0; q0 < ntask;) {
-        int q1 = q0;
-        while (q1 < ntask && tasks[order[q1]].node == tasks[order[q0]].node) ++q1;
-        for (int a = q0; a < q1; a += wmax) {
-          Work W; W.node = tasks[order[q0]].node; W.s0 = a; W.s1 = std::min(a + wmax, q1); W.pad = 0;
-          wv.push_back(W);
-        }
-        q0 = q1;
-      }
-      int *dlist = ar.alloc<int>(ntask);
-      h2d(dlist, list.data(), ntask, s);
-      Work *dwork = ar.alloc<Work>(wv.size());
-      h2d(dwork, wv.data(), wv.size(), s);
-      kt_fin.start(s);
-      launch_refine(dnodes, dwork, (int)wv.size(), dlist, slot_j, slo, shi, nullptr, nullptr, 0,
-                    P.o.rtol_vec, dfail + 2, ctr + 2, ctr + 1, s);
-      kt_fin.stop(s);
-    }
     VecTask *dt = ar.alloc<VecTask>(ntask);
     h2d(dt, tasks.data(), ntask, s);
-    const int nseg = (int)((nbmax + kSeg - 1) / kSeg);
-    FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg * (ntask + 32));
-    BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg * (ntask + 32));
-    double *lam = ar.alloc<double>(ntask);
-    auto items = make_warp_items(tasks);
-    WarpItem *ditems = ar.alloc<WarpItem>(items.size());
-    h2d(ditems, items.data(), items.size(), s);
-    WVecArgs A{};
-    A.nodes = dnodes; A.LDv = LDv; A.tasks = dt; A.items = ditems; A.nitems = (int)items.size();
-    A.lo = slo; A.hi = shi; A.fck = fck; A.bck = bck; A.ck_stride = ntask + 32; A.ntask = ntask;
-    A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam; A.mode = 0; A.ctr = ctr + 8;
-    A.slot_j = slot_j; A.rqc_max = std::max(1, P.o.rqc_max);
-    int *fail_list = ar.alloc<int>(ntask), *fail_count = ar.alloc<int>(1);
-    CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
-    A.fail_list = fail_list; A.fail_count = fail_count;
     {
       std::vector<Node> hnodes(nnodes);
       d2h(hnodes.data(), dnodes, nnodes, s);
@@ -1061,9 +1084,6 @@ int solve(Problem &P, int64_t *m_out) {
       g_stats.vec_tasks = ntask;
       g_stats.vec_elems = el;
     }
-    kt_vec.start(s);
-    launch_wvec(false, A, s);
-    kt_vec.stop(s);
     // deferred O10 fallback (reading 10): brackets of the tasks whose RQC did
     // not converge are refined to 4 eps, then one factorization at the
     // midpoint writes their vectors (mode 2)
@@ -1077,8 +1097,8 @@ int solve(Problem &P, int64_t *m_out) {
           return tasks[a].node != tasks[b].node ? tasks[a].node < tasks[b].node : a < b;
         });
         std::vector<int> slots(h_nf);
+        std::vector<VecTask> ft(h_nf);
         std::vector<Work> wv;
-        std::vector<WarpItem> fitems;
         for (int q0 = 0; q0 < h_nf;) {
           int q1 = q0;
           while (q1 < h_nf && tasks[fl[q1]].node == tasks[fl[q0]].node) ++q1;
@@ -1086,13 +1106,10 @@ int solve(Problem &P, int64_t *m_out) {
             Work W; W.node = tasks[fl[q0]].node; W.s0 = a; W.s1 = std::min(a + kRWMembers, q1); W.pad = 0;
             wv.push_back(W);
           }
-          for (int a = q0; a < q1; a += 32) {
-            WarpItem wi; wi.node = tasks[fl[q0]].node; wi.t0 = a; wi.t1 = std::min(a + 32, q1); wi.pad = 0;
-            fitems.push_back(wi);
-          }
           q0 = q1;
         }
-        for (int q = 0; q < h_nf; ++q) slots[q] = tasks[fl[q]].slot;
+        for (int q = 0; q < h_nf; ++q) { slots[q] = tasks[fl[q]].slot; ft[q] = tasks[fl[q]]; }
+        auto fitems = make_warp_items(ft);
         int *dslots = ar.alloc<int>(h_nf), *dfl = ar.alloc<int>(h_nf);
         h2d(dslots, slots.data(), h_nf, s);
         h2d(dfl, fl.data(), h_nf, s);
@@ -1100,11 +1117,21 @@ int solve(Problem &P, int64_t *m_out) {
         h2d(dw, wv.data(), wv.size(), s);
         launch_refine(dnodes, dw, (int)wv.size(), dslots, slot_j, slo, shi, nullptr, nullptr, 0, 4.0 * kEps,
                       dfail + 2, ctr + 2, ctr + 1, s);
+        VecTask *dft = ar.alloc<VecTask>(h_nf);
+        h2d(dft, ft.data(), h_nf, s);
         WarpItem *dfi = ar.alloc<WarpItem>(fitems.size());
         h2d(dfi, fitems.data(), fitems.size(), s);
-        WVecArgs F = A;
-        F.mode = 2; F.task_list = dfl; F.items = dfi; F.nitems = (int)fitems.size();
+        double *lam_c = ar.alloc<double>(h_nf);
+        WVecArgs F{};
+        F.nodes = dnodes; F.LDv = LDv; F.tasks = dft; F.items = dfi; F.nitems = (int)fitems.size();
+        F.lo = slo; F.hi = shi; F.slot_j = slot_j; F.ntask = h_nf; F.ck_stride = h_nf + 32;
+        F.fck = ar.alloc<FwdCk>((size_t)nseg_v * (h_nf + 32));
+        F.bck = ar.alloc<BwdCk>((size_t)nseg_v * (h_nf + 32));
+        F.Z = P.Z; F.ldz = P.ldz; F.lam_out = lam_c; F.mode = 2; F.ctr = ctr + 8;
         launch_wvec(false, F, s);
+        k_scatter<<<(h_nf + 255) / 256, 256, 0, s>>>(dfl, lam_c, h_nf, lam);
+        CK(cudaGetLastError());
+        g_stats.kernel_launches++;
       }
     }
     if (getenv("MRRR_DEBUG_TASKS")) {
@@ -1136,7 +1163,17 @@ int solve(Problem &P, int64_t *m_out) {
   g_stats.rqc_fallbacks = h_ctr[9];
   g_stats.ms_total = tall.stop();
   g_stats.ms_k_root_bisect = kt_root.ms();
-  g_stats.ms_k_vectors = kt_vec.ms();
+  {
+    double ms = 0;
+    for (auto &e : vec_ev) {
+      float v = 0;
+      cudaEventSynchronize(e.second);
+      cudaEventElapsedTime(&v, e.first, e.second);
+      ms += v;
+      cudaEventDestroy(e.first); cudaEventDestroy(e.second);
+    }
+    g_stats.ms_k_vectors = ms;
+  }
   g_stats.ms_k_final_refine = kt_fin.ms();
   return 0;
 }
@@ -1193,6 +1230,7 @@ int mrrr_stemr(int64_t n, const double *d, const double *e, int range, double vl
   P.n = n; P.d = d; P.e = e; P.range = range; P.vl = vl; P.vu = vu; P.il = il; P.iu = iu;
   P.w = w; P.Z = Z; P.ldz = ldz; P.s = (cudaStream_t)stream;
   if (opts) P.o = *opts; else mrrr_default_opts(&P.o);
+  if (P.o.rtol_vec != 0.0) return -14;  // oracle-only experiment (reading 10)
   try {
     if (n == 1) {
       double dv;
@@ -1283,6 +1321,7 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, doub
   P.rank = rank; P.nranks = nranks; P.allgather = allgather; P.ag_ctx = allgather_ctx;
   P.w_all = w_all;
   if (opts) P.o = *opts; else mrrr_default_opts(&P.o);
+  if (P.o.rtol_vec != 0.0) return -14;  // oracle-only experiment (reading 10)
   try {
     if (n == 1) {
       // one eigenpair: rank 0 owns it; w on every rank

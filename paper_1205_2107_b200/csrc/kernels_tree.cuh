@@ -1,6 +1,7 @@
-// kernels_tree.cuh -- prep, root representation, bisection/multisection,
-// classification, child representations (SURVEY §8(a)
-// rows a1-a5).  Included by mrrr.cu (single translation unit).
+// kernels_tree.cuh -- prep, split, root representation, root grid, adaptive
+// multisection, classification (SURVEY §8(a) rows
+// a1-a5; the child representations are in kernels_child.cuh).  Included by
+// mrrr.cu (single translation unit).
 #pragma once
 #include <cuda_pipeline.h>
 
@@ -295,46 +296,6 @@ __device__ void cta_sweep(const double2 *__restrict__ DL, int nb, double2 *sm, c
   }
 }
 
-// As cta_sweep, but a warp whose lanes carry no shift (`work` false for the
-// whole warp) only helps stage the tiles and skips the arithmetic.
-template <int M>
-__device__ void cta_sweep_masked(const double2 *__restrict__ DL, int nb, double2 *sm,
-                                 const double (&mu)[M], unsigned (&cnt)[M], bool &ok, bool work) {
-  Sturm s[M];
-#pragma unroll
-  for (int c = 0; c < M; ++c) sturm_init(s[c], mu[c]);
-  ok = true;
-  const int body = nb - 1;
-  const int ntiles = (body + kTile - 1) / kTile;
-  auto load = [&](int tile, int buf) {
-    int base = tile * kTile;
-    int rows = min(kTile, body - base);
-    for (int r = threadIdx.x; r < rows; r += blockDim.x)
-      __pipeline_memcpy_async(&sm[buf * kTile + r], &DL[base + r], sizeof(double2));
-    __pipeline_commit();
-  };
-  if (ntiles > 0) load(0, 0);
-  for (int tile = 0; tile < ntiles; ++tile) {
-    int buf = tile & 1;
-    if (tile + 1 < ntiles) {
-      load(tile + 1, buf ^ 1);
-      __pipeline_wait_prior(1);
-    } else {
-      __pipeline_wait_prior(0);
-    }
-    __syncthreads();
-    if (work) tile_steps<M>(sm + buf * kTile, min(kTile, body - tile * kTile), mu, s, ok);
-    __syncthreads();
-  }
-  double Dl = __ldg(&DL[nb - 1]).x;
-#pragma unroll
-  for (int c = 0; c < M; ++c) {
-    sturm_last(s[c], Dl);
-    ok &= sturm_ok(s[c]);
-    cnt[c] = s[c].c;
-  }
-}
-
 // ===========================================================================
 // Work item of the bisection kernels: a chunk of slots of one node.
 struct Work {
@@ -372,212 +333,6 @@ __global__ void __launch_bounds__(128) k_grid(const Node *nodes, int node, doubl
   }
 }
 
-// ===========================================================================
-// a3/a5 -- multisection refinement of slot intervals in node coordinates
-// until hi - lo <= rtol * max(|lo|, |hi|) or lo, hi have no double between
-// them (O7).  Invariant N(lo) < j <= N(hi).  Each thread owns one slot and
-// evaluates M shifts per round; the CTA sweeps the node once per round.
-// ===========================================================================
-template <int M>
-__global__ void __launch_bounds__(128) k_bisect(const Node *nodes, const Work *work,
-                                                const int *__restrict__ slot_j, double *lo_arr,
-                                                double *hi_arr, double rtol, int max_rounds,
-                                                unsigned long long *sweeps,
-                                                unsigned long long *safe_ctr) {
-  __shared__ double2 sm[2 * kTile];
-  const Work W = work[blockIdx.x];
-  const Node N = nodes[W.node];
-  int s = W.s0 + threadIdx.x;
-  bool mine = s < W.s1;
-  double lo = mine ? lo_arr[s] : 0.0, hi = mine ? hi_arr[s] : 1.0;
-  int j = mine ? slot_j[s] : 0;  // block-local 1-based eigen index
-  auto conv = [&](double a, double b) {
-    double m = 0.5 * (a + b);
-    return (b - a <= rtol * fmax(fabs(a), fabs(b))) || !(m > a && m < b);
-  };
-  bool done = !mine || conv(lo, hi);
-  int rounds = 0;
-  while (__syncthreads_or(!done) && rounds < max_rounds) {
-    double mu[M];
-#pragma unroll
-    for (int c = 0; c < M; ++c) mu[c] = lo + (hi - lo) * ((double)(c + 1) / (double)(M + 1));
-    unsigned k[M];
-    bool ok;
-    cta_sweep<M>(N.DL, N.nb, sm, mu, k, ok);
-    if (!done) {
-      if (!ok) {
-        atomicAdd(safe_ctr, 1ull);
-#pragma unroll
-        for (int c = 0; c < M; ++c) k[c] = negcount_qd_safe(N.DL, N.nb, mu[c]);
-      }
-      double nlo = lo, nhi = hi;
-#pragma unroll
-      for (int c = 0; c < M; ++c)
-        if ((int)k[c] < j && mu[c] > nlo) nlo = mu[c];
-#pragma unroll
-      for (int c = M - 1; c >= 0; --c)
-        if ((int)k[c] >= j && mu[c] > nlo && mu[c] < nhi) nhi = mu[c];
-      lo = nlo; hi = nhi;
-      done = conv(lo, hi);
-    }
-    ++rounds;
-  }
-  if (threadIdx.x == 0) atomicAdd(sweeps, (unsigned long long)rounds * M * (W.s1 - W.s0));
-  if (mine) { lo_arr[s] = lo; hi_arr[s] = hi; }
-}
-
-// a3/a5 -- adaptive multisection (replaces k_bisect + k_verify on the hot
-// path).  One CTA owns up to kRefMax member slots of one node.  Each round the
-// CTA sweeps the node once with blockDim.x * M shifts, spread evenly over the
-// members that have not converged yet: with a active members each gets
-// P = floor(blockDim.x * M / a) shifts, i.e. log2(P + 1) bits per round
-// (a lone eigenvalue gains 9 bits per sweep instead of 2.3).  Work item
-// slots are W.s0 .. W.s1-1, or slot_list[W.s0 .. W.s1-1] when a list is given.  Counts go to
-// shared memory; member i's owner thread then narrows [lo, hi] to the
-// neighbouring grid points around index j (invariant N(lo) < j <= N(hi)).
-// With `verify` set (child coordinates, O9.4) the member's grid first
-// includes both ends; an end that does not bracket j is widened by doubling
-// its offset from the translated parent interval (plo - wl, phi + wu) and the
-// member is narrowed only once both ends bracket j.
-// Stop: hi - lo <= rtol * max(|lo|, |hi|) or no double strictly inside.
-constexpr int kRefMax = 128;
-constexpr int kPmax = 16;
-
-template <int M>
-__global__ void __launch_bounds__(128) k_refine(const Node *nodes, const Work *work,
-                                                const int *__restrict__ slot_list,
-                                                const int *__restrict__ slot_j, double *lo_arr,
-                                                double *hi_arr, const double *wlo_arr,
-                                                const double *whi_arr, int verify, double rtol,
-                                                int max_rounds, int *fail,
-                                                unsigned long long *sweeps,
-                                                unsigned long long *safe_ctr) {
-  __shared__ double2 sm[2 * kTile];
-  __shared__ double m_lo[kRefMax], m_hi[kRefMax], m_wl[kRefMax], m_wu[kRefMax];
-  __shared__ double m_plo[kRefMax], m_phi[kRefMax];
-  __shared__ int m_j[kRefMax], m_state[kRefMax];  // state: 0 unverified, 1 verified, 2 done
-  __shared__ int act[kRefMax];                     // active member ids, compacted
-  __shared__ int cnt[128 * M];
-  __shared__ int s_na;
-  const Work W = work[blockIdx.x];
-  const Node N = nodes[W.node];
-  const int nm = W.s1 - W.s0;
-  const int tid = threadIdx.x, T = blockDim.x, S = T * M;
-  auto conv = [&](double a, double b) {
-    double m = 0.5 * (a + b);
-    return (b - a <= rtol * fmax(fabs(a), fabs(b))) || !(m > a && m < b);
-  };
-  for (int i = tid; i < nm; i += T) {
-    const int sl = slot_list ? slot_list[W.s0 + i] : W.s0 + i;
-    m_j[i] = slot_j[sl];
-    if (verify) {
-      m_plo[i] = lo_arr[sl]; m_phi[i] = hi_arr[sl];
-      m_wl[i] = wlo_arr[sl]; m_wu[i] = whi_arr[sl];
-      m_lo[i] = m_plo[i] - m_wl[i]; m_hi[i] = m_phi[i] + m_wu[i];
-      m_state[i] = 0;
-    } else {
-      m_lo[i] = lo_arr[sl]; m_hi[i] = hi_arr[sl];
-      m_state[i] = conv(m_lo[i], m_hi[i]) ? 2 : 1;
-    }
-  }
-  __syncthreads();
-  int rounds = 0;
-  for (; rounds < max_rounds; ++rounds) {
-    // compact the active members (warp 0; nm <= 128)
-    if (tid < 32) {
-      int base = 0;
-      for (int c0 = 0; c0 < nm; c0 += 32) {
-        const int i = c0 + tid;
-        const bool a = i < nm && m_state[i] != 2;
-        const unsigned b = __ballot_sync(0xffffffffu, a);
-        if (a) act[base + __popc(b & ((1u << tid) - 1u))] = i;
-        base += __popc(b);
-      }
-      if (tid == 0) s_na = base;
-    }
-    __syncthreads();
-    const int na = s_na;
-    if (na == 0) break;
-    // shifts per member: all of the CTA's, up to kPmax (log2(P+1) bits per
-    // round; beyond 16 shifts the bits per chain fall below 1/4)
-    const int P = min(S / na, kPmax);  // >= M
-    double mu[M];
-    bool any = false;
-#pragma unroll
-    for (int c = 0; c < M; ++c) {
-      const int f = tid * M + c;
-      const int ai = f / P, sub = f - ai * P;
-      mu[c] = 0.0;
-      if (ai < na) {
-        const int i = act[ai];
-        const double lo = m_lo[i], hi = m_hi[i];
-        // unverified: P points over [lo, hi] inclusive; verified: interior
-        mu[c] = (m_state[i] == 0) ? lo + (hi - lo) * ((double)sub / (double)(P - 1))
-                                  : lo + (hi - lo) * ((double)(sub + 1) / (double)(P + 1));
-        if (m_state[i] == 0 && sub == P - 1) mu[c] = hi;
-        any = true;
-      }
-    }
-    unsigned k[M];
-    bool ok;
-    cta_sweep_masked<M>(N.DL, N.nb, sm, mu, k, ok, __any_sync(0xffffffffu, any));
-    if (!ok && any) {
-      atomicAdd(safe_ctr, 1ull);
-#pragma unroll
-      for (int c = 0; c < M; ++c) k[c] = negcount_qd_safe(N.DL, N.nb, mu[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < M; ++c) cnt[tid * M + c] = (int)k[c];
-    __syncthreads();
-    // owners update their member
-    for (int ai = tid; ai < na; ai += T) {
-      const int i = act[ai];
-      const int j = m_j[i];
-      const int *cc = cnt + ai * P;
-      double lo = m_lo[i], hi = m_hi[i];
-      int st = m_state[i];
-      if (st == 0) {
-        const bool okl = cc[0] <= j - 1, oku = cc[P - 1] >= j;
-        if (!okl) { m_wl[i] *= 2.0; lo = m_plo[i] - m_wl[i]; }
-        if (!oku) { m_wu[i] *= 2.0; hi = m_phi[i] + m_wu[i]; }
-        if (okl && oku) {
-          st = 1;
-          double nlo = lo, nhi = hi;
-          for (int q = 1; q < P - 1; ++q) {
-            const double x = lo + (hi - lo) * ((double)q / (double)(P - 1));
-            if (cc[q] < j) nlo = fmax(nlo, x);
-          }
-          for (int q = P - 2; q >= 1; --q) {
-            const double x = lo + (hi - lo) * ((double)q / (double)(P - 1));
-            if (cc[q] >= j && x > nlo) nhi = fmin(nhi, x);
-          }
-          lo = nlo; hi = nhi;
-        }
-      } else {
-        double nlo = lo, nhi = hi;
-        for (int q = 0; q < P; ++q) {
-          const double x = lo + (hi - lo) * ((double)(q + 1) / (double)(P + 1));
-          if (cc[q] < j) nlo = fmax(nlo, x);
-        }
-        for (int q = P - 1; q >= 0; --q) {
-          const double x = lo + (hi - lo) * ((double)(q + 1) / (double)(P + 1));
-          if (cc[q] >= j && x > nlo) nhi = fmin(nhi, x);
-        }
-        lo = nlo; hi = nhi;
-      }
-      if (st == 1 && conv(lo, hi)) st = 2;
-      m_lo[i] = lo; m_hi[i] = hi; m_state[i] = st;
-    }
-    __syncthreads();
-  }
-  if (tid == 0) atomicAdd(sweeps, (unsigned long long)rounds * S);
-  for (int i = tid; i < nm; i += T) {
-    const int sl = slot_list ? slot_list[W.s0 + i] : W.s0 + i;
-    lo_arr[sl] = m_lo[i]; hi_arr[sl] = m_hi[i];
-    if (m_state[i] != 2) fail[0] = 1;
-  }
-}
-
 // a3/a5 -- the adaptive multisection per WARP (k_refine_warp): one warp owns up
 // to kRWMembers member slots of one node and sweeps the node once per round
 // with 32 * M shifts spread over its unconverged members (P = min(32 M / a,
@@ -585,7 +340,12 @@ __global__ void __launch_bounds__(128) k_refine(const Node *nodes, const Work *w
 // warp-private shared-memory ring of 16-row tiles filled by cp.async ahead of
 // the chains, so warps of different clusters never wait on each other (the
 // CTA-wide version spent most of its time in barrier stalls: ncu 9.3 barrier
-// stalls per issue).  Same arithmetic and update rules as k_refine.
+// stalls per issue).  Invariant N(lo) < j <= N(hi); a member stops when
+// hi - lo <= rtol max(|lo|, |hi|) or no double lies strictly inside.  With
+// `verify` set (child coordinates, O9.4) a member's first grid includes both
+// ends; an end that does not bracket index j is widened by doubling its
+// offset from the translated parent interval (plo - wl, phi + wu), and the
+// member is narrowed only once both ends bracket j.
 constexpr int kRWMembers = 8;
 constexpr int kRWT = 16, kRWRing = 6, kRWWarps = 4;
 
@@ -766,55 +526,6 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
   }
 }
 
-// a5 -- bracket verification in child coordinates (O9.4): counts at lo and
-// hi; an end that does not bracket index j is widened by doubling its offset
-// from the parent interval until it does.
-__global__ void __launch_bounds__(128) k_verify(const Node *nodes, const Work *work,
-                                                const int *__restrict__ slot_j, double *lo_arr,
-                                                double *hi_arr, const double *wlo_arr,
-                                                const double *whi_arr, int *fail,
-                                                unsigned long long *sweeps,
-                                                unsigned long long *safe_ctr) {
-  __shared__ double2 sm[2 * kTile];
-  const Work W = work[blockIdx.x];
-  const Node N = nodes[W.node];
-  int s = W.s0 + threadIdx.x;
-  bool mine = s < W.s1;
-  double lo = 0.0, hi = 1.0, wl = 0.0, wu = 0.0, plo = 0.0, phi = 0.0;
-  int j = 0;
-  if (mine) {
-    plo = lo_arr[s]; phi = hi_arr[s];  // parent-coordinate bracket minus sigma, unwidened
-    wl = wlo_arr[s]; wu = whi_arr[s];
-    lo = plo - wl; hi = phi + wu;
-    j = slot_j[s];
-  }
-  bool done = !mine;
-  int rounds = 0;
-  while (__syncthreads_or(!done) && rounds < 200) {
-    double mu[2] = {lo, hi};
-    unsigned k[2];
-    bool ok;
-    cta_sweep<2>(N.DL, N.nb, sm, mu, k, ok);
-    if (!done) {
-      if (!ok) {
-        atomicAdd(safe_ctr, 1ull);
-        k[0] = negcount_qd_safe(N.DL, N.nb, lo);
-        k[1] = negcount_qd_safe(N.DL, N.nb, hi);
-      }
-      bool okl = (int)k[0] <= j - 1, oku = (int)k[1] >= j;
-      if (!okl) { wl *= 2.0; lo = plo - wl; }
-      if (!oku) { wu *= 2.0; hi = phi + wu; }
-      done = okl && oku;
-    }
-    ++rounds;
-  }
-  if (threadIdx.x == 0) atomicAdd(sweeps, (unsigned long long)rounds * 2 * (W.s1 - W.s0));
-  if (mine) {
-    if (!done) fail[0] = 1;
-    lo_arr[s] = lo; hi_arr[s] = hi;
-  }
-}
-
 // ===========================================================================
 // a4 -- classification by relative gap (O8).  For consecutive
 // slots s, s+1 of the same node: boundary iff
@@ -834,194 +545,6 @@ __global__ void k_classify(const int *__restrict__ slot_node, const double *__re
     f = g > tol * fmax(fabs(m0), fabs(m1));
   }
   run_end[s] = f;
-}
-
-// ===========================================================================
-// a5 -- child representation by the stationary transform
-// L+ D+ L+^T = L D L^T - sigma I, projective form:
-//   t_i = D_i q + p (= D+_i q), p' = LLD_i p - sigma t, q' = t.
-// The child keeps the block's off-diagonals LD_i (= L+_i D+_i exactly in
-// exact arithmetic) and stores (D+_i, LLD+_i = LD_i^2 / D+_i).
-// k_cand: growth of the six candidate shifts (offsets 1, 2, 4 beyond each
-// cluster end, order L1 R1 L2 R2 L4 R4): raw max |D+| and the
-// eigenvector-weighted growth max over the parent's two end vectors z_L, z_R
-// of sum |D+_i| z_i^2 / ||z||^2 (reading 9, amended).
-// ===========================================================================
-struct Cand {
-  double sigma;
-  double raw;  // max |D+_i| (inf if not finite)
-  double wgt;  // max_{z in {z_L, z_R}} sum |D+_i| z_i^2 / ||z||^2 (inf if not finite / no z)
-  int32_t cluster;
-  int32_t which;  // 0..5 = (mult index) * 2 + (0 left, 1 right)
-};
-
-__global__ void k_cand(const Node *nodes, const int *cl_parent, const int *cl_s0, const int *cl_s1,
-                       const double *__restrict__ lo, const double *__restrict__ hi, int ncl,
-                       const double *__restrict__ zbuf, int64_t zstride, double rtol, Cand *cand) {
-  int id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= ncl * 6) return;
-  int c = id / 6, which = id % 6;
-  const Node P = nodes[cl_parent[c]];
-  int s0 = cl_s0[c], s1 = cl_s1[c] - 1;
-  double mult = (double)(1 << (which >> 1));
-  double sigma;
-  if ((which & 1) == 0) {
-    // offset unit (reading 8 amended): >= 2 rtol_c |lambda|, independent of
-    // how far below rtol_c the bracket converged
-    double dl = fmax(fmax(2.0 * (hi[s0] - lo[s0]), 2.0 * rtol * fabs(lo[s0])), 4.0 * kEps * fabs(lo[s0]));
-    sigma = lo[s0] - mult * dl;
-  } else {
-    double dr = fmax(fmax(2.0 * (hi[s1] - lo[s1]), 2.0 * rtol * fabs(hi[s1])), 4.0 * kEps * fabs(hi[s1]));
-    sigma = hi[s1] + mult * dr;
-  }
-  const double2 *DL = P.DL;
-  const double *zl = zbuf ? zbuf + (int64_t)(2 * c) * zstride : nullptr;
-  const double *zr = zbuf ? zbuf + (int64_t)(2 * c + 1) * zstride : nullptr;
-  double p = -sigma, q = 1.0, g = 0.0, nl = 0.0, dnl = 0.0, nr = 0.0, dnr = 0.0;
-  bool fin = true;
-  const int nb = P.nb;
-  auto row = [&](int i, const double2 &v, double a, double b) {
-    double t = fma(v.x, q, p);
-    double dp = t / q;  // D+_i (off the recurrence chain)
-    fin &= isfinite(dp) && dp != 0.0;
-    double adp = fabs(dp);
-    g = fmax(g, adp);
-    nl = fma(adp, a * a, nl); dnl = fma(a, a, dnl);
-    nr = fma(adp, b * b, nr); dnr = fma(b, b, dnr);
-    if (i < nb - 1) { p = fma(-sigma, t, v.y * p); q = t; }
-    if ((i & 7) == 7) {
-      int ee = max_exp(p, q);
-      fin &= ee < 2047;
-      double f = pow2_scale(min(ee, 2045));
-      p *= f; q *= f;
-    }
-  };
-  if (zl) {
-    // rows and both probe vectors prefetched one group ahead (ping-pong)
-    constexpr int G = 4;
-    const int ng = nb / G;
-    double2 vx[G], vy[G];
-    double ax[G], ay[G], bx[G], by[G];
-    auto ld = [&](int i, double2 (&v)[G], double (&a)[G], double (&b)[G]) {
-#pragma unroll
-      for (int k = 0; k < G; ++k) { v[k] = __ldg(&DL[i + k]); a[k] = __ldg(&zl[i + k]); b[k] = __ldg(&zr[i + k]); }
-    };
-    int m = 0;
-    if (ng > 0) {
-      ld(0, vx, ax, bx);
-      for (; m + 1 < ng; m += 2) {
-        const int i = G * m;
-        if (i + kPfDist < nb) {
-          prefetch_l2(&DL[i + kPfDist]);
-          if ((i & 15) == 0) { prefetch_l2(&zl[i + kPfDist]); prefetch_l2(&zr[i + kPfDist]); }
-        }
-        ld(i + G, vy, ay, by);
-#pragma unroll
-        for (int k = 0; k < G; ++k) row(i + k, vx[k], ax[k], bx[k]);
-        if (m + 2 < ng) ld(i + 2 * G, vx, ax, bx);
-#pragma unroll
-        for (int k = 0; k < G; ++k) row(i + G + k, vy[k], ay[k], by[k]);
-      }
-      if (m < ng) {
-#pragma unroll
-        for (int k = 0; k < G; ++k) row(G * m + k, vx[k], ax[k], bx[k]);
-      }
-    }
-    for (int i = G * ng; i < nb; ++i) row(i, __ldg(&DL[i]), __ldg(&zl[i]), __ldg(&zr[i]));
-  } else {
-    stream_rows<8>(DL, 0, nb, [&](int i, const double2 &v) { row(i, v, 0.0, 0.0); });
-  }
-  Cand C;
-  C.sigma = sigma;
-  C.raw = fin ? g : CUDART_INF;
-  C.wgt = (fin && zl && dnl > 0 && dnr > 0) ? fmax(nl / dnl, nr / dnr) : CUDART_INF;
-  C.cluster = c;
-  C.which = which;
-  cand[id] = C;
-}
-
-// Shift choice (O9.3, reading 9 amended): all six candidates;
-// (i) some raw growth <= 8 spdiam: the least raw growth among those; (ii) else
-// the least raw growth among the candidates with weighted growth <= 64
-// spdiam; (iii) else the least raw growth if <= 1e8 spdiam; else error 2.
-// Ties: the earlier candidate (order L1 R1 L2 R2 L4 R4).
-__global__ void k_pick(const Node *nodes, const int *cl_parent, const Cand *cand, int ncl,
-                       double *sigma_out, int *tier_out, int *fail) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncl) return;
-  double spd = nodes[cl_parent[c]].spdiam;
-  const Cand *C = cand + 6 * c;
-  int b1 = -1, b2 = -1, b3 = -1;
-  for (int k = 0; k < 6; ++k) {
-    double g = C[k].raw;
-    if (g <= 8.0 * spd && (b1 < 0 || g < C[b1].raw)) b1 = k;
-    if (isfinite(g) && C[k].wgt <= 64.0 * spd && (b2 < 0 || g < C[b2].raw)) b2 = k;
-    if (b3 < 0 || g < C[b3].raw) b3 = k;
-  }
-  int tier = 0, best = b1;
-  if (best < 0) { tier = 1; best = b2; }
-  if (best < 0) { tier = 3; best = b3; if (!(C[b3].raw <= 1e8 * spd)) best = -1; }
-  if (best < 0) {
-    sigma_out[c] = 0.0;
-    tier_out[c] = 4;
-    fail[0] = 1;
-    return;
-  }
-  sigma_out[c] = C[best].sigma;
-  tier_out[c] = tier;
-}
-
-// Accepted child, pass 1 (one thread per cluster): projective chain, storing
-// t_i and the rescale exponent applied after row i (like the root).
-__global__ void k_child_chain(const Node *nodes, const int *cl_parent, const double *sigma, int ncl,
-                              int64_t stride, double *tbuf, int *sbuf) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncl) return;
-  const Node P = nodes[cl_parent[c]];
-  double sg = sigma[c];
-  double p = -sg, q = 1.0;
-  double *tb = tbuf + (int64_t)c * stride;
-  int *sb = sbuf + (int64_t)c * stride;
-  const int nb = P.nb;
-  stream_rows<8>(P.DL, 0, nb, [&](int i, const double2 &v) {
-    double t = fma(v.x, q, p);
-    tb[i] = t;
-    int sh = 0;
-    if (i < nb - 1) {
-      p = fma(-sg, t, v.y * p);
-      q = t;
-      if ((i & 7) == 7) {
-        int ee = max_exp(p, q);
-        sh = 1023 - min(max(ee, 1), 2045);
-        double f = pow2(sh);
-        p *= f; q *= f;
-      }
-    }
-    sb[i] = sh;
-  });
-}
-
-// Accepted child, pass 2 (parallel over clusters x rows): D+_i = t_i / t_{i-1}
-// (t_{i-1} brought to t_i's scale), LLD+_i = LD_i^2 / D+_i.
-__global__ void k_child_finish(const Node *nodes, const int *cl_parent, const int *cl_node, int ncl,
-                               int64_t stride, const double *tbuf, const int *sbuf,
-                               const double2 *__restrict__ LDv, double2 *out_base, int *fail) {
-  int c = blockIdx.y;
-  if (c >= ncl) return;
-  const Node P = nodes[cl_parent[c]];
-  int nb = P.nb;
-  const double *tb = tbuf + (int64_t)c * stride;
-  const int *sb = sbuf + (int64_t)c * stride;
-  double2 *out = out_base + (int64_t)c * stride;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
-    double tp = (i > 0) ? tb[i - 1] * pow2(sb[i - 1]) : 1.0;
-    double Dp = tb[i] / tp;
-    double ld2 = (i < nb - 1) ? LDv[P.row0 + i].y : 0.0;
-    double lld = (i < nb - 1) ? ld2 / Dp : 0.0;
-    if (!isfinite(Dp) || Dp == 0.0 || !isfinite(lld)) fail[0] = 1;
-    out[i] = make_double2(Dp, lld);
-  }
-  (void)cl_node;
 }
 
 }  // namespace mrrr

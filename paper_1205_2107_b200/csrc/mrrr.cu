@@ -191,21 +191,6 @@ struct KTimer {
 };
 
 // Launch helpers -----------------------------------------------------------
-void launch_bisect(int M, const Node *nodes, const Work *work, int nwork, const int *slot_j,
-                   double *lo, double *hi, double rtol, unsigned long long *ctr,
-                   cudaStream_t s) {
-  if (nwork == 0) return;
-  switch (M) {
-    case 1: k_bisect<1><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
-    case 2: k_bisect<2><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
-    case 3: k_bisect<3><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
-    case 8: k_bisect<8><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
-    default: k_bisect<4><<<nwork, 128, 0, s>>>(nodes, work, slot_j, lo, hi, rtol, 4000, ctr, ctr + 1); break;
-  }
-  CK(cudaGetLastError());
-  g_stats.kernel_launches++;
-}
-
 __global__ void k_root_interval(const Node *nodes, const Block *blocks, const int *root_nodes,
                                 int nroot, double *lo0, double *hi0, double tnrm_scaled) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;

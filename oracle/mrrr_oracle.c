@@ -527,6 +527,12 @@ static void cluster(ctx_t *c, const rrr_t *R, int64_t s, int64_t t, int depth) {
     }
     if (best >= 0) c->st->tier[1]++;
   }
+  if (best < 0) {  /* tier (iii) */
+    for (int k = 0; k < 6; ++k)
+      if (best < 0 || cg[k] < cg[best]) best = k;
+    if (!(cg[best] <= 1e8 * spd)) { free(DpA); free(C.D); c->err = 2; return; }
+    c->st->tier[2]++;
+  }
   double sigma;
   sigma = cs[best];
   free(DpA);

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(128) k_grid(const Node *nodes, int node, doubl
 // ends; an end that does not bracket index j is widened by doubling its
 // offset from the translated parent interval (plo - wl, phi + wu), and the
 // member is narrowed only once both ends bracket j.
-constexpr int kRWMembers = 8;
+constexpr int kRWMembers = 32;  // capacity; a work item holds <= kRWMembers slots
 constexpr int kRWT = 16, kRWRing = 6, kRWWarps = 4;
 
 struct RefWarpSmem {

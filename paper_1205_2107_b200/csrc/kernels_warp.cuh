@@ -492,6 +492,7 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
     }
   }
   double lam_fin = lam;
+  const long long clk_full = clock64();
   if (A.mode == 0) {
     // O10 RQC (readings 10, 24): stop when |delta| <= 4 eps |lambda| or
     // fl(lambda + delta) == lambda; a step leaving [lo, hi] from the interior
@@ -534,6 +535,7 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
       ++nfact;
       if (!conv && !tw.ok) { conv = true; failed = true; W.tix = spare; }
     }
+    const long long clk_rqc = clock64();
     W.tix = active ? tix : spare;
     tw = best;
     lam = lam_best;
@@ -549,6 +551,14 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
     w_twist_solve(W, lam, tw.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !failed);
     if (active && !failed) A.lam_out[tix] = lam_fin;
     if (active) atomicAdd(&A.ctr[0], nfact);
+    if (lane == 0) {  // slowest warp: cycles of the first factorization, the RQC loop, the solve;
+                      // factorizations of the warp (MRRR_TRACE)
+      const long long clk_end = clock64();
+      atomicMax(&A.ctr[4], (unsigned long long)(clk_full - clk0));
+      atomicMax(&A.ctr[5], (unsigned long long)(clk_rqc - clk_full));
+      atomicMax(&A.ctr[6], (unsigned long long)(clk_end - clk_rqc));
+      atomicMax(&A.ctr[7], nfact);
+    }
     return;
   }
   const double sc = 1.0 / sqrt(tw.nrm2);

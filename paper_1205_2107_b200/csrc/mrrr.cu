@@ -17,6 +17,7 @@
 #include "kernels_vec.cuh"
 #include "kernels_warp.cuh"
 #include "kernels_child.cuh"
+#include "kernels_probe.cuh"
 
 using namespace mrrr;
 
@@ -78,8 +79,18 @@ void dump(const char *name, const T *dptr, size_t count, cudaStream_t s) {
 // Host wall-clock trace of the phases (MRRR_TRACE=1), for overhead hunting.
 struct Trace {
   bool on;
+  int lvl = 0;
   std::chrono::steady_clock::time_point t0, tl;
-  Trace() : on(getenv("MRRR_TRACE") != nullptr) { t0 = tl = std::chrono::steady_clock::now(); }
+  Trace() : on(getenv("MRRR_TRACE") != nullptr) {
+    t0 = tl = std::chrono::steady_clock::now();
+    if (on) lvl = atoi(getenv("MRRR_TRACE"));
+  }
+  // MRRR_TRACE=2: also the steps inside a tree level (synchronising the stream)
+  void fine(cudaStream_t s, const char *what) {
+    if (lvl < 2) return;
+    cudaStreamSynchronize(s);
+    mark(what);
+  }
   void mark(const char *what) {
     if (!on) return;
     auto t = std::chrono::steady_clock::now();
@@ -679,11 +690,15 @@ int solve(Problem &P, int64_t *m_out) {
       wv.push_back(W);
     }
   };
-  constexpr int kTreeChunk = 32;
-  auto pick_wmax = [&](int64_t slots) {
-    int w = 128;
-    while (w > 8 && slots / w < 4 * 148) w >>= 1;
-    return w;
+  // members per refinement warp for a node/cluster of m members: a large
+  // cluster is packed 32 to a warp (4 shifts each while all are active, i.e.
+  // near-bisection work per bit), a small one spread thin (up to 64 shifts
+  // each, fewer rounds).  Depends on m alone, so every rank that holds a
+  // shared cluster forms the same work items (§8(e)).
+  static const int rw_env = getenv("MRRR_RW_CHUNK") ? atoi(getenv("MRRR_RW_CHUNK")) : 0;
+  auto rw_chunk = [&](int m) {
+    if (rw_env > 0) return std::min(rw_env, kRWMembers);
+    return m >= 512 ? 32 : m >= 128 ? 16 : 8;
   };
   {
     std::vector<Work> wv;
@@ -702,7 +717,7 @@ int solve(Problem &P, int64_t *m_out) {
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }
-      make_work(B.root_node, B.slot0, B.slot1, kRWMembers, wv);
+      make_work(B.root_node, B.slot0, B.slot1, rw_chunk(B.nb), wv);  // rank-invariant (block size)
     }
     Work *dwork = ar.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
@@ -890,6 +905,7 @@ int solve(Problem &P, int64_t *m_out) {
     CK(cudaEventRecord(ea, s2));
     launch_wvec(false, A, s2);
     CK(cudaEventRecord(eb, s2));
+    tr.fine(s2, "  vectors (side stream)");
     vec_ev.push_back({ea, eb});
     vec_done = t1;
   };
@@ -955,21 +971,15 @@ int solve(Problem &P, int64_t *m_out) {
       VecTask *dzt = lv.alloc<VecTask>(zt.size());
       h2d(dzt, zt.data(), zt.size(), s);
       const int ntask = (int)zt.size();
-      const int nseg = (int)((nbmax + kSeg - 1) / kSeg);
-      FwdCk *fck = lv.alloc<FwdCk>((size_t)nseg * (ntask + 32));
-      BwdCk *bck = lv.alloc<BwdCk>((size_t)nseg * (ntask + 32));
-      // one probe per warp: a lockstep solve spans the union of its lanes'
-      // row ranges (up to 2n rows for two distant twist indices); alone it
-      // spans n rows (or less when truncated)
-      auto items = make_warp_items(zt, 1);
-      CK(cudaMemsetAsync(zbuf, 0, (size_t)2 * ncl * nbmax * sizeof(double), s));
-      WarpItem *ditems = lv.alloc<WarpItem>(items.size());
-      h2d(ditems, items.data(), items.size(), s);
-      WVecArgs A{};
-      A.nodes = dnodes; A.LDv = LDv; A.tasks = dzt; A.items = ditems; A.nitems = (int)items.size();
-      A.lo = slo; A.hi = shi; A.fck = fck; A.bck = bck; A.ck_stride = ntask + 32; A.ntask = ntask;
-      A.zbuf = zbuf; A.zstride = nbmax; A.mode = 1; A.ctr = ctr + 16; A.slot_j = slot_j;
-      launch_wvec(true, A, s);
+      double *scratch = lv.alloc<double>((size_t)4 * ntask * nbmax);
+      tr.fine(s, "  alloc+upload");
+      ProbeArgs A{};
+      A.nodes = dnodes; A.tasks = dzt; A.ntask = ntask; A.LDv = LDv; A.lo = slo; A.hi = shi;
+      A.zbuf = zbuf; A.zstride = nbmax; A.scratch = scratch; A.ctr = ctr + 16;
+      k_probe<<<ntask, 64, 0, s>>>(A);
+      CK(cudaGetLastError());
+      g_stats.kernel_launches++;
+      tr.fine(s, "  probes");
     }
     double *dsig = lv.alloc<double>(ncl);
     int *dtier = lv.alloc<int>(ncl);
@@ -984,6 +994,7 @@ int solve(Problem &P, int64_t *m_out) {
       CK(cudaGetLastError());
       g_stats.kernel_launches++;
     }
+    tr.fine(s, "  child");
     g_stats.child_sweeps += 6 * ncl + ncl;
     // the child node entries are written before the translate kernel reads sigma
     int *slot_jl = slot_j;
@@ -1011,14 +1022,15 @@ int solve(Problem &P, int64_t *m_out) {
     nnodes += ncl;
     // verify + refine in child coordinates
     std::vector<Work> wv;
-    // chunks of kTreeChunk members from each cluster's start: the refinement of
+    // chunks of rw_chunk(m) members from each cluster's start: the refinement of
     // a cluster depends on the cluster alone, so every rank that holds a
     // shared cluster computes bitwise the same child intervals (§8(e))
-    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], kRWMembers, wv);
+    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], rw_chunk(cl_s1[c] - cl_s0[c]), wv);
     Work *dwork = lv.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
     launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, wlo, whi, 1, P.o.rtol_class,
                   dfail + 2, ctr + 2, ctr + 1, s);
+    tr.fine(s, "  refine");
     d2h(h_fail, dfail, 4, s);
     if (getenv("MRRR_DUMP")) {
       char nm[64];
@@ -1087,8 +1099,8 @@ int solve(Problem &P, int64_t *m_out) {
         for (int q0 = 0; q0 < h_nf;) {
           int q1 = q0;
           while (q1 < h_nf && tasks[fl[q1]].node == tasks[fl[q0]].node) ++q1;
-          for (int a = q0; a < q1; a += kRWMembers) {
-            Work W; W.node = tasks[fl[q0]].node; W.s0 = a; W.s1 = std::min(a + kRWMembers, q1); W.pad = 0;
+          for (int a = q0; a < q1; a += 8) {
+            Work W; W.node = tasks[fl[q0]].node; W.s0 = a; W.s1 = std::min(a + 8, q1); W.pad = 0;
             wv.push_back(W);
           }
           q0 = q1;
@@ -1137,8 +1149,9 @@ int solve(Problem &P, int64_t *m_out) {
   finish_w();
   d2h(h_ctr, ctr, 32, s);
   if (tr.on)
-    fprintf(stderr, "[mrrr] nudged factorizations: probes %llu (why %llu), vectors %llu (why %llu); probe max cycles: factorization %llu solve %llu\n",
-            h_ctr[18], h_ctr[19], h_ctr[10], h_ctr[11], h_ctr[20], h_ctr[21]);
+    fprintf(stderr, "[mrrr] probes %llu; nudged vector factorizations %llu (why %llu); slowest vector warp: "
+            "cycles full %llu rqc %llu solve %llu, max factorizations per warp %llu\n",
+            h_ctr[16], h_ctr[10], h_ctr[11], h_ctr[12], h_ctr[13], h_ctr[14], h_ctr[15]);
   tr.mark("vectors");
   g_stats.ms_vectors = tv.stop();
   g_stats.root_sweeps += h_ctr[0];

@@ -367,6 +367,7 @@ def main():
     launches = sum(int(s["kernel_launches"]) for s in stats)
     line = {"metric": METRIC, "value": value, "unit": "eigenpairs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "step_ms": [round(x, 3) for x in ms],
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "n": n, "k": k, "range": "all" if rng is None else

@@ -147,10 +147,13 @@ int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range,
  * (<= 24 n bytes per cluster node). */
 size_t mrrr_workspace_bytes(int64_t n, int64_t k);
 
-/* Workspace is taken from a library-owned stream-ordered memory pool per
- * device that keeps freed blocks mapped between calls (repeated solves do not
- * pay for remapping).  Releases that cached memory back to the driver; the
- * next call re-grows it.  Returns 0 or MRRR_ERR_CUDA. */
+/* Workspace is taken from library-owned device chunks per host thread and
+ * device, kept between calls (repeated solves allocate nothing); the buffers
+ * of mrrr_stemr_host come from a library-owned stream-ordered pool.  Releases
+ * the calling thread's chunks (cudaFree: synchronises the device) and the
+ * pool's cached memory; the next call re-grows them.  Must not run while a
+ * call of this thread is in flight (calls are synchronous, so it cannot).
+ * Returns 0 or MRRR_ERR_CUDA. */
 int mrrr_trim_workspace(void);
 
 /* Static description of a return code. */

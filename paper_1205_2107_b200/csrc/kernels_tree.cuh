@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
                                                                int max_rounds, int *fail,
                                                                unsigned long long *sweeps,
                                                                unsigned long long *safe_ctr) {
-  static_assert(M == 4, "cnt[] is sized for 4 shifts per lane");
+  static_assert(M >= 1 && M <= 4, "cnt[] is sized for at most 4 shifts per lane");
   __shared__ RefWarpSmem smem[kRWWarps];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * kRWWarps + wid;

@@ -1,4 +1,4 @@
-// kernels_warp.cuh -- a6 (and the a5 probes): twisted factorizations and
+// kernels_warp.cuh -- a6: twisted factorizations and
 // eigenvector solves in WARP LOCKSTEP.  One warp owns up to 32 eigenpairs of
 // ONE node (one lane each).  All lanes walk the node's rows in the same
 // order, so the rows are staged once per warp through a shared-memory ring of
@@ -62,9 +62,8 @@ __device__ __forceinline__ void w_tiles_up(const WarpCtx &W, int c0, int c1, F &
   for (int c = c0; c <= c1; ++c) {
     __pipeline_wait_prior(kRing - 2);
     __syncwarp();
-    const bool stop = f(c, c % kRing);
+    f(c, c % kRing);
     __syncwarp();
-    if (__any_sync(0xffffffffu, stop)) break;  // warp-uniform early end (truncated solves)
     const int cn = c + kRing - 1;
     w_issue(W, cn <= c1 ? cn : -1, cn % kRing);
   }
@@ -80,9 +79,8 @@ __device__ __forceinline__ void w_tiles_down(const WarpCtx &W, int c1, int c0, F
   for (int c = c1; c >= c0; --c) {
     __pipeline_wait_prior(kRing - 2);
     __syncwarp();
-    const bool stop = f(c, c % kRing);
+    f(c, c % kRing);
     __syncwarp();
-    if (__any_sync(0xffffffffu, stop)) break;  // warp-uniform early end (truncated solves)
     const int cn = c - (kRing - 1);
     w_issue(W, cn >= c0 ? cn : -1, (cn + 64 * kRing) % kRing);
   }
@@ -305,12 +303,8 @@ __device__ __forceinline__ void w_flush(const WarpCtx &W, int a, int b, double *
 // The ratios q_i / t_i (left) and b_{i+1} / u_{i+1} (right) are formed during
 // the replay with correctly rounded reciprocals (off the z recurrence), so
 // the z loops are pure multiply chains.
-// trunc: stop a side once every lane's |z| fell below 2^-100 (the rows not
-// written keep the caller's zeros); used for the probes, whose vectors only
-// weight the growth test, never for Z.
 __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int r, double scale, double *col,
-                                              bool active, bool trunc = false) {
-  constexpr double kNeg = 7.888609052210118e-31;  // 2^-100
+                                              bool active) {
   const int nb = W.nb, L = W.lane;
   WarpSmem &S = *W.sm;
   if (active) col[r] = scale;
@@ -359,8 +353,7 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
       for (int k = r1 - r0 - 1; k >= 0; --k) zstep(k);
     }
     w_flush(W, r0, r1 - 1, col);  // chunk rows r0 .. r1-1 from sA[0 ..]
-    const bool done = !active || r == 0 || (on && fabs(z1) < kNeg && fabs(z2) < kNeg);
-    return trunc && __all_sync(0xffffffffu, done);
+    return false;
   });
   // ---- right part, rows i > r, ascending: z_{i+1} = -LD_i (b_{i+1} / u_{i+1}) z_i
   const int cfirst = (active && r < nb - 1) ? r / kTR : W.nseg;
@@ -408,8 +401,7 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
       for (int i = lo_i; i < top; ++i) ystep(i - r0, i - lo_i);
     }
     w_flush(W, lo_i + 1, top, col);
-    const bool done = !active || r >= nb - 1 || (on && fabs(y1) < kNeg && fabs(y2) < kNeg);
-    return trunc && __all_sync(0xffffffffu, done);
+    return false;
   });
 }
 
@@ -435,9 +427,8 @@ struct WVecArgs {
   int ntask;
   double *Z; int64_t ldz;    // modes 0, 2: Z columns (tk.col), node rows at N.row0
   double *lam_out;           // modes 0, 2: final lambda (node coordinates) per task
-  double *zbuf; int64_t zstride;  // mode 1: unit vectors to zbuf + tk.col * zstride
-  int mode;                  // 0: RQC (reading 10); 1: one factorization (probes);
-                             // 2: one factorization at the bracket midpoint (RQC fallback)
+  int mode;                  // 0: RQC (reading 10); 2: one factorization at the bracket
+                             // midpoint (RQC fallback)
   int rqc_max;               // mode 0: factorizations before the fallback (3)
   int *fail_list;            // mode 0: tasks that did not converge (appended as task_base + tix)
   int *fail_count;
@@ -464,10 +455,7 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
   W.tix = active ? tix : spare;
   double lo = A.lo[tk.slot], hi = A.hi[tk.slot];
   if (N.nb == 1) {
-    if (active) {
-      if (A.mode != 1) { A.Z[tk.col * A.ldz + N.row0] = 1.0; A.lam_out[tix] = __ldg(&N.DL[0]).x; }
-      else A.zbuf[tk.col * A.zstride] = 1.0;
-    }
+    if (active) { A.Z[tk.col * A.ldz + N.row0] = 1.0; A.lam_out[tix] = __ldg(&N.DL[0]).x; }
     return;
   }
   double lam = (A.mode == 2 || isnan(tk.lam0)) ? 0.5 * (lo + hi) : tk.lam0;
@@ -561,22 +549,15 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
     }
     return;
   }
+  // mode 2: the vector of the one factorization at the refined midpoint
   const double sc = 1.0 / sqrt(tw.nrm2);
-  double *col = (A.mode == 2) ? A.Z + tk.col * A.ldz + N.row0 : A.zbuf + tk.col * A.zstride;
-  const long long clk1 = clock64();
-  w_twist_solve(W, lam, tw.r, sc, col, active, /*trunc=*/A.mode == 1);
-  const long long clk2 = clock64();
-  if (lane == 0) {  // per-phase cycles of the slowest warp (MRRR_TRACE)
-    atomicMax(&A.ctr[4], (unsigned long long)(clk1 - clk0));
-    atomicMax(&A.ctr[5], (unsigned long long)(clk2 - clk1));
-  }
+  w_twist_solve(W, lam, tw.r, sc, A.Z + tk.col * A.ldz + N.row0, active);
   if (active) {
-    if (A.mode == 2) A.lam_out[tix] = lam_fin;
+    A.lam_out[tix] = lam_fin;
     atomicAdd(&A.ctr[0], nfact);
   }
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerCta) k_wvectors(WVecArgs A) { wvec_body(A); }
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_wprobe(WVecArgs A) { wvec_body(A); }
 
 }  // namespace mrrr

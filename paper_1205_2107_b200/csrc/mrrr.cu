@@ -101,24 +101,67 @@ struct Trace {
   }
 };
 
-// Stream-ordered device allocations released (to the library pool) at scope exit.
+// Device workspace: per-thread, per-device bump allocators over chunks that
+// are kept across calls.  A solve allocates from two of them: the CALL
+// workspace (reset when a call starts; everything that lives until the
+// vectors) and the LEVEL workspace (reset at every tree level; probe scratch,
+// cluster lists, work items).  Reuse is safe by stream order: a call
+// synchronises its stream (and joins its side stream) before returning, and
+// level L+1's uploads and kernels follow level L's on the call's stream.  In
+// steady state no call allocates device memory at all: the stream-ordered
+// pool this replaces grew (remapped) at unpredictable levels, which cost up
+// to a second inside a level (MRRR_TRACE=2, n = 1e5) and 100-700 ms outliers
+// per solve at n = 20000.  mrrr_trim_workspace() frees the chunks.
+struct BumpWs {
+  std::vector<std::pair<char *, size_t>> chunks;
+  size_t chunk = 0, off = 0;
+  void *get(size_t bytes) {
+    bytes = (std::max<size_t>(bytes, 1) + 255) & ~size_t(255);
+    for (;;) {
+      if (chunk < chunks.size() && off + bytes <= chunks[chunk].second) {
+        void *p = chunks[chunk].first + off;
+        off += bytes;
+        return p;
+      }
+      if (chunk + 1 < chunks.size()) { ++chunk; off = 0; continue; }
+      size_t sz = std::max<size_t>(bytes, chunks.empty() ? (size_t(64) << 20) : 2 * chunks.back().second);
+      char *p = nullptr;
+      cudaError_t e = cudaMalloc((void **)&p, sz);
+      if (e == cudaErrorMemoryAllocation && sz > bytes) {
+        cudaGetLastError();
+        sz = bytes;
+        e = cudaMalloc((void **)&p, sz);
+      }
+      if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); throw MrrrError{MRRR_ERR_NOMEM}; }
+      CK(e);
+      chunks.push_back({p, sz});
+      chunk = chunks.size() - 1;
+      off = 0;
+    }
+  }
+  void reset() { chunk = 0; off = 0; }
+  void release() {
+    for (auto &c : chunks) cudaFree(c.first);
+    chunks.clear();
+    reset();
+  }
+};
+thread_local BumpWs g_ws_call[64], g_ws_level[64];
+
+BumpWs &device_ws(BumpWs *arr) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  return arr[dev & 63];
+}
+
+// Allocations from one workspace; the workspace is reset when the arena is
+// created (a call, a level) -- nothing is freed individually.
 struct DevArena {
-  cudaStream_t s;
-  cudaMemPool_t pool;
-  std::vector<void *> ptrs;
-  explicit DevArena(cudaStream_t st) : s(st), pool(lib_pool()) {}
+  BumpWs &ws;
+  explicit DevArena(BumpWs &w) : ws(w) { ws.reset(); }
   template <class T>
   T *alloc(size_t count) {
-    void *p = nullptr;
-    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, s);
-    if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); throw MrrrError{MRRR_ERR_NOMEM}; }
-    CK(e);
-    ptrs.push_back(p);
-    return (T *)p;
-  }
-  ~DevArena() {
-    for (void *p : ptrs) cudaFreeAsync(p, s);
+    return (T *)ws.get(count * sizeof(T));
   }
 };
 
@@ -418,18 +461,16 @@ std::vector<WarpItem> make_warp_items(const std::vector<VecTask> &t, int lanes =
   return v;
 }
 
-void launch_wvec(bool probe, WVecArgs A, cudaStream_t s) {
+void launch_wvec(WVecArgs A, cudaStream_t s) {
   const size_t smem = kWarpsPerCta * sizeof(WarpSmem);
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(k_wvectors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(k_wprobe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   const int grid = (A.nitems + kWarpsPerCta - 1) / kWarpsPerCta;
   if (grid == 0) return;
-  if (probe) k_wprobe<<<grid, 32 * kWarpsPerCta, smem, s>>>(A);
-  else k_wvectors<<<grid, 32 * kWarpsPerCta, smem, s>>>(A);
+  k_wvectors<<<grid, 32 * kWarpsPerCta, smem, s>>>(A);
   CK(cudaGetLastError());
   g_stats.kernel_launches++;
 }
@@ -439,10 +480,18 @@ void launch_wvec(bool probe, WVecArgs A, cudaStream_t s) {
 void launch_refine(const Node *nodes, const Work *work, int nwork, const int *slot_list,
                    const int *slot_j, double *lo, double *hi, const double *wlo, const double *whi,
                    int verify, double rtol, int *fail, unsigned long long *sweeps,
-                   unsigned long long *safe, cudaStream_t s) {
+                   unsigned long long *safe, cudaStream_t s, int M = 4) {
   if (nwork == 0) return;
-  k_refine_warp<4><<<(nwork + kRWWarps - 1) / kRWWarps, 32 * kRWWarps, 0, s>>>(
-      nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi, verify, rtol, 4000, fail, sweeps, safe);
+  const int grid = (nwork + kRWWarps - 1) / kRWWarps;
+  if (M == 1)
+    k_refine_warp<1><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
+                                                   verify, rtol, 4000, fail, sweeps, safe);
+  else if (M == 2)
+    k_refine_warp<2><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
+                                                   verify, rtol, 4000, fail, sweeps, safe);
+  else
+    k_refine_warp<4><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
+                                                   verify, rtol, 4000, fail, sweeps, safe);
   CK(cudaGetLastError());
   g_stats.kernel_launches++;
 }
@@ -472,7 +521,7 @@ struct HostNode {
 int solve(Problem &P, int64_t *m_out) {
   cudaStream_t s = P.s;
   const int64_t n = P.n;
-  DevArena ar(s);
+  DevArena ar(device_ws(g_ws_call));
   Trace tr;
   g_staging.reset();
   Timer tm(s), tall(s);
@@ -696,10 +745,17 @@ int solve(Problem &P, int64_t *m_out) {
   // each, fewer rounds).  Depends on m alone, so every rank that holds a
   // shared cluster forms the same work items (§8(e)).
   static const int rw_env = getenv("MRRR_RW_CHUNK") ? atoi(getenv("MRRR_RW_CHUNK")) : 0;
+  static const int rw_m_env = getenv("MRRR_RW_M") ? atoi(getenv("MRRR_RW_M")) : 0;
   auto rw_chunk = [&](int m) {
     if (rw_env > 0) return std::min(rw_env, kRWMembers);
     return m >= 512 ? 32 : m >= 128 ? 16 : 8;
   };
+  auto rw_chunk_tree = [&](int m) {
+    if (rw_env > 0) return std::min(rw_env, kRWMembers);
+    (void)m;
+    return 8;
+  };
+  const int rw_m_tree = rw_m_env > 0 ? rw_m_env : 1;
   {
     std::vector<Work> wv;
     kt_root.start(s);
@@ -903,7 +959,7 @@ int solve(Problem &P, int64_t *m_out) {
     cudaEvent_t ea, eb;
     CK(cudaEventCreate(&ea)); CK(cudaEventCreate(&eb));
     CK(cudaEventRecord(ea, s2));
-    launch_wvec(false, A, s2);
+    launch_wvec(A, s2);
     CK(cudaEventRecord(eb, s2));
     tr.fine(s2, "  vectors (side stream)");
     vec_ev.push_back({ea, eb});
@@ -955,7 +1011,7 @@ int solve(Problem &P, int64_t *m_out) {
       dnodes = nn; node_cap = ncap;
     }
     // per-level scratch, released (to the library pool) at the end of the level
-    DevArena lv(s);
+    DevArena lv(device_ws(g_ws_level));
     int *dcl_parent = lv.alloc<int>(ncl), *dcl_s0 = lv.alloc<int>(ncl), *dcl_s1 = lv.alloc<int>(ncl);
     h2d(dcl_parent, cl_parent.data(), ncl, s);
     h2d(dcl_s0, cl_s0.data(), ncl, s);
@@ -1025,11 +1081,11 @@ int solve(Problem &P, int64_t *m_out) {
     // chunks of rw_chunk(m) members from each cluster's start: the refinement of
     // a cluster depends on the cluster alone, so every rank that holds a
     // shared cluster computes bitwise the same child intervals (§8(e))
-    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], rw_chunk(cl_s1[c] - cl_s0[c]), wv);
+    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], rw_chunk_tree(cl_s1[c] - cl_s0[c]), wv);
     Work *dwork = lv.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);
     launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, wlo, whi, 1, P.o.rtol_class,
-                  dfail + 2, ctr + 2, ctr + 1, s);
+                  dfail + 2, ctr + 2, ctr + 1, s, rw_m_tree);
     tr.fine(s, "  refine");
     d2h(h_fail, dfail, 4, s);
     if (getenv("MRRR_DUMP")) {
@@ -1125,7 +1181,7 @@ int solve(Problem &P, int64_t *m_out) {
         F.fck = ar.alloc<FwdCk>((size_t)nseg_v * (h_nf + 32));
         F.bck = ar.alloc<BwdCk>((size_t)nseg_v * (h_nf + 32));
         F.Z = P.Z; F.ldz = P.ldz; F.lam_out = lam_c; F.mode = 2; F.ctr = ctr + 8;
-        launch_wvec(false, F, s);
+        launch_wvec(F, s);
         k_scatter<<<(h_nf + 255) / 256, 256, 0, s>>>(dfl, lam_c, h_nf, lam);
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
@@ -1353,6 +1409,8 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, doub
 }
 
 int mrrr_trim_workspace(void) {
+  for (auto &w : g_ws_call) w.release();
+  for (auto &w : g_ws_level) w.release();
   std::lock_guard<std::mutex> lk(g_pool_mu);
   for (auto &p : g_pools)
     if (p && cudaMemPoolTrimTo(p, 0) != cudaSuccess) return MRRR_ERR_CUDA;

@@ -917,19 +917,29 @@ int solve(Problem &P, int64_t *m_out) {
   double *lam = ar.alloc<double>(std::max<int64_t>(nslots, 1));
   int *fail_list = ar.alloc<int>(std::max<int64_t>(nslots, 1)), *fail_count = ar.alloc<int>(1);
   CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
-  cudaStream_t s2 = nullptr;
-  {
-    int lo_pr = 0, hi_pr = 0;
-    CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
-    CK(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, lo_pr));
-  }
-  struct StreamGuard {
-    cudaStream_t a, b;
-    ~StreamGuard() {
-      if (b) { cudaEvent_t e; cudaEventCreateWithFlags(&e, cudaEventDisableTiming); cudaEventRecord(e, b);
-               cudaStreamWaitEvent(a, e, 0); cudaEventDestroy(e); cudaStreamDestroy(b); }
+  // MRRR_VEC_MODE=1 (diagnostic): all vectors in one batch after the tree
+  static const int vec_mode = getenv("MRRR_VEC_MODE") ? atoi(getenv("MRRR_VEC_MODE")) : 0;
+  // batches go round-robin to kSide side streams so that they overlap one
+  // another as well as the tree (one side stream ran them back to back: the
+  // batches are latency-bound, ~12 ms each at n = 20000, and their chain
+  // outlasted the tree by ~50 ms)
+  constexpr int kSide = 4;
+  struct SideStreams {
+    cudaStream_t main, st[kSide] = {};
+    ~SideStreams() {
+      for (auto &x : st)
+        if (x) {
+          cudaEvent_t e;
+          cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+          cudaEventRecord(e, x);
+          cudaStreamWaitEvent(main, e, 0);
+          cudaEventDestroy(e);
+          cudaStreamDestroy(x);
+        }
     }
-  } sguard{s, s2};
+  } side{s};
+  for (auto &x : side.st) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  int nbatch = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vec_ev;
   const int nseg_v = (int)((nbmax + kSeg - 1) / kSeg);
   size_t vec_done = 0;
@@ -948,6 +958,7 @@ int solve(Problem &P, int64_t *m_out) {
     cudaEvent_t ready;
     CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     CK(cudaEventRecord(ready, s));
+    cudaStream_t s2 = side.st[nbatch++ % kSide];
     CK(cudaStreamWaitEvent(s2, ready, 0));
     cudaEventDestroy(ready);
     WVecArgs A{};
@@ -998,7 +1009,7 @@ int solve(Problem &P, int64_t *m_out) {
       }
     }
     const int ncl = (int)cl_parent.size();
-    if (vectors) flush_vectors();
+    if (vectors && (vec_mode == 0 || ncl == 0)) flush_vectors();
     if (ncl == 0) break;
     if (level + 1 > P.o.max_depth) throw MrrrError{MRRR_ERR_DEPTH};
     g_stats.nodes += ncl;
@@ -1119,12 +1130,14 @@ int solve(Problem &P, int64_t *m_out) {
   const int ntask = (int)tasks.size();
   g_stats.singletons = ntask;
   {
-    // join the side stream
-    cudaEvent_t j;
-    CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
-    CK(cudaEventRecord(j, s2));
-    CK(cudaStreamWaitEvent(s, j, 0));
-    cudaEventDestroy(j);
+    // join the side streams
+    for (auto x : side.st) {
+      cudaEvent_t j;
+      CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+      CK(cudaEventRecord(j, x));
+      CK(cudaStreamWaitEvent(s, j, 0));
+      cudaEventDestroy(j);
+    }
   }
   if (ntask > 0) {
     VecTask *dt = ar.alloc<VecTask>(ntask);

@@ -1,17 +1,30 @@
-// kernels_child.cuh -- a5: the cluster step of one tree level in one kernel
-// (SURVEY §8(c) O9), one warp per cluster.
+// kernels_child.cuh -- a5: the cluster step of one tree level (PAPER.md
+// L1092-1111), one CTA of five warps per cluster.
 //
-// Pass 1: lanes 0..5 run the six candidate shifts (offsets 1, 2, 4 beyond
-// each cluster end, readings 8 and 9) through the projective
-// stationary transform of the parent, accumulating the raw growth max|D+|
-// and the growth weighted by the parent's two end-eigenvalue vectors (the
-// probes of k_wprobe).  The tiered choice is made in-warp.  Pass 2: every
-// lane runs the chosen shift's transform (the same instruction stream), the
-// chain values of each 16-row tile go to shared memory and lane k forms row
-// k's (D+_k, LLD+_k = LD_k^2 / D+_k), stored with one coalesced 256-byte
-// write per tile.  Rows come through a shared-memory ring filled by cp.async
-// ahead of the chains (as in kernels_warp.cuh).  Replaces k_cand + k_pick +
-// k_child_chain + k_child_finish (same arithmetic as those).
+// Every dependent recurrence the step needs runs AT THE SAME TIME, one per warp:
+//   warps 0, 1   the parent's twisted factorization at the cluster's left end
+//                eigenvalue (stationary from the top, progressive from the
+//                bottom), warps 2, 3 the same at the right end -- the probes
+//                whose vectors weight the tier-(ii) growth test (reading 9);
+//   warp 4       the six candidate shifts (offsets 1, 2, 4 beyond each end,
+//                readings 8 and 9), one per lane, through the projective
+//                stationary transform of the parent, storing every D+_i.
+// After one chain's latency the rest is parallel over the rows: the twist
+// index r = argmin |gamma_i| of each probe, its |z| by log2 scans from r, the
+// raw growth max |D+| and the growth weighted by z_L^2 and z_R^2 of every
+// candidate (block reductions), the tiered choice, and the chosen child
+// (D+_i, LLD+_i = LD_i^2 / D+_i) written with coalesced stores.  (This
+// replaces a probe kernel followed by a two-pass child kernel: three chain
+// latencies per level instead of one.)
+//
+// Chain warps: every lane runs the same chain (no divergence) and lane k
+// keeps row k's values of a 16-row tile, divides once per tile and stores
+// them with one coalesced write; rows come through a per-warp cp.async ring.
+// Probe arrays, state before / at row i (kernels_vec.cuh notation):
+//   forward   s_i = p_i / q_i,   rho_i = z_i / z_{i+1} = -LD_i q_i / t_i
+//   backward  P_i = a_i / b_i,   sig_i = z_{i+1} / z_i = -LD_i b_{i+1} / u_{i+1}
+//   gamma_i = s_i + P_i + lambda; z_r = 1; only z_i^2 is used downstream
+//   (sum |D+_i| z_i^2 / sum z_i^2), so |z_i| is stored.
 #pragma once
 #include <cuda_pipeline.h>
 
@@ -19,188 +32,370 @@
 
 namespace mrrr {
 
-constexpr int kCT = 16;         // rows per tile
-constexpr int kCRing = 6;       // tiles in flight
-constexpr int kCWarps = 4;      // warps (clusters) per CTA
+constexpr int kCT = 16;     // rows per tile
+constexpr int kCRing = 6;   // tiles in flight per warp
+constexpr int kCSWarps = 5; // 4 probe chains + the candidate warp
+constexpr int kCSRows = 16; // scratch rows per cluster: D+ of 6 candidates, 4 per probe, |z| of 2
+
+struct ChainRing {
+  double2 rDL[kCRing][kCT];  // (D, LLD)
+  double2 rLD[kCRing][kCT];  // (LD, LD^2)
+};
 
 struct ChildSmem {
-  double2 rDL[kCRing][kCT];     // parent (D, LLD)
-  double rZL[kCRing][kCT], rZR[kCRing][kCT];  // probe vectors (pass 1)
-  double2 rLD[kCRing][kCT];     // block (LD, LD^2) (pass 2)
-  double tq[2][kCT];            // pass 2: t_i and q_i of the tile
+  ChainRing ring[kCSWarps];
+  double tq[2][6][kCT];      // candidate tile: t_i, q_i per candidate
+  double red[kCSWarps][20];  // per-warp partials of the growth reductions
+  unsigned okw[kCSWarps];    // per-warp finiteness masks of the candidates
+  double sig[6];             // the candidates' shifts
+  double am_v[4];            // per-warp argmin (probes)
+  int am_i[4];
+  int best, tier, bad;
+  double sg;
 };
 
 struct ChildArgs {
   const Node *nodes;
   const int *cl_parent, *cl_s0, *cl_s1;
-  const double *lo, *hi;
-  const double *zbuf;           // probes: rows of cluster c at zbuf + (2c + side) * zstride
-  int64_t zstride;
-  const double2 *LDv;           // global (LD, LD^2) per row
-  int ncl;
+  const double *lo, *hi;       // slot brackets (parent coordinates)
+  const double2 *LDv;          // global (LD, LD^2) per row
+  int c0, ncl;                 // clusters c0 .. ncl-1 (one CTA each)
   double rtol;
-  double2 *pool;                // child c's rows at pool + c * stride
+  double *scratch;             // kCSRows * zstride doubles per cluster of the launch
+  int64_t zstride;
+  double2 *pool;               // child c's rows at pool + c * stride
   int64_t stride;
   double *sigma_out;
   int *tier_out;
   int *fail;
+  unsigned long long *ctr;     // [0] probes (twisted factorizations)
 };
 
-__global__ void __launch_bounds__(32 * kCWarps) k_child_warp(ChildArgs A) {
-  __shared__ ChildSmem smem[kCWarps];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * kCWarps + wid;
+// Issue the rows of tile `tile` into ring slot `slot` (lanes 0-15: (D, LLD),
+// lanes 16-31: (LD, LD^2) when needed); always commits a group.
+__device__ __forceinline__ void cs_issue(ChainRing &R, const double2 *DL, const double2 *LD, int nb,
+                                         int tile, int slot, int lane, bool need_ld) {
+  const int k = lane & (kCT - 1);
+  if (tile >= 0) {
+    const int row = tile * kCT + k;
+    if (row < nb) {
+      if (lane < kCT) __pipeline_memcpy_async(&R.rDL[slot][k], &DL[row], sizeof(double2));
+      else if (need_ld) __pipeline_memcpy_async(&R.rLD[slot][k], &LD[row], sizeof(double2));
+    }
+  }
+  __pipeline_commit();
+}
+
+// Stationary chain of a probe: sS[i] = s_i (i < nb), sR[i] = rho_i (i < nb - 1).
+__device__ __forceinline__ void cs_probe_fwd(ChainRing &R, const double2 *DL, const double2 *LD, int nb,
+                                             double lam, int lane, double *sS, double *sR) {
+  const int ntile = (nb + kCT - 1) / kCT;
+#pragma unroll
+  for (int k = 0; k < kCRing - 1; ++k) cs_issue(R, DL, LD, nb, k < ntile ? k : -1, k, lane, true);
+  double p = -lam, q = 1.0;
+  for (int c = 0; c < ntile; ++c) {
+    __pipeline_wait_prior(kCRing - 2);
+    __syncwarp();
+    const int slot = c % kCRing, r0 = c * kCT, rows = min(kCT, nb - r0);
+    double kp = 0.0, kq = 1.0, kt = 1.0, kld = 0.0;
+    auto row = [&](int k) {
+      const int i = r0 + k;
+      const double2 v = R.rDL[slot][k];
+      const double ld = R.rLD[slot][k].x;
+      const double tt = fma(v.x, q, p);
+      if (lane == k) { kp = p; kq = q; kt = tt; kld = ld; }
+      if (i < nb - 1) { p = fma(-lam, tt, v.y * p); q = tt; }
+      if ((k & 7) == 7) {
+        const double f = pow2_scale(min(max(max_exp(p, q), 1), 2045));
+        p *= f; q *= f;
+      }
+    };
+    if (rows == kCT) {
+#pragma unroll
+      for (int k = 0; k < kCT; ++k) row(k);
+    } else {
+      for (int k = 0; k < rows; ++k) row(k);
+    }
+    if (lane < rows) {
+      const int i = r0 + lane;
+      sS[i] = kp / kq;
+      if (i < nb - 1) sR[i] = -kld * (kq / kt);
+    }
+    __syncwarp();
+    const int cn = c + kCRing - 1;
+    cs_issue(R, DL, LD, nb, cn < ntile ? cn : -1, cn % kCRing, lane, true);
+  }
+  __pipeline_wait_prior(0);
+}
+
+// Progressive chain of a probe: sP[i] = P_i (i < nb), sG[i] = sig_i (i < nb - 1).
+__device__ __forceinline__ void cs_probe_bwd(ChainRing &R, const double2 *DL, const double2 *LD, int nb,
+                                             double lam, int lane, double *sP, double *sG) {
+  const int ntile = (nb + kCT - 1) / kCT;
+#pragma unroll
+  for (int k = 0; k < kCRing - 1; ++k) cs_issue(R, DL, LD, nb, k < ntile ? ntile - 1 - k : -1, k, lane, true);
+  double a = __ldg(&DL[nb - 1]).x - lam, b = 1.0;
+  if (lane == 0) sP[nb - 1] = a;
+  for (int c = 0; c < ntile; ++c) {
+    __pipeline_wait_prior(kCRing - 2);
+    __syncwarp();
+    const int slot = c % kCRing, r0 = (ntile - 1 - c) * kCT;
+    const int top = min(r0 + kCT, nb - 1) - 1;  // rows r0 .. top step (row i from i+1)
+    double kb = 1.0, ku = 1.0, ka = 0.0, kld = 0.0;
+    auto row = [&](int k) {
+      const double2 v = R.rDL[slot][k];
+      const double ld = R.rLD[slot][k].x;
+      const double u = fma(v.y, b, a);
+      const double an = fma(-lam, u, v.x * a);
+      if (lane == k) { kb = b; ku = u; ka = an; kld = ld; }
+      a = an; b = u;
+      if ((k & 7) == 0) {
+        const double f = pow2_scale(min(max(max_exp(a, b), 1), 2045));
+        a *= f; b *= f;
+      }
+    };
+    if (top - r0 + 1 == kCT) {
+#pragma unroll
+      for (int k = kCT - 1; k >= 0; --k) row(k);
+    } else {
+      for (int k = top - r0; k >= 0; --k) row(k);
+    }
+    if (lane <= top - r0) {
+      const int i = r0 + lane;
+      sP[i] = ka / ku;
+      sG[i] = -kld * (kb / ku);
+    }
+    __syncwarp();
+    const int cn = c + kCRing - 1;
+    cs_issue(R, DL, LD, nb, cn < ntile ? ntile - 1 - cn : -1, cn % kCRing, lane, true);
+  }
+  __pipeline_wait_prior(0);
+}
+
+// The six candidate chains (lane k < 6 runs shift sig[k]; the other lanes
+// repeat lane 0's); DP[k * zstride + i] = D+_i of candidate k.
+__device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const double2 *DL, int nb,
+                                              double sigma, int lane, double *DP, int64_t zstride) {
+  const int ntile = (nb + kCT - 1) / kCT;
+#pragma unroll
+  for (int k = 0; k < kCRing - 1; ++k) cs_issue(R, DL, nullptr, nb, k < ntile ? k : -1, k, lane, false);
+  double p = -sigma, q = 1.0;
+  for (int c = 0; c < ntile; ++c) {
+    __pipeline_wait_prior(kCRing - 2);
+    __syncwarp();
+    const int slot = c % kCRing, r0 = c * kCT, rows = min(kCT, nb - r0);
+    auto row = [&](int k) {
+      const int i = r0 + k;
+      const double2 v = R.rDL[slot][k];
+      const double tt = fma(v.x, q, p);
+      if (lane < 6) { S.tq[0][lane][k] = tt; S.tq[1][lane][k] = q; }
+      if (i < nb - 1) { p = fma(-sigma, tt, v.y * p); q = tt; }
+      if ((k & 7) == 7) {
+        const double f = pow2_scale(min(max(max_exp(p, q), 1), 2045));
+        p *= f; q *= f;
+      }
+    };
+    if (rows == kCT) {
+#pragma unroll
+      for (int k = 0; k < kCT; ++k) row(k);
+    } else {
+      for (int k = 0; k < rows; ++k) row(k);
+    }
+    __syncwarp();
+    // D+_i = t_i / q_i, 96 divisions spread over the warp (off the chains)
+#pragma unroll
+    for (int e = lane; e < 6 * kCT; e += 32) {
+      const int cc = e >> 4, k = e & (kCT - 1);
+      if (k < rows) DP[cc * zstride + r0 + k] = S.tq[0][cc][k] / S.tq[1][cc][k];
+    }
+    __syncwarp();
+    const int cn = c + kCRing - 1;
+    cs_issue(R, DL, nullptr, nb, cn < ntile ? cn : -1, cn % kCRing, lane, false);
+  }
+  __pipeline_wait_prior(0);
+}
+
+__global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
+  __shared__ ChildSmem S;
+  const int c = A.c0 + blockIdx.x;
   if (c >= A.ncl) return;
-  ChildSmem &S = smem[wid];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const Node P = A.nodes[A.cl_parent[c]];
   const int nb = P.nb;
   const int s0 = A.cl_s0[c], s1 = A.cl_s1[c] - 1;
-  const double *zl = A.zbuf + (int64_t)(2 * c) * A.zstride;
-  const double *zr = A.zbuf + (int64_t)(2 * c + 1) * A.zstride;
-  const double2 *LDb = A.LDv + P.row0;
-  const int ntile = (nb + kCT - 1) / kCT;
+  const double2 *DL = P.DL, *LD = A.LDv + P.row0;
+  const int64_t zs = A.zstride;
+  double *base = A.scratch + (int64_t)blockIdx.x * kCSRows * zs;
+  double *DP = base;                 // 6 candidates
+  double *pr[2] = {base + 6 * zs, base + 10 * zs};  // per probe: s, P, rho, sig
+  double *zl = base + 14 * zs, *zr = base + 15 * zs;
 
-  // ---- candidate shift of this lane (lanes >= 6 duplicate lane 0)
-  const int which = lane < 6 ? lane : 0;
-  const double mult = (double)(1 << (which >> 1));
-  double sigma;
-  if ((which & 1) == 0) {
-    const double l = A.lo[s0], h = A.hi[s0];
-    const double dl = fmax(fmax(2.0 * (h - l), 2.0 * A.rtol * fabs(l)), 4.0 * kEps * fabs(l));
-    sigma = l - mult * dl;
+  // ---- phase 1: the five chains
+  if (wid < 4) {
+    const int side = wid >> 1;
+    const int slot = side == 0 ? s0 : s1;
+    const double lam = 0.5 * (A.lo[slot] + A.hi[slot]);
+    double *q = pr[side];
+    if ((wid & 1) == 0) cs_probe_fwd(S.ring[wid], DL, LD, nb, lam, lane, q, q + 2 * zs);
+    else cs_probe_bwd(S.ring[wid], DL, LD, nb, lam, lane, q + zs, q + 3 * zs);
   } else {
-    const double l = A.lo[s1], h = A.hi[s1];
-    const double dr = fmax(fmax(2.0 * (h - l), 2.0 * A.rtol * fabs(h)), 4.0 * kEps * fabs(h));
-    sigma = h + mult * dr;
-  }
-
-  // ---- pass 1: growth of the six candidates
-  auto issue1 = [&](int t) {
-    const int slot = t % kCRing;
-    const int k = lane & (kCT - 1), row = t * kCT + k;
-    if (t < ntile && row < nb) {
-      if (lane < kCT) __pipeline_memcpy_async(&S.rDL[slot][k], &P.DL[row], sizeof(double2));
-      else {
-        __pipeline_memcpy_async(&S.rZL[slot][k], &zl[row], sizeof(double));
-        __pipeline_memcpy_async(&S.rZR[slot][k], &zr[row], sizeof(double));
-      }
-    }
-    __pipeline_commit();
-  };
-  double p = -sigma, q = 1.0, g = 0.0, nl = 0.0, dnl = 0.0, nr = 0.0, dnr = 0.0;
-  bool fin = true;
-#pragma unroll
-  for (int k = 0; k < kCRing - 1; ++k) issue1(k);
-  for (int t = 0; t < ntile; ++t) {
-    __pipeline_wait_prior(kCRing - 2);
-    __syncwarp();
-    const int slot = t % kCRing, r0 = t * kCT;
-    const int rows = min(kCT, nb - r0);
-    auto row = [&](int k) {
-      const int i = r0 + k;
-      const double2 v = S.rDL[slot][k];
-      const double a = S.rZL[slot][k], b = S.rZR[slot][k];
-      const double tt = fma(v.x, q, p);
-      const double dp = tt * rcp_nr(q);  // D+_i (off the recurrence chain, branch-free)
-      fin &= isfinite(dp) && dp != 0.0;
-      const double adp = fabs(dp);
-      g = fmax(g, adp);
-      nl = fma(adp, a * a, nl); dnl = fma(a, a, dnl);
-      nr = fma(adp, b * b, nr); dnr = fma(b, b, dnr);
-      if (i < nb - 1) { p = fma(-sigma, tt, v.y * p); q = tt; }
-      if ((k & 7) == 7) {
-        const int ee = max_exp(p, q);
-        fin &= ee < 2047;
-        const double f = pow2_scale(min(ee, 2045));
-        p *= f; q *= f;
-      }
-    };
-    if (rows == kCT) {
-#pragma unroll
-      for (int k = 0; k < kCT; ++k) row(k);
+    const int which = lane < 6 ? lane : 0;
+    const double mult = (double)(1 << (which >> 1));
+    double sigma;
+    if ((which & 1) == 0) {
+      const double l = A.lo[s0], h = A.hi[s0];
+      const double dl = fmax(fmax(2.0 * (h - l), 2.0 * A.rtol * fabs(l)), 4.0 * kEps * fabs(l));
+      sigma = l - mult * dl;
     } else {
-      for (int k = 0; k < rows; ++k) row(k);
+      const double l = A.lo[s1], h = A.hi[s1];
+      const double dr = fmax(fmax(2.0 * (h - l), 2.0 * A.rtol * fabs(h)), 4.0 * kEps * fabs(h));
+      sigma = h + mult * dr;
     }
-    __syncwarp();
-    issue1(t + kCRing - 1);
+    cs_candidates(S.ring[4], S, DL, nb, sigma, lane, DP, zs);
+    if (lane < 6) S.sig[lane] = sigma;
   }
-  __pipeline_wait_prior(0);
-  const double raw = fin ? g : CUDART_INF;
-  const double wgt = (fin && dnl > 0 && dnr > 0) ? fmax(nl / dnl, nr / dnr) : CUDART_INF;
+  __syncthreads();
 
-  // ---- tiered choice (reading 9, as k_pick)
-  const double spd = P.spdiam;
-  int b1 = -1, b2 = -1, b3 = -1;
-  double r1 = 0, r2 = 0, r3 = 0;
+  // ---- phase 2: each probe's twist index and |z| (warps 2 side, 2 side + 1)
+  if (wid < 4) {
+    const int side = wid >> 1, gt = tid & 63;
+    const double lam = 0.5 * (A.lo[side == 0 ? s0 : s1] + A.hi[side == 0 ? s0 : s1]);
+    const double *sS = pr[side], *sP = pr[side] + zs, *sR = pr[side] + 2 * zs, *sG = pr[side] + 3 * zs;
+    double *z = side == 0 ? zl : zr;
+    double bv = CUDART_INF;
+    int bi = nb;
+#pragma unroll 4
+    for (int i = gt; i < nb; i += 64) {
+      const double g = fabs(sS[i] + sP[i] + lam);
+      if (g < bv) { bv = g; bi = i; }  // ascending i per thread: first minimum kept
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { S.am_v[wid] = bv; S.am_i[wid] = bi; }
+    // the two warps of a probe meet here (named barrier per probe)
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + side));
+    const double v0 = S.am_v[2 * side], v1 = S.am_v[2 * side + 1];
+    const int i0 = S.am_i[2 * side], i1 = S.am_i[2 * side + 1];
+    int r = (v1 < v0 || (v1 == v0 && i1 < i0)) ? i1 : i0;
+    if (r >= nb) r = nb - 1;  // no finite gamma: any twist (the vector only weights)
+    // |z| by a two-level scan of log2 |ratio|: lane l owns a contiguous run of
+    // the side's ratios (sum, warp scan of the sums, second walk writing z)
+    const bool up = (wid & 1) == 0;     // up: rows r-1 .. 0 from rho; down: rows r+1 .. nb-1 from sig
+    const int m = up ? r : nb - 1 - r;  // ratios on this side
+    if (up && lane == 0) z[r] = 1.0;
+    const int chunk = (m + 31) >> 5, j0 = min(lane * chunk, m), j1 = min(j0 + chunk, m);
+    auto lval = [&](int j) {
+      const double x = up ? sR[r - 1 - j] : sG[r + j];
+      return fmin(fmax(log2(fabs(x)), -4096.0), 4096.0);
+    };
+    double run = 0.0;
+    for (int j = j0; j < j1; ++j) run += lval(j);
+    double incl = run;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    double acc = incl - run;  // exclusive prefix of this lane's run
+    for (int j = j0; j < j1; ++j) {
+      acc += lval(j);
+      if (up) z[r - 1 - j] = exp2(acc);
+      else z[r + j + 1] = exp2(acc);
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 3: growth of the candidates, raw and weighted (all threads)
+  double g[6], nl[6], nr[6], dnl = 0.0, dnr = 0.0;
+  unsigned okm = 0x3f;
 #pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    const double gk = __shfl_sync(0xffffffffu, raw, k);
-    const double wk = __shfl_sync(0xffffffffu, wgt, k);
-    if (gk <= 8.0 * spd && (b1 < 0 || gk < r1)) { b1 = k; r1 = gk; }
-    if (isfinite(gk) && wk <= 64.0 * spd && (b2 < 0 || gk < r2)) { b2 = k; r2 = gk; }
-    if (b3 < 0 || gk < r3) { b3 = k; r3 = gk; }
+  for (int k = 0; k < 6; ++k) { g[k] = 0.0; nl[k] = 0.0; nr[k] = 0.0; }
+  for (int i = tid; i < nb; i += 32 * kCSWarps) {
+    const double a = zl[i], b = zr[i];
+    const double a2 = a * a, b2 = b * b;
+    dnl += a2; dnr += b2;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double d = DP[k * zs + i];
+      const double ad = fabs(d);
+      if (!(isfinite(d) && d != 0.0)) okm &= ~(1u << k);
+      g[k] = fmax(g[k], ad);
+      nl[k] = fma(ad, a2, nl[k]);
+      nr[k] = fma(ad, b2, nr[k]);
+    }
   }
-  int tier = 0, best = b1;
-  if (best < 0) { tier = 1; best = b2; }
-  if (best < 0) { tier = 3; best = b3; if (!(r3 <= 1e8 * spd)) best = -1; }
-  if (best < 0) {
-    if (lane == 0) { A.sigma_out[c] = 0.0; A.tier_out[c] = 4; A.fail[0] = 1; }
-    return;
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      g[k] = fmax(g[k], __shfl_xor_sync(0xffffffffu, g[k], o));
+      nl[k] += __shfl_xor_sync(0xffffffffu, nl[k], o);
+      nr[k] += __shfl_xor_sync(0xffffffffu, nr[k], o);
+    }
+    dnl += __shfl_xor_sync(0xffffffffu, dnl, o);
+    dnr += __shfl_xor_sync(0xffffffffu, dnr, o);
+    okm &= __shfl_xor_sync(0xffffffffu, okm, o);
   }
-  const double sg = __shfl_sync(0xffffffffu, sigma, best);
-  if (lane == 0) { A.sigma_out[c] = sg; A.tier_out[c] = tier; }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { S.red[wid][k] = g[k]; S.red[wid][6 + k] = nl[k]; S.red[wid][12 + k] = nr[k]; }
+    S.red[wid][18] = dnl; S.red[wid][19] = dnr; S.okw[wid] = okm;
+  }
+  __syncthreads();
 
-  // ---- pass 2: the chosen child, (D+_i, LLD+_i = LD_i^2 / D+_i)
+  // ---- phase 4: the tiered choice (reading 9) by thread 0
+  if (tid == 0) {
+    double G[6], NL[6], NR[6], DNL = 0.0, DNR = 0.0;
+    unsigned ok = 0x3f;
+    for (int k = 0; k < 6; ++k) { G[k] = 0.0; NL[k] = 0.0; NR[k] = 0.0; }
+    for (int w = 0; w < kCSWarps; ++w) {
+      for (int k = 0; k < 6; ++k) {
+        G[k] = fmax(G[k], S.red[w][k]);
+        NL[k] += S.red[w][6 + k];
+        NR[k] += S.red[w][12 + k];
+      }
+      DNL += S.red[w][18]; DNR += S.red[w][19];
+      ok &= S.okw[w];
+    }
+    const double spd = P.spdiam;
+    int b1 = -1, b2 = -1, b3 = -1;
+    double r1 = 0, r2 = 0, r3 = 0;
+    for (int k = 0; k < 6; ++k) {
+      const bool fin = (ok >> k) & 1u;
+      const double gk = fin ? G[k] : CUDART_INF;
+      const double wk = (fin && DNL > 0 && DNR > 0) ? fmax(NL[k] / DNL, NR[k] / DNR) : CUDART_INF;
+      if (gk <= 8.0 * spd && (b1 < 0 || gk < r1)) { b1 = k; r1 = gk; }
+      if (isfinite(gk) && wk <= 64.0 * spd && (b2 < 0 || gk < r2)) { b2 = k; r2 = gk; }
+      if (b3 < 0 || gk < r3) { b3 = k; r3 = gk; }
+    }
+    int tier = 0, best = b1;
+    if (best < 0) { tier = 1; best = b2; }
+    if (best < 0) { tier = 3; best = b3; if (!(r3 <= 1e8 * spd)) best = -1; }
+    S.best = best;
+    S.tier = best < 0 ? 4 : tier;
+    S.sg = best < 0 ? 0.0 : S.sig[best];
+    S.bad = 0;
+    A.sigma_out[c] = S.sg;
+    A.tier_out[c] = S.tier;
+    if (best < 0) A.fail[0] = 1;
+    atomicAdd(&A.ctr[0], 2ull);
+  }
+  __syncthreads();
+  const int best = S.best;
+  if (best < 0) return;
+
+  // ---- phase 5: the chosen child, (D+_i, LLD+_i = LD_i^2 / D+_i), coalesced
   double2 *out = A.pool + (int64_t)c * A.stride;
-  auto issue2 = [&](int t) {
-    const int slot = t % kCRing;
-    const int k = lane & (kCT - 1), row = t * kCT + k;
-    if (t < ntile && row < nb) {
-      if (lane < kCT) __pipeline_memcpy_async(&S.rDL[slot][k], &P.DL[row], sizeof(double2));
-      else __pipeline_memcpy_async(&S.rLD[slot][k], &LDb[row], sizeof(double2));
-    }
-    __pipeline_commit();
-  };
-  p = -sg; q = 1.0;
+  const double *dp = DP + best * zs;
   bool bad = false;
-#pragma unroll
-  for (int k = 0; k < kCRing - 1; ++k) issue2(k);
-  for (int t = 0; t < ntile; ++t) {
-    __pipeline_wait_prior(kCRing - 2);
-    __syncwarp();
-    const int slot = t % kCRing, r0 = t * kCT;
-    const int rows = min(kCT, nb - r0);
-    auto row = [&](int k) {
-      const int i = r0 + k;
-      const double2 v = S.rDL[slot][k];
-      const double tt = fma(v.x, q, p);
-      if (lane == 0) { S.tq[0][k] = tt; S.tq[1][k] = q; }
-      if (i < nb - 1) { p = fma(-sg, tt, v.y * p); q = tt; }
-      if ((k & 7) == 7) {
-        const int ee = max_exp(p, q);
-        const double f = pow2_scale(min(max(ee, 1), 2045));
-        p *= f; q *= f;
-      }
-    };
-    if (rows == kCT) {
-#pragma unroll
-      for (int k = 0; k < kCT; ++k) row(k);
-    } else {
-      for (int k = 0; k < rows; ++k) row(k);
-    }
-    __syncwarp();
-    if (lane < rows) {
-      const int i = r0 + lane;
-      const double Dp = S.tq[0][lane] / S.tq[1][lane];
-      const double ld2 = (i < nb - 1) ? S.rLD[slot][lane].y : 0.0;
-      const double lld = (i < nb - 1) ? ld2 / Dp : 0.0;
-      bad |= !isfinite(Dp) || Dp == 0.0 || !isfinite(lld);
-      out[i] = make_double2(Dp, lld);
-    }
-    __syncwarp();
-    issue2(t + kCRing - 1);
+#pragma unroll 4
+  for (int i = tid; i < nb; i += 32 * kCSWarps) {
+    const double Dp = dp[i];
+    const double lld = (i < nb - 1) ? __ldg(&LD[i]).y / Dp : 0.0;
+    bad |= !isfinite(Dp) || Dp == 0.0 || !isfinite(lld);
+    out[i] = make_double2(Dp, lld);
   }
-  __pipeline_wait_prior(0);
   if (__any_sync(0xffffffffu, bad) && lane == 0) A.fail[0] = 1;
 }
 

@@ -17,7 +17,6 @@
 #include "kernels_vec.cuh"
 #include "kernels_warp.cuh"
 #include "kernels_child.cuh"
-#include "kernels_probe.cuh"
 
 using namespace mrrr;
 
@@ -124,7 +123,9 @@ struct BumpWs {
         return p;
       }
       if (chunk + 1 < chunks.size()) { ++chunk; off = 0; continue; }
-      size_t sz = std::max<size_t>(bytes, chunks.empty() ? (size_t(64) << 20) : 2 * chunks.back().second);
+      // geometric growth up to 1 GiB chunks; a larger request gets its own size
+      size_t sz = std::max<size_t>(bytes, chunks.empty() ? (size_t(64) << 20)
+                                                         : std::min<size_t>(2 * chunks.back().second, size_t(1) << 30));
       char *p = nullptr;
       cudaError_t e = cudaMalloc((void **)&p, sz);
       if (e == cudaErrorMemoryAllocation && sz > bytes) {
@@ -152,6 +153,33 @@ BumpWs &device_ws(BumpWs *arr) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
   return arr[dev & 63];
+}
+
+// A grow-only device buffer kept across calls, for the one large per-level
+// scratch whose size climbs level by level (in a bump workspace every larger
+// level would strand the previous chunk).  Growing frees the old buffer:
+// cudaFree waits for the device, so nothing still reads it.
+struct GrowBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+};
+thread_local GrowBuf g_child_scratch_arr[64];
+GrowBuf &child_scratch() {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  return g_child_scratch_arr[d & 63];
+}
+void *grow_buffer(GrowBuf &b, size_t bytes) {
+  if (bytes <= b.cap) return b.p;
+  if (b.p) { CK(cudaFree(b.p)); b.p = nullptr; b.cap = 0; }
+  const size_t want = bytes + bytes / 4;
+  cudaError_t e = cudaMalloc(&b.p, want);
+  size_t got = want;
+  if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); e = cudaMalloc(&b.p, bytes); got = bytes; }
+  if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); b.p = nullptr; throw MrrrError{MRRR_ERR_NOMEM}; }
+  CK(e);
+  b.cap = got;
+  return b.p;
 }
 
 // Allocations from one workspace; the workspace is reset when the arena is
@@ -940,41 +968,54 @@ int solve(Problem &P, int64_t *m_out) {
   } side{s};
   for (auto &x : side.st) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
   int nbatch = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vec_ev;
+  // checkpoint columns: one buffer of ck_cap tasks per side stream, reused by
+  // the stream's next batch (stream order); a level's singletons go out in
+  // pieces of at most ck_cap - 32 tasks, so the checkpoints take
+  // kSide * ck_cap * nseg * 48 bytes whatever the batch sizes
+  const int64_t ck_cap = std::max<int64_t>(256, (nslots + 2 * kSide - 1) / (2 * kSide)) + 32;
   const int nseg_v = (int)((nbmax + kSeg - 1) / kSeg);
+  FwdCk *ck_f[kSide] = {};
+  BwdCk *ck_b[kSide] = {};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vec_ev;
   size_t vec_done = 0;
   auto flush_vectors = [&]() {
-    const size_t t0 = vec_done, t1 = tasks.size();
-    if (t1 == t0) return;
-    const int nbt = (int)(t1 - t0);
-    std::vector<VecTask> bt(tasks.begin() + t0, tasks.begin() + t1);
-    VecTask *dtb = ar.alloc<VecTask>(nbt);
-    FwdCk *fck = ar.alloc<FwdCk>((size_t)nseg_v * (nbt + 32));
-    BwdCk *bck = ar.alloc<BwdCk>((size_t)nseg_v * (nbt + 32));
-    auto items = make_warp_items(bt);
-    WarpItem *ditems = ar.alloc<WarpItem>(items.size());
-    h2d(dtb, bt.data(), nbt, s);
-    h2d(ditems, items.data(), items.size(), s);
-    cudaEvent_t ready;
-    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    CK(cudaEventRecord(ready, s));
-    cudaStream_t s2 = side.st[nbatch++ % kSide];
-    CK(cudaStreamWaitEvent(s2, ready, 0));
-    cudaEventDestroy(ready);
-    WVecArgs A{};
-    A.nodes = dnodes; A.LDv = LDv; A.tasks = dtb; A.items = ditems; A.nitems = (int)items.size();
-    A.lo = slo; A.hi = shi; A.fck = fck; A.bck = bck; A.ck_stride = nbt + 32; A.ntask = nbt;
-    A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam + t0; A.mode = 0; A.ctr = ctr + 8;
-    A.slot_j = slot_j; A.rqc_max = std::max(1, P.o.rqc_max);
-    A.fail_list = fail_list; A.fail_count = fail_count; A.task_base = (int)t0;
-    cudaEvent_t ea, eb;
-    CK(cudaEventCreate(&ea)); CK(cudaEventCreate(&eb));
-    CK(cudaEventRecord(ea, s2));
-    launch_wvec(A, s2);
-    CK(cudaEventRecord(eb, s2));
-    tr.fine(s2, "  vectors (side stream)");
-    vec_ev.push_back({ea, eb});
-    vec_done = t1;
+    for (size_t t0 = vec_done; t0 < tasks.size();) {
+      const size_t t1 = std::min<size_t>(tasks.size(), t0 + (size_t)(ck_cap - 32));
+      const int nbt = (int)(t1 - t0);
+      std::vector<VecTask> bt(tasks.begin() + t0, tasks.begin() + t1);
+      VecTask *dtb = ar.alloc<VecTask>(nbt);
+      const int sk = nbatch % kSide;
+      if (!ck_f[sk]) {
+        ck_f[sk] = ar.alloc<FwdCk>((size_t)nseg_v * ck_cap);
+        ck_b[sk] = ar.alloc<BwdCk>((size_t)nseg_v * ck_cap);
+      }
+      auto items = make_warp_items(bt);
+      WarpItem *ditems = ar.alloc<WarpItem>(items.size());
+      h2d(dtb, bt.data(), nbt, s);
+      h2d(ditems, items.data(), items.size(), s);
+      cudaEvent_t ready;
+      CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      CK(cudaEventRecord(ready, s));
+      cudaStream_t s2 = side.st[sk];
+      ++nbatch;
+      CK(cudaStreamWaitEvent(s2, ready, 0));
+      cudaEventDestroy(ready);
+      WVecArgs A{};
+      A.nodes = dnodes; A.LDv = LDv; A.tasks = dtb; A.items = ditems; A.nitems = (int)items.size();
+      A.lo = slo; A.hi = shi; A.fck = ck_f[sk]; A.bck = ck_b[sk]; A.ck_stride = ck_cap; A.ntask = nbt;
+      A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam + t0; A.mode = 0; A.ctr = ctr + 8;
+      A.slot_j = slot_j; A.rqc_max = std::max(1, P.o.rqc_max);
+      A.fail_list = fail_list; A.fail_count = fail_count; A.task_base = (int)t0;
+      cudaEvent_t ea, eb;
+      CK(cudaEventCreate(&ea)); CK(cudaEventCreate(&eb));
+      CK(cudaEventRecord(ea, s2));
+      launch_wvec(A, s2);
+      CK(cudaEventRecord(eb, s2));
+      tr.fine(s2, "  vectors (side stream)");
+      vec_ev.push_back({ea, eb});
+      t0 = t1;
+    }
+    vec_done = tasks.size();
   };
   Timer ttree(s);
   for (;;) {
@@ -1027,41 +1068,30 @@ int solve(Problem &P, int64_t *m_out) {
     h2d(dcl_parent, cl_parent.data(), ncl, s);
     h2d(dcl_s0, cl_s0.data(), ncl, s);
     h2d(dcl_s1, cl_s1.data(), ncl, s);
-    // tier-(ii) vectors: parent twisted solve at both end eigenvalues
-    double *zbuf = lv.alloc<double>((size_t)2 * ncl * nbmax);
-    {
-      std::vector<VecTask> zt(2 * ncl);
-      for (int c = 0; c < ncl; ++c) {
-        zt[2 * c] = {cl_s0[c], cl_parent[c], 2 * c, NAN};
-        zt[2 * c + 1] = {cl_s1[c] - 1, cl_parent[c], 2 * c + 1, NAN};
-      }
-      VecTask *dzt = lv.alloc<VecTask>(zt.size());
-      h2d(dzt, zt.data(), zt.size(), s);
-      const int ntask = (int)zt.size();
-      double *scratch = lv.alloc<double>((size_t)4 * ntask * nbmax);
-      tr.fine(s, "  alloc+upload");
-      ProbeArgs A{};
-      A.nodes = dnodes; A.tasks = dzt; A.ntask = ntask; A.LDv = LDv; A.lo = slo; A.hi = shi;
-      A.zbuf = zbuf; A.zstride = nbmax; A.scratch = scratch; A.ctr = ctr + 16;
-      k_probe<<<ntask, 64, 0, s>>>(A);
-      CK(cudaGetLastError());
-      g_stats.kernel_launches++;
-      tr.fine(s, "  probes");
-    }
+    // a5 cluster step: probes, six candidates, choice, chosen child (one kernel)
+    // the step's scratch (kCSRows rows of nbmax doubles per cluster) is capped
+    // at 16 GB: beyond, clusters go through in groups that reuse it (stream
+    // order; each group costs one more chain latency)
+    const int cgrp =
+        (int)std::max<int64_t>(1, std::min<int64_t>(ncl, (int64_t)(16e9 / (8.0 * kCSRows * nbmax))));
+    double *scratch = (double *)grow_buffer(child_scratch(), (size_t)kCSRows * cgrp * nbmax * sizeof(double));
     double *dsig = lv.alloc<double>(ncl);
     int *dtier = lv.alloc<int>(ncl);
     double2 *pool = ar.alloc<double2>((size_t)ncl * nbmax);  // child RRRs live until the vectors
-    {
+    tr.fine(s, "  alloc+upload");
+    for (int c0 = 0; c0 < ncl; c0 += cgrp) {
       ChildArgs C{};
       C.nodes = dnodes; C.cl_parent = dcl_parent; C.cl_s0 = dcl_s0; C.cl_s1 = dcl_s1;
-      C.lo = slo; C.hi = shi; C.zbuf = zbuf; C.zstride = nbmax; C.LDv = LDv; C.ncl = ncl;
-      C.rtol = P.o.rtol_class; C.pool = pool; C.stride = nbmax; C.sigma_out = dsig;
-      C.tier_out = dtier; C.fail = dfail + 1;
-      k_child_warp<<<(ncl + kCWarps - 1) / kCWarps, 32 * kCWarps, 0, s>>>(C);
+      C.lo = slo; C.hi = shi; C.LDv = LDv; C.c0 = c0; C.ncl = std::min(ncl, c0 + cgrp);
+      C.rtol = P.o.rtol_class;
+      C.scratch = scratch; C.zstride = nbmax;
+      C.pool = pool; C.stride = nbmax; C.sigma_out = dsig; C.tier_out = dtier; C.fail = dfail + 1;
+      C.ctr = ctr + 16;
+      k_child_step<<<C.ncl - c0, 32 * kCSWarps, 0, s>>>(C);
       CK(cudaGetLastError());
       g_stats.kernel_launches++;
     }
-    tr.fine(s, "  child");
+    tr.fine(s, "  child step");
     g_stats.child_sweeps += 6 * ncl + ncl;
     // the child node entries are written before the translate kernel reads sigma
     int *slot_jl = slot_j;
@@ -1107,7 +1137,6 @@ int solve(Problem &P, int64_t *m_out) {
       snprintf(nm, sizeof nm, "L%d_s0.bin", level); dump(nm, dcl_s0, ncl, s);
       snprintf(nm, sizeof nm, "L%d_s1.bin", level); dump(nm, dcl_s1, ncl, s);
       snprintf(nm, sizeof nm, "L%d_parent.bin", level); dump(nm, dcl_parent, ncl, s);
-      snprintf(nm, sizeof nm, "L%d_zbuf.bin", level); dump(nm, zbuf, (size_t)2 * ncl * nbmax, s);
       snprintf(nm, sizeof nm, "L%d_lo.bin", level); dump(nm, slo, nslots, s);
       snprintf(nm, sizeof nm, "L%d_hi.bin", level); dump(nm, shi, nslots, s);
     }
@@ -1424,6 +1453,10 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, doub
 int mrrr_trim_workspace(void) {
   for (auto &w : g_ws_call) w.release();
   for (auto &w : g_ws_level) w.release();
+  for (auto &b : g_child_scratch_arr) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr; b.cap = 0;
+  }
   std::lock_guard<std::mutex> lk(g_pool_mu);
   for (auto &p : g_pools)
     if (p && cudaMemPoolTrimTo(p, 0) != cudaSuccess) return MRRR_ERR_CUDA;

@@ -296,6 +296,8 @@ def test_config5_random_100000(torch_cuda, P, oracle_mod):
     pairs, seeded random pairs), Sturm placement of sampled
     eigenvalues with an independent count, oracle index windows."""
     torch = torch_cuda
+    torch.cuda.empty_cache()  # Z alone is 80 GB: start from the earlier tests' caches released
+    P.trim_workspace()
     n = 100000
     d, e = W.random_uniform(n, 0)
     dd, ee = torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda")

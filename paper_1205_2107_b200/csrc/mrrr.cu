@@ -75,6 +75,22 @@ void dump(const char *name, const T *dptr, size_t count, cudaStream_t s) {
   if (f) { fwrite(h.data(), sizeof(T), count, f); fclose(f); }
 }
 
+constexpr int kSide = 4;  // side streams for the vector batches
+cudaStream_t *side_streams() {
+  thread_local cudaStream_t st[64][kSide] = {};
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  cudaStream_t *x = st[d & 63];
+  if (!x[0])
+    for (int k = 0; k < kSide; ++k) CK(cudaStreamCreateWithFlags(&x[k], cudaStreamNonBlocking));
+  return x;
+}
+
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 // Host wall-clock trace of the phases (MRRR_TRACE=1), for overhead hunting.
 struct Trace {
   bool on;
@@ -240,11 +256,33 @@ void d2h(T *dst, const T *src, size_t count, cudaStream_t s) {
   CK(cudaStreamSynchronize(s));
 }
 
+// Per-thread event pools, reset at the start of every call (the previous
+// call synchronised all its work): no event is created or destroyed per call
+// in steady state (driver object churn next to an nvidia-smi sampler cost
+// milliseconds per call).
+struct EvPool {
+  unsigned flags;
+  std::vector<cudaEvent_t> ev;
+  size_t i = 0;
+  cudaEvent_t get() {
+    if (i == ev.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, flags));
+      ev.push_back(e);
+    }
+    return ev[i++];
+  }
+};
+thread_local EvPool g_ev_sync{cudaEventDisableTiming}, g_ev_time{cudaEventDefault};
+cudaEvent_t ev_sync() { return g_ev_sync.get(); }
+cudaEvent_t ev_time() { return g_ev_time.get(); }
+void ev_reset() { g_ev_sync.i = 0; g_ev_time.i = 0; }
+
 struct Timer {
   cudaEvent_t a, b;
   cudaStream_t s;
   explicit Timer(cudaStream_t st) : s(st) {
-    cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, s);
+    a = ev_time(); b = ev_time(); cudaEventRecord(a, s);
   }
   double stop() {
     cudaEventRecord(b, s); cudaEventSynchronize(b);
@@ -252,7 +290,6 @@ struct Timer {
     cudaEventRecord(a, s);
     return ms;
   }
-  ~Timer() { cudaEventDestroy(a); cudaEventDestroy(b); }
 };
 
 // Event pair around one group of launches on the call's stream; read at the
@@ -260,7 +297,7 @@ struct Timer {
 struct KTimer {
   cudaEvent_t a = nullptr, b = nullptr;
   bool used = false;
-  KTimer() { cudaEventCreate(&a); cudaEventCreate(&b); }
+  KTimer() { a = ev_time(); b = ev_time(); }
   void start(cudaStream_t s) { cudaEventRecord(a, s); used = true; }
   void stop(cudaStream_t s) { cudaEventRecord(b, s); }
   double ms() {
@@ -269,7 +306,6 @@ struct KTimer {
     float v = 0; cudaEventElapsedTime(&v, a, b);
     return v;
   }
-  ~KTimer() { cudaEventDestroy(a); cudaEventDestroy(b); }
 };
 
 // Launch helpers -----------------------------------------------------------
@@ -552,6 +588,7 @@ int solve(Problem &P, int64_t *m_out) {
   DevArena ar(device_ws(g_ws_call));
   Trace tr;
   g_staging.reset();
+  ev_reset();
   Timer tm(s), tall(s);
   KTimer kt_root, kt_vec, kt_fin;
   memset(&g_stats, 0, sizeof(g_stats));
@@ -772,8 +809,9 @@ int solve(Problem &P, int64_t *m_out) {
   // near-bisection work per bit), a small one spread thin (up to 64 shifts
   // each, fewer rounds).  Depends on m alone, so every rank that holds a
   // shared cluster forms the same work items (§8(e)).
-  static const int rw_env = getenv("MRRR_RW_CHUNK") ? atoi(getenv("MRRR_RW_CHUNK")) : 0;
-  static const int rw_m_env = getenv("MRRR_RW_M") ? atoi(getenv("MRRR_RW_M")) : 0;
+  // diagnostics (read per call): MRRR_RW_CHUNK / MRRR_RW_M override the refinement work items
+  const int rw_env = env_int("MRRR_RW_CHUNK", 0);
+  const int rw_m_env = env_int("MRRR_RW_M", 0);
   auto rw_chunk = [&](int m) {
     if (rw_env > 0) return std::min(rw_env, kRWMembers);
     return m >= 512 ? 32 : m >= 128 ? 16 : 8;
@@ -946,27 +984,24 @@ int solve(Problem &P, int64_t *m_out) {
   int *fail_list = ar.alloc<int>(std::max<int64_t>(nslots, 1)), *fail_count = ar.alloc<int>(1);
   CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
   // MRRR_VEC_MODE=1 (diagnostic): all vectors in one batch after the tree
-  static const int vec_mode = getenv("MRRR_VEC_MODE") ? atoi(getenv("MRRR_VEC_MODE")) : 0;
+  const int vec_mode = env_int("MRRR_VEC_MODE", 0);
   // batches go round-robin to kSide side streams so that they overlap one
   // another as well as the tree (one side stream ran them back to back: the
   // batches are latency-bound, ~12 ms each at n = 20000, and their chain
   // outlasted the tree by ~50 ms)
-  constexpr int kSide = 4;
+  // The side streams are created once per host thread and device (creating
+  // streams every call cost 10-40 ms per call next to an nvidia-smi sampler);
+  // the guard joins them into the call's stream on every exit path.
   struct SideStreams {
-    cudaStream_t main, st[kSide] = {};
+    cudaStream_t main, *st;
     ~SideStreams() {
-      for (auto &x : st)
-        if (x) {
-          cudaEvent_t e;
-          cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-          cudaEventRecord(e, x);
-          cudaStreamWaitEvent(main, e, 0);
-          cudaEventDestroy(e);
-          cudaStreamDestroy(x);
-        }
+      for (int k = 0; k < kSide; ++k) {
+        cudaEvent_t e = ev_sync();
+        cudaEventRecord(e, st[k]);
+        cudaStreamWaitEvent(main, e, 0);
+      }
     }
-  } side{s};
-  for (auto &x : side.st) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  } side{s, side_streams()};
   int nbatch = 0;
   // checkpoint columns: one buffer of ck_cap tasks per side stream, reused by
   // the stream's next batch (stream order); a level's singletons go out in
@@ -993,21 +1028,18 @@ int solve(Problem &P, int64_t *m_out) {
       WarpItem *ditems = ar.alloc<WarpItem>(items.size());
       h2d(dtb, bt.data(), nbt, s);
       h2d(ditems, items.data(), items.size(), s);
-      cudaEvent_t ready;
-      CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      cudaEvent_t ready = ev_sync();
       CK(cudaEventRecord(ready, s));
       cudaStream_t s2 = side.st[sk];
       ++nbatch;
       CK(cudaStreamWaitEvent(s2, ready, 0));
-      cudaEventDestroy(ready);
       WVecArgs A{};
       A.nodes = dnodes; A.LDv = LDv; A.tasks = dtb; A.items = ditems; A.nitems = (int)items.size();
       A.lo = slo; A.hi = shi; A.fck = ck_f[sk]; A.bck = ck_b[sk]; A.ck_stride = ck_cap; A.ntask = nbt;
       A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam + t0; A.mode = 0; A.ctr = ctr + 8;
       A.slot_j = slot_j; A.rqc_max = std::max(1, P.o.rqc_max);
       A.fail_list = fail_list; A.fail_count = fail_count; A.task_base = (int)t0;
-      cudaEvent_t ea, eb;
-      CK(cudaEventCreate(&ea)); CK(cudaEventCreate(&eb));
+      cudaEvent_t ea = ev_time(), eb = ev_time();
       CK(cudaEventRecord(ea, s2));
       launch_wvec(A, s2);
       CK(cudaEventRecord(eb, s2));
@@ -1072,8 +1104,8 @@ int solve(Problem &P, int64_t *m_out) {
     // the step's scratch (kCSRows rows of nbmax doubles per cluster) is capped
     // at 16 GB: beyond, clusters go through in groups that reuse it (stream
     // order; each group costs one more chain latency)
-    const int cgrp =
-        (int)std::max<int64_t>(1, std::min<int64_t>(ncl, (int64_t)(16e9 / (8.0 * kCSRows * nbmax))));
+    int cgrp = (int)std::max<int64_t>(1, std::min<int64_t>(ncl, (int64_t)(16e9 / (8.0 * kCSRows * nbmax))));
+    if (env_int("MRRR_CS_GROUP", 0) > 0) cgrp = std::min(cgrp, env_int("MRRR_CS_GROUP", 0));  // test hook
     double *scratch = (double *)grow_buffer(child_scratch(), (size_t)kCSRows * cgrp * nbmax * sizeof(double));
     double *dsig = lv.alloc<double>(ncl);
     int *dtier = lv.alloc<int>(ncl);
@@ -1160,12 +1192,11 @@ int solve(Problem &P, int64_t *m_out) {
   g_stats.singletons = ntask;
   {
     // join the side streams
-    for (auto x : side.st) {
-      cudaEvent_t j;
-      CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+    for (int k = 0; k < kSide; ++k) {
+      cudaStream_t x = side.st[k];
+      cudaEvent_t j = ev_sync();
       CK(cudaEventRecord(j, x));
       CK(cudaStreamWaitEvent(s, j, 0));
-      cudaEventDestroy(j);
     }
   }
   if (ntask > 0) {
@@ -1266,7 +1297,6 @@ int solve(Problem &P, int64_t *m_out) {
       cudaEventSynchronize(e.second);
       cudaEventElapsedTime(&v, e.first, e.second);
       ms += v;
-      cudaEventDestroy(e.first); cudaEventDestroy(e.second);
     }
     g_stats.ms_k_vectors = ms;
   }

@@ -8,8 +8,8 @@ element, plus the BASELINE.json accuracy contract:
   sign-free vectors of well-separated eigenvalues (Davis-Kahan rule,
   DESIGN.md reading 18) agree to 1e-9.
 
-Small cases span several smem tiles (256 rows), checkpoint segments (32
-rows) and ragged tails; the BASELINE configs run at full size in the launch
+Small cases span many 16-row shared-memory tiles (= checkpoint segments),
+ragged tails and several tree levels; the BASELINE configs run at full size in the launch
 configuration bench.py times, compared on oracle-computable samples (index
 windows solved by the oracle) plus properties that hold at any size.
 """
@@ -168,6 +168,24 @@ def test_deterministic(torch_cuda, P):
     w1, Z1 = gpu_solve(P, torch_cuda, d, e)
     w2, Z2 = gpu_solve(P, torch_cuda, d, e)
     assert np.array_equal(w1, w2) and np.array_equal(Z1, Z2)
+
+
+@pytest.mark.parametrize("env", [{"MRRR_CS_GROUP": "3"}, {"MRRR_VEC_MODE": "1"}])
+def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
+    """The launch schedule does not change a single bit: cluster steps in
+    groups that reuse the scratch (MRRR_CS_GROUP, the n = 1e5 memory cap's
+    path) and all vectors in one batch after the tree (MRRR_VEC_MODE=1)
+    against per-level vector pieces on four side streams (default).  Each
+    cluster's step and each eigenpair's RQC depend on their own data only."""
+    for d, e in (W.glued_wilkinson(40), W.random_uniform(3000, 2)):
+        w1, Z1 = gpu_solve(P, torch_cuda, d, e)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        w2, Z2 = gpu_solve(P, torch_cuda, d, e)
+        for k in env:
+            monkeypatch.delenv(k)
+        assert P.last_stats()["levels"] >= 2
+        assert np.array_equal(w1, w2) and np.array_equal(Z1, Z2)
 
 
 def test_host_entry_matches_device(torch_cuda, P):

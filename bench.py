@@ -284,7 +284,12 @@ def main():
     roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
             "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
             "kernel_ms": kms, "kernel_share_of_step": kms / (tot_ms / args.steps),
-            "algorithmic_slots_per_launch": slots, "w_div": W_DIV,
+            "algorithmic_slots_per_step": slots, "w_div": W_DIV,
+            "note": "k_wvectors runs as per-level pieces on four side streams that overlap each other "
+                    "and the tree; achieved = sum of its slots / sum of its launch durations (CUDA "
+                    "events on each launch's stream), i.e. the work-weighted per-launch rate; a piece "
+                    "holds few warps and is latency-bound, so this sits far below the step fraction, "
+                    "and kernel_share_of_step (sum of launch durations / step) can exceed 1",
             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 1.965 GHz = 1.861e13 slots/s, x2 flop "
                            "(guide unit counts; microbenchmark 1.708e13 DFMA/s)",
             "root_bisect": {"ms": kb, "achieved_tflops": 2 * slots_bis / (kb / 1e3) / 1e12 if kb else None},

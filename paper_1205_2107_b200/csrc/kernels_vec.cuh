@@ -35,7 +35,7 @@ struct VecTask {
 };
 
 struct FwdCk { double p, q, H; int neg; int pad; };
-struct BwdCk { double a, b; };
+struct BwdCk { double a, b, K; int neg; int pad; };
 
 struct VecCtx {
   const double2 *DL;   // node (D, LLD)

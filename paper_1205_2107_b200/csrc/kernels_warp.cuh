@@ -1,18 +1,18 @@
-// kernels_warp.cuh -- a6: twisted factorizations and
-// eigenvector solves in WARP LOCKSTEP.  One warp owns up to 32 eigenpairs of
-// ONE node (one lane each).  All lanes walk the node's rows in the same
-// order, so the rows are staged once per warp through a shared-memory ring of
-// 32-row tiles filled by cp.async (LDGSTS) kRing-1 tiles ahead, and read back
-// as broadcasts.  Measured on B200 (tools/ubench_chain.cu): a dependent
-// projective sweep costs 37 cycles/row from such tiles against 72-80 from
-// global memory with register prefetch, and 26.5 with rows in registers.
+// kernels_warp.cuh -- a6: twisted factorizations and eigenvector solves in
+// WARP LOCKSTEP.  A work item is up to 32 eigenpairs of ONE node (one lane
+// each); all lanes walk the node's rows in the same order, so the rows are
+// staged once per warp through a shared-memory ring of 16-row tiles filled
+// by cp.async (LDGSTS) kRing-1 tiles ahead, and read back as broadcasts.
+// Measured on B200 (tools/ubench_chain.cu): a dependent projective sweep
+// costs 37 cycles/row from such tiles against 72-80 from global memory with
+// register prefetch, and 26.5 with rows in registers.
 //
 // Arithmetic is that of kernels_vec.cuh: projective
 // stationary/progressive transforms, twist by cross-multiplied |gamma|,
-// running partial norms H/K, checkpoints every kTR rows with replay of the
-// forward segment during the backward sweep.  The eigenvector z of each lane
-// is formed per segment in shared memory and written to its column with
-// 256-byte coalesced stores (lane j's chunk by the whole warp).
+// running partial norms H/K, checkpoints every kTR rows with replay.  Each
+// item runs on a PAIR of warps (stationary sweeps on one, progressive on the
+// other, concurrently; see below).  The eigenvector z of each lane is formed
+// per segment in shared memory and written to its column with 16-byte stores.
 #pragma once
 #include <cuda_pipeline.h>
 
@@ -22,7 +22,6 @@ namespace mrrr {
 
 constexpr int kTR = 16;          // rows per tile (= checkpoint segment)
 constexpr int kRing = 6;         // tiles in flight per warp
-constexpr int kWarpsPerCta = 2;  // independent warps per CTA
 static_assert(kTR == kSeg, "tiles and checkpoint segments coincide");
 
 // Shared memory of one warp.
@@ -101,6 +100,279 @@ __device__ __forceinline__ int warp_min(int v) {
   for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
+
+// ---------------------------------------------------------------------------
+// PAIR execution.  A CTA holds one work item (up to 32 eigenpairs of one node)
+// and two warps: warp F (role 0) runs every stationary (top-down) sweep and
+// warp B (role 1) every progressive (bottom-up) one, at the same time.  The
+// two halves of a twisted factorization are independent until the twist, so
+// each factorization costs one sweep of latency instead of two: the full
+// factorization (both sweeps, then the twist search split between the warps
+// over the segments, each replaying both states from the checkpoints), every
+// fixed-twist RQC factorization (rows < r on F, rows > r on B) and the z
+// solve (left part on F, right part on B).  The warps meet at CTA barriers
+// to exchange the twist quantities; both then run the same RQC control
+// (identical inputs, identical decisions); only F writes the side effects.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void put_bck(const WarpCtx &W, int c, const Bwd &B) {
+  BwdCk bk; bk.a = B.a; bk.b = B.b; bk.K = B.K; bk.neg = B.neg; bk.pad = 0;
+  W.bck[(int64_t)c * W.ck_stride + W.tix] = bk;
+}
+
+// Best twist of a range of rows: |gamma| = |N| / |q b| compared by
+// cross-multiplication; among equal values the lowest row (the full search
+// scans downward and keeps a later row on ties).
+struct TwistPart {
+  double N, den, H, q, K, b;
+  int r, neg, have;
+};
+
+// Per-CTA exchange between the two warps (per lane).
+struct PairX {
+  double fp[32], fq[32], fH[32];
+  double ba[32], bb[32], bK[32];
+  int fneg[32], bneg[32], ok[2][32];
+  double eN[2][32], eden[2][32], eH[2][32], eq[2][32], eK[2][32], eb[2][32];
+  int er[2][32], eneg[2][32], ehave[2][32];
+};
+
+// Twist search over segments c = chi .. clo (descending), replaying the
+// forward state of each segment from its checkpoint into shared memory and
+// the backward state from its checkpoint (both sweeps of the same
+// factorization wrote them).
+__device__ __forceinline__ TwistPart w_eval_segments(const WarpCtx &W, double lam, int chi, int clo) {
+  const int nb = W.nb, L = W.lane;
+  WarpSmem &S = *W.sm;
+  TwistPart T;
+  T.N = 0; T.den = 0; T.H = 0; T.q = 1; T.K = 0; T.b = 1; T.r = nb - 1; T.neg = 0; T.have = 0;
+  if (chi < clo) return T;
+  FwdCk ckn = W.fck[(int64_t)chi * W.ck_stride + W.tix];
+  BwdCk bkn = W.bck[(int64_t)chi * W.ck_stride + W.tix];
+  bool have = false;
+  w_tiles_down(W, chi, clo, [&](int c, int slot) {
+    const int r0 = c * kTR, r1 = min(r0 + kTR, nb);
+    const FwdCk ck = ckn;
+    const BwdCk bk = bkn;
+    if (c > clo) {
+      ckn = W.fck[(int64_t)(c - 1) * W.ck_stride + W.tix];
+      bkn = W.bck[(int64_t)(c - 1) * W.ck_stride + W.tix];
+    }
+    Fwd G{ck.p, ck.q, ck.H, 0};
+    Bwd B{bk.a, bk.b, bk.K, bk.neg};
+    unsigned mask = 0;
+    auto eval = [&](int k) {
+      const double fpi = S.sA[k][L], fqi = S.sB[k][L], fHi = S.sC[k][L];
+      const double qb = fqi * B.b;
+      const double N = fma(fpi, B.b, fma(B.a, fqi, lam * qb));
+      const bool better = (!have || (fabs(N) * fabs(T.den) <= fabs(T.N) * fabs(qb))) && qb != 0.0 &&
+                          isfinite(N);
+      const int negk = ck.neg + __popc(mask & ((1u << k) - 1u)) + B.neg;
+      have |= better;
+      T.r = better ? r0 + k : T.r;
+      T.N = better ? N : T.N;
+      T.den = better ? qb : T.den;
+      T.H = better ? fHi : T.H;
+      T.q = better ? fqi : T.q;
+      T.K = better ? B.K : T.K;
+      T.b = better ? B.b : T.b;
+      T.neg = better ? negk : T.neg;
+    };
+    if (r1 < nb) {  // full segment, rows r0 .. r0+15 all below nb-1
+#pragma unroll 8
+      for (int k = 0; k < kTR; ++k) {
+        S.sA[k][L] = G.p; S.sB[k][L] = G.q; S.sC[k][L] = G.H;
+        const int before = G.neg;
+        G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+        mask |= (unsigned)(G.neg - before) << k;
+      }
+#pragma unroll 8
+      for (int k = kTR - 1; k >= 0; --k) {
+        B.step_r(w_row(W, slot, k), lam, (k & 7) == 0);
+        eval(k);
+      }
+    } else {  // the top segment: rows r0 .. nb-1
+      const int nr = r1 - r0;
+      for (int k = 0; k < nr; ++k) {
+        S.sA[k][L] = G.p; S.sB[k][L] = G.q; S.sC[k][L] = G.H;
+        if (k < nr - 1) {
+          const int before = G.neg;
+          G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+          mask |= (unsigned)(G.neg - before) << k;
+        }
+      }
+      eval(nr - 1);
+      for (int k = nr - 2; k >= 0; --k) {
+        B.step_r(w_row(W, slot, k), lam, (k & 7) == 0);
+        eval(k);
+      }
+    }
+    return false;
+  });
+  T.have = have;
+  return T;
+}
+
+// Full twisted factorization of every lane at its own lambda (inactive lanes
+// compute too, on a harmless shift; their results are ignored).  Called by
+// both warps of the pair.
+__device__ __forceinline__ Twist w_full_pair(const WarpCtx &W, double lam, int role, PairX &X) {
+  const int nb = W.nb, L = W.lane;
+  bool ok;
+  if (role == 0) {  // stationary sweep, checkpoints of every segment
+    Fwd F{-lam, 1.0, 0.0, 0};
+    w_tiles_up(W, 0, W.nseg - 1, [&](int c, int slot) {
+      put_fck(VecCtx{nullptr, nullptr, nb, W.nseg, W.fck, W.bck, W.ck_stride}, c, W.tix, F);
+      const int r0 = c * kTR;
+      const int rows = min(kTR, nb - 1 - r0);  // rows carrying LLD
+      if (rows == kTR) {
+#pragma unroll
+        for (int k = 0; k < kTR; ++k) F.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+      } else {
+        for (int k = 0; k < rows; ++k) F.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+      }
+      return false;
+    });
+    ok = isfinite(F.p) && isfinite(F.q);
+  } else {  // progressive sweep, checkpoint = state at row min(r0 + kTR, nb - 1)
+    Bwd B{__ldg(&W.DL[nb - 1]).x - lam, 1.0, 0.0, 0};
+    w_tiles_down(W, W.nseg - 1, 0, [&](int c, int slot) {
+      put_bck(W, c, B);
+      const int r0 = c * kTR, r1 = min(r0 + kTR, nb);
+      if (r1 < nb) {
+#pragma unroll
+        for (int k = kTR - 1; k >= 0; --k) B.step_r(w_row(W, slot, k), lam, (k & 7) == 0);
+      } else {
+        for (int k = r1 - r0 - 2; k >= 0; --k) B.step_r(w_row(W, slot, k), lam, (k & 7) == 0);
+      }
+      return false;
+    });
+    ok = isfinite(B.a) && isfinite(B.b);
+  }
+  __syncthreads();  // both sweeps' checkpoints are written (global memory, CTA scope)
+  // twist search: F takes the lower half of the segments, B the upper half
+  const int h = W.nseg / 2;
+  const TwistPart T = role == 0 ? w_eval_segments(W, lam, h - 1, 0) : w_eval_segments(W, lam, W.nseg - 1, h);
+  X.eN[role][L] = T.N; X.eden[role][L] = T.den; X.eH[role][L] = T.H; X.eq[role][L] = T.q;
+  X.eK[role][L] = T.K; X.eb[role][L] = T.b; X.er[role][L] = T.r; X.eneg[role][L] = T.neg;
+  X.ehave[role][L] = T.have; X.ok[role][L] = ok;
+  __syncthreads();
+  // combine: the lower half wins ties (it comes later in the downward scan)
+  const bool h0 = X.ehave[0][L], h1 = X.ehave[1][L];
+  const bool low = h0 && (!h1 || fabs(X.eN[0][L]) * fabs(X.eden[1][L]) <= fabs(X.eN[1][L]) * fabs(X.eden[0][L]));
+  const int s = low ? 0 : 1;
+  const double bN = X.eN[s][L], bden = X.eden[s][L], bH = X.eH[s][L], bq = X.eq[s][L];
+  const double bK = X.eK[s][L], bb = X.eb[s][L];
+  Twist tw;
+  tw.r = X.er[s][L];
+  tw.gamma = bN / bden;
+  tw.nrm2 = 1.0 + bH / (bq * bq) + bK / (bb * bb);
+  tw.negc = X.eneg[s][L] + ((tw.gamma < 0.0) ? 1 : 0);
+  tw.ok = X.ok[0][L] && X.ok[1][L] && (h0 || h1) && isfinite(tw.gamma) && isfinite(tw.nrm2);
+  __syncthreads();  // X is reused by the next exchange
+  return tw;
+}
+
+// Fixed-twist factorization of every lane at its own (lambda, r): F steps
+// rows 0..r-1 (ascending tiles up to the warp's largest r), B rows nb-2..r
+// (descending tiles down to the smallest r), each lane only its own rows.
+// Checkpoints: F of the segments below r, B of the segments from r / kTR
+// (the solve replays them).  Called by both warps of the pair.
+__device__ __forceinline__ Twist w_fixed_pair(const WarpCtx &W, double lam, int r, bool active, int role,
+                                              PairX &X) {
+  const int nb = W.nb, L = W.lane;
+  if (role == 0) {
+    Fwd F{-lam, 1.0, 0.0, 0};
+    const int rf = active ? r : 0;  // an idle lane steps no rows
+    const VecCtx Xc{nullptr, nullptr, nb, W.nseg, W.fck, W.bck, W.ck_stride};
+    const int cf = warp_max(rf > 0 ? (rf - 1) / kTR : -1);
+    w_tiles_up(W, 0, cf, [&](int c, int slot) {
+      const int r0 = c * kTR;
+      if (r0 < rf) put_fck(Xc, c, W.tix, F);
+#pragma unroll
+      for (int k = 0; k < kTR; ++k) {
+        const Row R = w_row(W, slot, k);
+        if (r0 + k < rf) {
+          const double t = fma(R.D, F.q, F.p);
+          F.neg += negbit(t, F.q);
+          F.H = R.LD2 * fma(F.q, F.q, F.H);
+          F.p = fma(-lam, t, R.LLD * F.p);
+          F.q = t;
+          if ((k & 7) == 7) fwd_rescale(F.p, F.q, F.H);
+        }
+      }
+      return false;
+    });
+    X.fp[L] = F.p; X.fq[L] = F.q; X.fH[L] = F.H; X.fneg[L] = F.neg;
+  } else {
+    Bwd B{__ldg(&W.DL[nb - 1]).x - lam, 1.0, 0.0, 0};
+    const int rb = active ? r : nb - 1;  // backward steps into rows [rb, nb - 1)
+    const int cb = warp_min(rb / kTR);
+    w_tiles_down(W, W.nseg - 1, cb, [&](int c, int slot) {
+      const int r0 = c * kTR;
+      const int top = min(r0 + kTR, nb) - 1;  // rows r0 .. top in this tile
+      if (c >= rb / kTR) put_bck(W, c, B);    // state at row min(r0 + kTR, nb - 1)
+      auto bstep = [&](int k) {
+        const Row R = w_row(W, slot, k);
+        const double u = fma(R.LLD, B.b, B.a);
+        B.neg += negbit(u, B.b);
+        B.K = R.LD2 * fma(B.b, B.b, B.K);
+        B.a = fma(-lam, u, R.D * B.a);
+        B.b = u;
+        if ((k & 7) == 0) bwd_rescale(B.a, B.b, B.K);
+      };
+      if (top - r0 + 1 == kTR && top < nb - 1) {
+#pragma unroll
+        for (int k = kTR - 1; k >= 0; --k)
+          if (r0 + k >= rb) bstep(k);
+      } else {
+        for (int k = top - r0; k >= 0; --k) {
+          const int i = r0 + k;
+          if (i < nb - 1 && i >= rb) bstep(k);
+        }
+      }
+      return false;
+    });
+    X.ba[L] = B.a; X.bb[L] = B.b; X.bK[L] = B.K; X.bneg[L] = B.neg;
+  }
+  __syncthreads();
+  const double Fp = X.fp[L], Fq = X.fq[L], FH = X.fH[L];
+  const double Ba = X.ba[L], Bb = X.bb[L], BK = X.bK[L];
+  const double qb = Fq * Bb;
+  const double N = fma(Fp, Bb, fma(Ba, Fq, lam * qb));
+  Twist tw;
+  tw.r = r;
+  tw.gamma = N / qb;
+  tw.nrm2 = 1.0 + FH / (Fq * Fq) + BK / (Bb * Bb);
+  tw.negc = X.fneg[L] + X.bneg[L] + ((tw.gamma < 0.0) ? 1 : 0);
+  tw.ok = isfinite(tw.gamma) && isfinite(tw.nrm2) && qb != 0.0;
+  __syncthreads();
+  return tw;
+}
+
+// Each lane writes its chunk rows [a, b] (values sA[0 .. b-a][lane]) to its
+// own column: 16-byte stores when the chunk start is 16-byte aligned.
+__device__ __forceinline__ void w_flush(const WarpCtx &W, int a, int b, double *col) {
+  const int L = W.lane;
+  if (b < a) return;
+  double *dst = col + a;
+  const int cnt = b - a + 1;
+  if ((((uintptr_t)dst) & 15) == 0) {
+    int k = 0;
+    for (; k + 1 < cnt; k += 2) {
+      double2 v = make_double2(W.sm->sA[k][L], W.sm->sA[k + 1][L]);
+      __stcg(reinterpret_cast<double2 *>(dst + k), v);
+    }
+    if (k < cnt) __stcg(dst + k, W.sm->sA[k][L]);
+  } else {
+    for (int k = 0; k < cnt; ++k) __stcg(dst + k, W.sm->sA[k][L]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SINGLE-warp execution (one warp per item, both sweeps in sequence): fewer
+// resources per item, used for the pieces that overlap the tree levels.
+// ---------------------------------------------------------------------------
 
 // Full twisted factorization of every lane at its own lambda (inactive lanes
 // compute too, on a harmless shift; their results are ignored).
@@ -280,25 +552,6 @@ __device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int
   return tw;
 }
 
-// Each lane writes its chunk rows [a, b] (values sA[0 .. b-a][lane]) to its
-// own column: 16-byte stores when the chunk start is 16-byte aligned.
-__device__ __forceinline__ void w_flush(const WarpCtx &W, int a, int b, double *col) {
-  const int L = W.lane;
-  if (b < a) return;
-  double *dst = col + a;
-  const int cnt = b - a + 1;
-  if ((((uintptr_t)dst) & 15) == 0) {
-    int k = 0;
-    for (; k + 1 < cnt; k += 2) {
-      double2 v = make_double2(W.sm->sA[k][L], W.sm->sA[k + 1][L]);
-      __stcg(reinterpret_cast<double2 *>(dst + k), v);
-    }
-    if (k < cnt) __stcg(dst + k, W.sm->sA[k][L]);
-  } else {
-    for (int k = 0; k < cnt; ++k) __stcg(dst + k, W.sm->sA[k][L]);
-  }
-}
-
 // z pass of every active lane: z_r = 1, written as scale * z to col[0 .. nb).
 // The ratios q_i / t_i (left) and b_{i+1} / u_{i+1} (right) are formed during
 // the replay with correctly rounded reciprocals (off the z recurrence), so
@@ -405,7 +658,117 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
   });
 }
 
-// One warp item: up to 32 tasks of one node.
+// z of every active lane, z_r = 1, written as scale * z to col[0 .. nb): F
+// the rows below r (and r itself), B the rows above.  The ratios q_i / t_i
+// (left) and b_{i+1} / u_{i+1} (right) are formed during the replay with
+// correctly rounded reciprocals (off the z recurrence), so the z loops are
+// pure multiply chains.
+__device__ __forceinline__ void w_solve_pair(const WarpCtx &W, double lam, int r, double scale, double *col,
+                                             bool active, int role) {
+  const int nb = W.nb, L = W.lane;
+  WarpSmem &S = *W.sm;
+  if (role == 0) {
+    if (active) col[r] = scale;
+    // ---- left part, rows i < r, descending: z_i = -LD_i (q_i / t_i) z_{i+1}
+    const int clast = (active && r > 0) ? (r - 1) / kTR : -1;
+    const int cmax = warp_max(clast);
+    double z1 = 1.0, z2 = 0.0, ldn = (active && r > 0) ? __ldg(&W.LDv[r]).x : 0.0;
+    FwdCk ckn = W.fck[(int64_t)max(min(clast, cmax), 0) * W.ck_stride + W.tix];
+    w_tiles_down(W, cmax, 0, [&](int c, int slot) {
+      const bool on = c <= clast;
+      const int r0 = c * kTR, r1 = on ? min(r0 + kTR, r) : r0;  // rows [r0, r1)
+      const FwdCk ck = ckn;
+      if (on && c > 0) ckn = W.fck[(int64_t)(c - 1) * W.ck_stride + W.tix];
+      Fwd G{ck.p, ck.q, 0.0, 0};
+      auto rep = [&](int k) {
+        const Row R = w_row(W, slot, k);
+        const double t = fma(R.D, G.q, G.p);
+        S.sA[k][L] = -R.LD * (G.q * rcp_nr(t));  // z_i / z_{i+1}
+        S.sC[k][L] = R.LD;
+        G.p = fma(-lam, t, R.LLD * G.p);
+        G.q = t;
+        if ((k & 7) == 7) fwd_rescale(G.p, G.q, G.H);
+      };
+      if (on && r1 == r0 + kTR) {
+#pragma unroll
+        for (int k = 0; k < kTR; ++k) rep(k);
+      } else if (on) {
+        for (int k = 0; k < r1 - r0; ++k) rep(k);
+      }
+      // branch-free: the zero-component rule (row i+1 of (LDL^T - lambda I) z
+      // = 0 gives z_i = -(LD_{i+1} / LD_i) z_{i+2}) is evaluated every row and
+      // selected, so no division slow path splits the unrolled block
+      auto zstep = [&](int k) {
+        const double ld = S.sC[k][L];
+        const double za = S.sA[k][L] * z1;
+        const double zb = -(ldn * rcp_nr(ld)) * z2;
+        double zi = (z1 != 0.0) ? za : zb;
+        zi = (fabs(zi) >= kTiny) ? zi : 0.0;
+        S.sA[k][L] = zi * scale;
+        z2 = z1; z1 = zi; ldn = ld;
+      };
+      if (r1 - r0 == kTR) {
+#pragma unroll
+        for (int k = kTR - 1; k >= 0; --k) zstep(k);
+      } else {
+        for (int k = r1 - r0 - 1; k >= 0; --k) zstep(k);
+      }
+      w_flush(W, r0, r1 - 1, col);  // chunk rows r0 .. r1-1 from sA[0 ..]
+      return false;
+    });
+  } else {
+    // ---- right part, rows i > r, ascending: z_{i+1} = -LD_i (b_{i+1} / u_{i+1}) z_i
+    const int cfirst = (active && r < nb - 1) ? r / kTR : W.nseg;
+    const int cmin = warp_min(cfirst);
+    double y1 = 1.0, y2 = 0.0, ldp = (active && r > 0) ? __ldg(&W.LDv[r - 1]).x : 0.0;
+    BwdCk bkn = W.bck[(int64_t)min(max(cfirst, cmin), W.nseg - 1) * W.ck_stride + W.tix];
+    w_tiles_up(W, cmin, W.nseg - 1, [&](int c, int slot) {
+      const bool on = c >= cfirst;
+      const int r0 = c * kTR;
+      const int top = min(r0 + kTR, nb - 1);  // checkpoint row
+      const int lo_i = on ? max(r0, r) : top;  // rows i in [lo_i, top) give U-_i
+      const BwdCk bk = bkn;
+      if (on && c + 1 < W.nseg) bkn = W.bck[(int64_t)(c + 1) * W.ck_stride + W.tix];
+      Bwd G{bk.a, bk.b, 0.0, 0};
+      auto rep = [&](int k) {
+        const Row R = w_row(W, slot, k);
+        const double u = fma(R.LLD, G.b, G.a);
+        S.sA[k][L] = -R.LD * (G.b * rcp_nr(u));  // z_{i+1} / z_i
+        S.sC[k][L] = R.LD;
+        G.a = fma(-lam, u, R.D * G.a);
+        G.b = u;
+        if ((k & 7) == 0) bwd_rescale(G.a, G.b, G.K);
+      };
+      if (on && lo_i == r0 && top == r0 + kTR) {
+#pragma unroll
+        for (int k = kTR - 1; k >= 0; --k) rep(k);
+      } else if (on) {
+        for (int k = top - 1 - r0; k >= lo_i - r0; --k) rep(k);
+      }
+      // z_{i+1} for i in [lo_i, top): chunk rows lo_i+1 .. top, stored at sA[i - lo_i]
+      // (ascending i: index i - lo_i <= i - r0 was already read)
+      auto ystep = [&](int k, int o) {
+        const double ld = S.sC[k][L];
+        const double za = S.sA[k][L] * y1;
+        const double zb = -(ldp * rcp_nr(ld)) * y2;  // row i of (LDL^T - lambda I) z = 0
+        double zn = (y1 != 0.0) ? za : zb;
+        zn = (fabs(zn) >= kTiny) ? zn : 0.0;
+        S.sA[o][L] = zn * scale;
+        y2 = y1; y1 = zn; ldp = ld;
+      };
+      if (lo_i == r0 && top == r0 + kTR) {
+#pragma unroll
+        for (int k = 0; k < kTR; ++k) ystep(k, k);
+      } else {
+        for (int i = lo_i; i < top; ++i) ystep(i - r0, i - lo_i);
+      }
+      w_flush(W, lo_i + 1, top, col);
+      return false;
+    });
+  }
+}
+
+// One work item: up to 32 tasks of one node.
 struct WarpItem {
   int32_t node;
   int32_t t0, t1;  // task ids [t0, t1) (tasks of one node are consecutive)
@@ -423,23 +786,153 @@ struct WVecArgs {
   const int *slot_j;         // block-local 1-based eigen index per slot
   FwdCk *fck;
   BwdCk *bck;
-  int64_t ck_stride;         // = number of tasks + 32 (columns ntask + lane: idle lanes)
+  int64_t ck_stride;         // >= number of tasks + 32 (columns ntask + lane: idle lanes)
   int ntask;
   double *Z; int64_t ldz;    // modes 0, 2: Z columns (tk.col), node rows at N.row0
   double *lam_out;           // modes 0, 2: final lambda (node coordinates) per task
   int mode;                  // 0: RQC (reading 10); 2: one factorization at the bracket
                              // midpoint (RQC fallback)
-  int rqc_max;               // mode 0: factorizations before the fallback (3)
+  int rqc_max;               // mode 0: factorizations before the fallback
   int *fail_list;            // mode 0: tasks that did not converge (appended as task_base + tix)
   int *fail_count;
   int task_base;             // global index of this launch's task 0
-  unsigned long long *ctr;   // [0] factorizations, [1] fallbacks
+  unsigned long long *ctr;   // [0] factorizations, [1] fallbacks, [2..3] nudges, [4..7] slowest item
 };
 
-__device__ __forceinline__ void wvec_body(const WVecArgs &A) {
+constexpr int kPairThreads = 64;  // pair kernel: one item per CTA, warp F + warp B
+constexpr int kSingleWarps = 2;   // single-warp kernel: independent items per CTA
+
+__device__ __forceinline__ void wvec_pair_body(const WVecArgs &A) {
+  extern __shared__ __align__(16) unsigned char wsm_raw[];
+  const int role = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x;
+  if (item >= A.nitems) return;  // whole CTA
+  const WarpItem It = A.items[item];
+  const Node N = A.nodes[It.node];
+  const bool active = It.t0 + lane < It.t1;
+  const int tix = A.task_list ? A.task_list[active ? It.t0 + lane : It.t0] : (active ? It.t0 + lane : It.t0);
+  const VecTask tk = A.tasks[tix];
+  WarpCtx W;
+  W.DL = N.DL; W.LDv = A.LDv + N.row0; W.nb = N.nb; W.nseg = (N.nb + kTR - 1) / kTR;
+  W.lane = lane;
+  W.sm = reinterpret_cast<WarpSmem *>(wsm_raw) + role;
+  PairX &X = *reinterpret_cast<PairX *>(wsm_raw + 2 * sizeof(WarpSmem));
+  W.fck = A.fck; W.bck = A.bck; W.ck_stride = A.ck_stride;
+  const int64_t spare = A.ntask + lane;   // idle lanes checkpoint into spare columns
+  W.tix = active ? tix : spare;
+  const bool lead = role == 0;            // side effects by warp F only
+  double lo = A.lo[tk.slot], hi = A.hi[tk.slot];
+  if (N.nb == 1) {
+    if (active && lead) { A.Z[tk.col * A.ldz + N.row0] = 1.0; A.lam_out[tix] = __ldg(&N.DL[0]).x; }
+    return;
+  }
+  double lam = (A.mode == 2 || isnan(tk.lam0)) ? 0.5 * (lo + hi) : tk.lam0;
+  unsigned long long nfact = 0;
+  Twist tw;
+  const long long clk0 = clock64();
+  // full factorization; nudge lambda if not finite (overflow insurance, reading 25)
+  {
+    double nudge = 2.0 * kEps * fabs(lam) + kTiny;
+    const double lam_base = lam;
+    for (int tries = 0; tries < 60; ++tries) {
+      tw = w_full_pair(W, lam, role, X);
+      ++nfact;
+      if (!__any_sync(0xffffffffu, active && !tw.ok)) break;
+      if (active && !tw.ok) {
+        lam = lam_base + nudge; nudge *= 2.0;
+        if (lead) {
+          atomicAdd(&A.ctr[2], 1ull);
+          if (A.ctr[3] == 0)  // first failure: record why (debug aid, MRRR_TRACE)
+            A.ctr[3] = 1 + (isfinite(tw.gamma) ? 0 : 2) + (isfinite(tw.nrm2) ? 0 : 4);
+        }
+      }
+    }
+  }
+  double lam_fin = lam;
+  const long long clk_full = clock64();
+  if (A.mode == 0) {
+    // O10 RQC (readings 10, 24): stop when |delta| <= 4 eps |lambda| or
+    // fl(lambda + delta) == lambda; a step leaving [lo, hi] from the interior
+    // is clamped to the violated end, from an end it bisects.  A lane that
+    // has converged keeps its factorization (its checkpoint column is parked
+    // on a spare column while the other lanes iterate).
+    const int j = A.slot_j[tk.slot];
+    bool conv = !active, failed = false;
+    Twist best = tw;
+    const int best_r0 = tw.r;
+    double lam_best = lam, delta_prev = CUDART_INF;
+    for (int it = 1;; ++it) {
+      if (!conv) {
+        if (tw.negc >= j) { if (lam < hi) hi = lam; } else { if (lam > lo) lo = lam; }
+        const double delta = tw.gamma / tw.nrm2;
+        // stop (reading 10): |delta| <= 4 eps |lambda|, fl(lambda + delta) ==
+        // lambda, or stagnation (the correction no longer halves)
+        if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam ||
+            (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
+          conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
+        } else {
+          delta_prev = delta;
+          double nw = lam + delta;
+          if (nw <= lo || nw >= hi) {
+            if (lam == lo || lam == hi) {
+              nw = 0.5 * (lo + hi);
+              if (nw <= lo || nw >= hi) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }
+            } else {
+              nw = (nw <= lo) ? lo : hi;
+            }
+          }
+          lam = nw;
+        }
+        if (!conv && it >= A.rqc_max) { conv = true; failed = true; }
+        if (conv) W.tix = spare;  // park: later factorizations must not touch its checkpoints
+      }
+      if (__all_sync(0xffffffffu, conv)) break;
+      // later iterations keep the first factorization's twist index
+      tw = w_fixed_pair(W, lam, best_r0, !conv, role, X);
+      ++nfact;
+      if (!conv && !tw.ok) { conv = true; failed = true; W.tix = spare; }
+    }
+    const long long clk_rqc = clock64();
+    W.tix = active ? tix : spare;
+    tw = best;
+    lam = lam_best;
+    if (active && failed && lead) {
+      // O10 fallback, deferred: the bracket goes back to the slot; the host
+      // refines it to 4 eps and a mode-2 pass writes the vector
+      A.lo[tk.slot] = lo; A.hi[tk.slot] = hi;
+      A.fail_list[atomicAdd(A.fail_count, 1)] = A.task_base + tix;
+      atomicAdd(&A.ctr[1], 1ull);
+    }
+    // failed lanes skip the solve (their column is written by the fallback)
+    const double sc = 1.0 / sqrt(tw.nrm2);
+    w_solve_pair(W, lam, tw.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !failed, role);
+    if (lead) {
+      if (active && !failed) A.lam_out[tix] = lam_fin;
+      if (active) atomicAdd(&A.ctr[0], nfact);
+      if (lane == 0) {  // slowest item: cycles of the first factorization, the RQC loop, the solve;
+                        // factorizations of the item (MRRR_TRACE)
+        const long long clk_end = clock64();
+        atomicMax(&A.ctr[4], (unsigned long long)(clk_full - clk0));
+        atomicMax(&A.ctr[5], (unsigned long long)(clk_rqc - clk_full));
+        atomicMax(&A.ctr[6], (unsigned long long)(clk_end - clk_rqc));
+        atomicMax(&A.ctr[7], nfact);
+      }
+    }
+    return;
+  }
+  // mode 2: the vector of the one factorization at the refined midpoint
+  const double sc = 1.0 / sqrt(tw.nrm2);
+  w_solve_pair(W, lam, tw.r, sc, A.Z + tk.col * A.ldz + N.row0, active, role);
+  if (active && lead) {
+    A.lam_out[tix] = lam_fin;
+    atomicAdd(&A.ctr[0], nfact);
+  }
+}
+
+__device__ __forceinline__ void wvec_single_body(const WVecArgs &A) {
   extern __shared__ __align__(16) unsigned char wsm_raw[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item = blockIdx.x * kWarpsPerCta + wid;
+  const int item = blockIdx.x * kSingleWarps + wid;
   if (item >= A.nitems) return;  // whole warp
   const WarpItem It = A.items[item];
   const Node N = A.nodes[It.node];
@@ -558,6 +1051,7 @@ __device__ __forceinline__ void wvec_body(const WVecArgs &A) {
   }
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_wvectors(WVecArgs A) { wvec_body(A); }
+__global__ void __launch_bounds__(kPairThreads) k_wvectors_pair(WVecArgs A) { wvec_pair_body(A); }
+__global__ void __launch_bounds__(32 * kSingleWarps) k_wvectors(WVecArgs A) { wvec_single_body(A); }
 
 }  // namespace mrrr

@@ -525,16 +525,19 @@ std::vector<WarpItem> make_warp_items(const std::vector<VecTask> &t, int lanes =
   return v;
 }
 
-void launch_wvec(WVecArgs A, cudaStream_t s) {
-  const size_t smem = kWarpsPerCta * sizeof(WarpSmem);
+// pair = true: k_wvectors_pair (one item per CTA on two warps, one sweep of
+// latency per factorization); false: k_wvectors (one warp per item).
+void launch_wvec(WVecArgs A, cudaStream_t s, bool pair) {
+  const size_t smem1 = kSingleWarps * sizeof(WarpSmem), smem2 = 2 * sizeof(WarpSmem) + sizeof(PairX);
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_wvectors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_wvectors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+    CK(cudaFuncSetAttribute(k_wvectors_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     attr = true;
   }
-  const int grid = (A.nitems + kWarpsPerCta - 1) / kWarpsPerCta;
-  if (grid == 0) return;
-  k_wvectors<<<grid, 32 * kWarpsPerCta, smem, s>>>(A);
+  if (A.nitems == 0) return;
+  if (pair) k_wvectors_pair<<<A.nitems, kPairThreads, smem2, s>>>(A);
+  else k_wvectors<<<(A.nitems + kSingleWarps - 1) / kSingleWarps, 32 * kSingleWarps, smem1, s>>>(A);
   CK(cudaGetLastError());
   g_stats.kernel_launches++;
 }
@@ -582,13 +585,45 @@ struct HostNode {
   int slot0, slot1, depth;
 };
 
+// The solve runs on a library stream of the device's greatest priority,
+// ordered after the caller's stream on entry and before it on every exit:
+// when the vector pieces (side streams, default priority) and the tree's
+// kernels wait for SM resources at the same time, the block scheduler
+// serves the tree -- the critical path -- first.
+cudaStream_t hp_stream() {
+  thread_local cudaStream_t st[64] = {};
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  if (!st[d & 63]) {
+    int lo_pr = 0, hi_pr = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
+    CK(cudaStreamCreateWithPriority(&st[d & 63], cudaStreamNonBlocking, hi_pr));
+  }
+  return st[d & 63];
+}
+
 int solve(Problem &P, int64_t *m_out) {
-  cudaStream_t s = P.s;
+  ev_reset();
+  const int use_hp = env_int("MRRR_HP_STREAM", 1);
+  cudaStream_t s = use_hp ? hp_stream() : P.s;
+  struct Join {  // caller's stream waits for the solve stream on every exit
+    cudaStream_t user, inner;
+    ~Join() {
+      if (inner == user) return;
+      cudaEvent_t e = ev_sync();
+      cudaEventRecord(e, inner);
+      cudaStreamWaitEvent(user, e, 0);
+    }
+  } join{P.s, s};
+  if (s != P.s) {
+    cudaEvent_t e = ev_sync();
+    CK(cudaEventRecord(e, P.s));
+    CK(cudaStreamWaitEvent(s, e, 0));
+  }
   const int64_t n = P.n;
   DevArena ar(device_ws(g_ws_call));
   Trace tr;
   g_staging.reset();
-  ev_reset();
   Timer tm(s), tall(s);
   KTimer kt_root, kt_vec, kt_fin;
   memset(&g_stats, 0, sizeof(g_stats));
@@ -1013,7 +1048,13 @@ int solve(Problem &P, int64_t *m_out) {
   BwdCk *ck_b[kSide] = {};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vec_ev;
   size_t vec_done = 0;
-  auto flush_vectors = [&]() {
+  // pieces that overlap a busy tree level run on single warps (smaller
+  // footprint next to the tree's kernels); the last flush, and pieces whose
+  // level leaves at most kPairMaxClusters clusters to refine, on warp pairs
+  // (half the latency, resources to spare).  MRRR_VEC_PAIR: 0 never, 2 always.
+  constexpr int kPairMaxClusters = 32;
+  const int vec_pair = env_int("MRRR_VEC_PAIR", 1);
+  auto flush_vectors = [&](int tree_left) {
     for (size_t t0 = vec_done; t0 < tasks.size();) {
       const size_t t1 = std::min<size_t>(tasks.size(), t0 + (size_t)(ck_cap - 32));
       const int nbt = (int)(t1 - t0);
@@ -1041,7 +1082,7 @@ int solve(Problem &P, int64_t *m_out) {
       A.fail_list = fail_list; A.fail_count = fail_count; A.task_base = (int)t0;
       cudaEvent_t ea = ev_time(), eb = ev_time();
       CK(cudaEventRecord(ea, s2));
-      launch_wvec(A, s2);
+      launch_wvec(A, s2, vec_pair == 2 || (vec_pair == 1 && tree_left <= kPairMaxClusters));
       CK(cudaEventRecord(eb, s2));
       tr.fine(s2, "  vectors (side stream)");
       vec_ev.push_back({ea, eb});
@@ -1082,7 +1123,7 @@ int solve(Problem &P, int64_t *m_out) {
       }
     }
     const int ncl = (int)cl_parent.size();
-    if (vectors && (vec_mode == 0 || ncl == 0)) flush_vectors();
+    if (vectors && (vec_mode == 0 || ncl == 0)) flush_vectors(ncl);
     if (ncl == 0) break;
     if (level + 1 > P.o.max_depth) throw MrrrError{MRRR_ERR_DEPTH};
     g_stats.nodes += ncl;
@@ -1254,7 +1295,7 @@ int solve(Problem &P, int64_t *m_out) {
         F.fck = ar.alloc<FwdCk>((size_t)nseg_v * (h_nf + 32));
         F.bck = ar.alloc<BwdCk>((size_t)nseg_v * (h_nf + 32));
         F.Z = P.Z; F.ldz = P.ldz; F.lam_out = lam_c; F.mode = 2; F.ctr = ctr + 8;
-        launch_wvec(F, s);
+        launch_wvec(F, s, vec_pair != 0);
         k_scatter<<<(h_nf + 255) / 256, 256, 0, s>>>(dfl, lam_c, h_nf, lam);
         CK(cudaGetLastError());
         g_stats.kernel_launches++;

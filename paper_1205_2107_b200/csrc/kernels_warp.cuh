@@ -791,12 +791,15 @@ struct WVecArgs {
   double *Z; int64_t ldz;    // modes 0, 2: Z columns (tk.col), node rows at N.row0
   double *lam_out;           // modes 0, 2: final lambda (node coordinates) per task
   int mode;                  // 0: RQC (reading 10); 2: one factorization at the bracket
-                             // midpoint (RQC fallback)
+                             // midpoint (RQC fallback); 3, 4: the split RQC's phases
+                             // (k_wvectors_split)
   int rqc_max;               // mode 0: factorizations before the fallback
   int *fail_list;            // mode 0: tasks that did not converge (appended as task_base + tix)
   int *fail_count;
   int task_base;             // global index of this launch's task 0
   unsigned long long *ctr;   // [0] factorizations, [1] fallbacks, [2..3] nudges, [4..7] slowest item
+  struct RqcState *state;    // modes 3, 4: per-task RQC state between the split phases
+  int *rkey;                 // mode 3: per-task twist index (sort key)
 };
 
 constexpr int kPairThreads = 64;  // pair kernel: one item per CTA, warp F + warp B
@@ -1050,6 +1053,153 @@ __device__ __forceinline__ void wvec_single_body(const WVecArgs &A) {
     atomicAdd(&A.ctr[0], nfact);
   }
 }
+
+// ---------------------------------------------------------------------------
+// SPLIT execution of the single-warp kernel.  Lanes of an item are
+// consecutive eigenvalues whose twist indices r lie anywhere in the node, so
+// a fixed-twist factorization (rows < r forward, rows > r backward) and the
+// solve walk the union of the lanes' ranges -- about 2 nb rows per warp
+// where each lane needs nb.  Phase 1 (mode 3) runs the full factorization
+// and the first RQC update and stores each task's state; the host's stream
+// then sorts every node's tasks by r (segmented radix sort); phase 2 (mode 4)
+// runs the rest of the RQC and the solve with the items' lanes taken in that
+// order (task_list), so the lanes of a warp share one row window.  Per-lane
+// arithmetic is unchanged (bit-identical results; the state is stored and
+// reloaded exactly).
+// ---------------------------------------------------------------------------
+struct RqcState {
+  double lam, lo, hi, delta_prev, lam_best, lam_fin, gamma, nrm2;
+  int r, negc, best_r0, flags;  // flags: 1 converged, 2 failed, 4 twist ok
+  unsigned long long nfact;
+};
+
+// The RQC update after a factorization `tw` at `lam` (iteration `it`), O10
+// readings 10 and 24 (the code of wvec_single_body's loop).
+struct RqcLane {
+  double lam, lo, hi, delta_prev, lam_best, lam_fin;
+  Twist best;
+  bool conv, failed;
+  __device__ __forceinline__ void update(const Twist &tw, int j, int it, int rqc_max) {
+    if (tw.negc >= j) { if (lam < hi) hi = lam; } else { if (lam > lo) lo = lam; }
+    const double delta = tw.gamma / tw.nrm2;
+    if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam ||
+        (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
+      conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
+    } else {
+      delta_prev = delta;
+      double nw = lam + delta;
+      if (nw <= lo || nw >= hi) {
+        if (lam == lo || lam == hi) {
+          nw = 0.5 * (lo + hi);
+          if (nw <= lo || nw >= hi) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }
+        } else {
+          nw = (nw <= lo) ? lo : hi;
+        }
+      }
+      lam = nw;
+    }
+    if (!conv && it >= rqc_max) { conv = true; failed = true; }
+  }
+};
+
+__device__ __forceinline__ void wvec_split_body(const WVecArgs &A) {
+  extern __shared__ __align__(16) unsigned char wsm_raw[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kSingleWarps + wid;
+  if (item >= A.nitems) return;  // whole warp
+  const WarpItem It = A.items[item];
+  const Node N = A.nodes[It.node];
+  const bool active = It.t0 + lane < It.t1;
+  const int tix = A.task_list ? A.task_list[active ? It.t0 + lane : It.t0] : (active ? It.t0 + lane : It.t0);
+  const VecTask tk = A.tasks[tix];
+  WarpCtx W;
+  W.DL = N.DL; W.LDv = A.LDv + N.row0; W.nb = N.nb; W.nseg = (N.nb + kTR - 1) / kTR;
+  W.lane = lane;
+  W.sm = reinterpret_cast<WarpSmem *>(wsm_raw) + wid;
+  W.fck = A.fck; W.bck = A.bck; W.ck_stride = A.ck_stride;
+  const int64_t spare = A.ntask + lane;
+  W.tix = active ? tix : spare;
+  const int j = A.slot_j[tk.slot];
+  if (A.mode == 3) {
+    if (N.nb == 1) return;  // phase 2 writes it
+    double lam = isnan(tk.lam0) ? 0.5 * (A.lo[tk.slot] + A.hi[tk.slot]) : tk.lam0;
+    unsigned long long nfact = 0;
+    Twist tw;
+    {
+      double nudge = 2.0 * kEps * fabs(lam) + kTiny;
+      const double lam_base = lam;
+      for (int tries = 0; tries < 60; ++tries) {
+        tw = w_twist_full(W, lam);
+        ++nfact;
+        if (!__any_sync(0xffffffffu, active && !tw.ok)) break;
+        if (active && !tw.ok) {
+          lam = lam_base + nudge; nudge *= 2.0;
+          atomicAdd(&A.ctr[2], 1ull);
+          if (A.ctr[3] == 0) A.ctr[3] = 1 + (isfinite(tw.gamma) ? 0 : 2) + (isfinite(tw.nrm2) ? 0 : 4);
+        }
+      }
+    }
+    RqcLane Q;
+    Q.lam = lam; Q.lo = A.lo[tk.slot]; Q.hi = A.hi[tk.slot]; Q.delta_prev = CUDART_INF;
+    Q.lam_best = lam; Q.lam_fin = lam; Q.best = tw; Q.conv = !active; Q.failed = false;
+    if (!Q.conv) Q.update(tw, j, 1, A.rqc_max);
+    if (active) {
+      RqcState st;
+      st.lam = Q.lam; st.lo = Q.lo; st.hi = Q.hi; st.delta_prev = Q.delta_prev;
+      st.lam_best = Q.lam_best; st.lam_fin = Q.lam_fin; st.gamma = Q.best.gamma; st.nrm2 = Q.best.nrm2;
+      st.r = Q.best.r; st.negc = Q.best.negc; st.best_r0 = tw.r;
+      st.flags = (Q.conv ? 1 : 0) | (Q.failed ? 2 : 0) | (Q.best.ok ? 4 : 0);
+      st.nfact = nfact;
+      A.state[tix] = st;
+      A.rkey[tix] = tw.r;
+    }
+    return;
+  }
+  // ---- mode 4: the rest of the RQC and the solve, lanes in twist order
+  if (N.nb == 1) {
+    if (active) { A.Z[tk.col * A.ldz + N.row0] = 1.0; A.lam_out[tix] = __ldg(&N.DL[0]).x; }
+    return;
+  }
+  RqcLane Q;
+  int best_r0 = 0;
+  unsigned long long nfact = 0;
+  if (active) {
+    const RqcState st = A.state[tix];
+    Q.lam = st.lam; Q.lo = st.lo; Q.hi = st.hi; Q.delta_prev = st.delta_prev;
+    Q.lam_best = st.lam_best; Q.lam_fin = st.lam_fin;
+    Q.best.r = st.r; Q.best.gamma = st.gamma; Q.best.nrm2 = st.nrm2; Q.best.negc = st.negc;
+    Q.best.ok = (st.flags & 4) != 0;
+    Q.conv = (st.flags & 1) != 0; Q.failed = (st.flags & 2) != 0;
+    best_r0 = st.best_r0; nfact = st.nfact;
+  } else {
+    Q.lam = 0.0; Q.lo = 0.0; Q.hi = 0.0; Q.delta_prev = CUDART_INF; Q.lam_best = 0.0; Q.lam_fin = 0.0;
+    Q.best.r = 0; Q.best.gamma = 0.0; Q.best.nrm2 = 1.0; Q.best.negc = 0; Q.best.ok = true;
+    Q.conv = true; Q.failed = false;
+  }
+  if (Q.conv) W.tix = spare;  // parked: its column holds the phase-1 factorization
+  for (int it = 1;;) {
+    if (__all_sync(0xffffffffu, Q.conv)) break;
+    const Twist tw = w_twist_fixed(W, Q.lam, best_r0, !Q.conv);
+    ++nfact;
+    ++it;
+    if (!Q.conv && !tw.ok) { Q.conv = true; Q.failed = true; }
+    else if (!Q.conv) Q.update(tw, j, it, A.rqc_max);
+    if (Q.conv) W.tix = spare;
+  }
+  W.tix = active ? tix : spare;
+  if (active && Q.failed) {
+    A.lo[tk.slot] = Q.lo; A.hi[tk.slot] = Q.hi;
+    A.fail_list[atomicAdd(A.fail_count, 1)] = A.task_base + tix;
+    atomicAdd(&A.ctr[1], 1ull);
+  }
+  const double sc = 1.0 / sqrt(Q.best.nrm2);
+  w_twist_solve(W, Q.lam_best, Q.best.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !Q.failed);
+  if (active && !Q.failed) A.lam_out[tix] = Q.lam_fin;
+  if (active) atomicAdd(&A.ctr[0], nfact);
+  if (lane == 0) atomicMax(&A.ctr[7], nfact);
+}
+
+__global__ void __launch_bounds__(32 * kSingleWarps) k_wvectors_split(WVecArgs A) { wvec_split_body(A); }
 
 __global__ void __launch_bounds__(kPairThreads) k_wvectors_pair(WVecArgs A) { wvec_pair_body(A); }
 __global__ void __launch_bounds__(32 * kSingleWarps) k_wvectors(WVecArgs A) { wvec_single_body(A); }

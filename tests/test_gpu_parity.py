@@ -171,7 +171,7 @@ def test_deterministic(torch_cuda, P):
 
 
 @pytest.mark.parametrize("env", [{"MRRR_CS_GROUP": "3"}, {"MRRR_VEC_MODE": "1"}, {"MRRR_VEC_PAIR": "0"},
-                                 {"MRRR_VEC_PAIR": "2"}, {"MRRR_HP_STREAM": "0"}])
+                                 {"MRRR_VEC_PAIR": "2"}, {"MRRR_HP_STREAM": "0"}, {"MRRR_VEC_SPLIT": "0"}])
 def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     """The launch schedule does not change a single bit: cluster steps in
     groups that reuse the scratch (MRRR_CS_GROUP, the n = 1e5 memory cap's
@@ -179,7 +179,9 @@ def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     vector piece on single warps or on warp pairs (MRRR_VEC_PAIR=0/2: the two
     kernels run the same per-lane arithmetic, the pair one with the sweeps
     split over two warps), the caller's stream instead of the library's
-    high-priority one (MRRR_HP_STREAM=0) -- against the default schedule.
+    high-priority one (MRRR_HP_STREAM=0), the single-warp RQC in one kernel
+    instead of two phases with the lanes regrouped by twist index
+    (MRRR_VEC_SPLIT=0) -- against the default schedule.
     Each cluster's step and each eigenpair's RQC depend on their own data only."""
     for d, e in (W.glued_wilkinson(40), W.random_uniform(3000, 2)):
         w1, Z1 = gpu_solve(P, torch_cuda, d, e)

@@ -173,16 +173,18 @@ typedef struct {
   int64_t safe_resweeps;    /* projective sweeps redone by the qd safe path */
   int64_t kernel_launches;  /* kernels launched by this call */
   double ms_root;           /* device time: prep + root RRR + root bisection */
-  double ms_tree;           /* device time: classification, children, refine */
-  double ms_vectors;        /* device time: singleton vectors + output */
+  double ms_tree;           /* device time: classification, children, refine (the vector
+                               pieces run beside it on side streams) */
+  double ms_vectors;        /* device time after the tree: the vector tail + output */
   double ms_total;          /* device time of the whole call */
   /* per-kernel device time (CUDA events on the call's stream) and the units
    * they processed, for the roofline of bench.py */
   double ms_k_root_bisect;  /* root grid + multisection kernels */
-  double ms_k_vectors;      /* singleton RQC + twisted + Z kernel */
+  double ms_k_vectors;      /* singleton RQC + twisted + Z kernels: sum of the pieces'
+                               event times (pieces overlap each other and the tree) */
   int64_t vec_tasks;        /* eigenvectors computed by that kernel */
   int64_t vec_elems;        /* sum over those tasks of their block order */
-  double ms_k_final_refine; /* singleton brackets to 2^-40 before the vectors */
+  double ms_k_final_refine; /* RQC fallback: bracket refinement to 4 eps (0 without fallback) */
 } mrrr_stats_t;
 int mrrr_get_stats(mrrr_stats_t *out);
 

@@ -656,7 +656,7 @@ int solve(Problem &P, int64_t *m_out) {
   Trace tr;
   g_staging.reset();
   Timer tm(s), tall(s);
-  KTimer kt_root, kt_vec, kt_fin;
+  KTimer kt_root, kt_fin;
   memset(&g_stats, 0, sizeof(g_stats));
   const bool vectors = P.Z != nullptr;
 
@@ -1354,8 +1354,10 @@ int solve(Problem &P, int64_t *m_out) {
         h2d(dfl, fl.data(), h_nf, s);
         Work *dw = ar.alloc<Work>(wv.size());
         h2d(dw, wv.data(), wv.size(), s);
+        kt_fin.start(s);
         launch_refine(dnodes, dw, (int)wv.size(), dslots, slot_j, slo, shi, nullptr, nullptr, 0, 4.0 * kEps,
                       dfail + 2, ctr + 2, ctr + 1, s);
+        kt_fin.stop(s);
         VecTask *dft = ar.alloc<VecTask>(h_nf);
         h2d(dft, ft.data(), h_nf, s);
         WarpItem *dfi = ar.alloc<WarpItem>(fitems.size());

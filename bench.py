@@ -269,7 +269,9 @@ def main():
     slots_bis = float(np.sum(B)) * (2 + W_DIV) * n
     slots_vec = stats[-1]["vec_elems"] * (R_RQC * (10 + 2 * W_DIV) + 1)
     # the dominant kernel carrying algorithmic work: the singleton vectors
-    dom, slots, kms = "k_wvectors", slots_vec, kv
+    # (k_wvectors_split's two phases for single-warp pieces, k_wvectors_pair
+    # for pieces beside narrow tree levels; their launches' event times summed)
+    dom, slots, kms = "k_wvectors_split", slots_vec, kv
     achieved = 2 * slots / (kms / 1e3) / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -285,7 +287,7 @@ def main():
             "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
             "kernel_ms": kms, "kernel_share_of_step": kms / (tot_ms / args.steps),
             "algorithmic_slots_per_step": slots, "w_div": W_DIV,
-            "note": "k_wvectors runs as per-level pieces on four side streams that overlap each other "
+            "note": "the vector kernels run as per-level pieces on four side streams that overlap each other "
                     "and the tree; achieved = sum of its slots / sum of its launch durations (CUDA "
                     "events on each launch's stream), i.e. the work-weighted per-launch rate; a piece "
                     "holds few warps and is latency-bound, so this sits far below the step fraction, "

@@ -14,7 +14,7 @@ timeout 600 python bench.py --steps 3 --warmup 3 --impl reference > gpurun_out/$
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 timeout 600 $CMD > gpurun_out/${T}_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/${T}_launches.csv $CMD > gpurun_out/${T}_ncu_launch.log 2>&1 && \
-for k in k_wvectors:8 k_child_step:7 regex:k_refine_warp:9; do
+for k in k_wvectors_split:9 k_child_step:7 regex:k_refine_warp:9; do
   name=${k%:*}; skip=${k##*:}; tag=${name#regex:}
   timeout 900 ncu --set full --clock-control none --import-source on -k $name -s $skip -c 1 -o gpurun_out/${T}_prof_$tag $CMD > gpurun_out/${T}_ncu_full_$tag.log 2>&1
 done

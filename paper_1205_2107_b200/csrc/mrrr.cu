@@ -88,6 +88,14 @@ cudaStream_t *side_streams() {
   return x;
 }
 
+cudaStream_t copy_stream() {  // Z downloads of the host entry (per thread and device)
+  thread_local cudaStream_t st[64] = {};
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  if (!st[d & 63]) CK(cudaStreamCreateWithFlags(&st[d & 63], cudaStreamNonBlocking));
+  return st[d & 63];
+}
+
 int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return v ? atoi(v) : dflt;
@@ -610,6 +618,10 @@ struct Problem {
   void *ag_ctx = nullptr;
   double *w_all = nullptr;  // dist: all m eigenvalues (device); P.w is then unused
   int64_t col_begin = 0, m_local = 0;
+  // host entry with a pinned destination: Z column blocks are downloaded to
+  // hZ (leading dimension hldz) as soon as their vectors are written
+  double *hZ = nullptr;
+  int64_t hldz = 0;
 };
 
 struct HostNode {
@@ -1079,6 +1091,38 @@ int solve(Problem &P, int64_t *m_out) {
   BwdCk *ck_b[kSide] = {};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vec_ev;
   size_t vec_done = 0;
+  // streamed download (host entry, pinned Z): a block of kZB columns goes to
+  // the host on the copy stream once every piece that writes into it has been
+  // launched, after those pieces' events -- the D2H of Z (3.2 GB at n = 20000)
+  // overlaps the rest of the solve instead of following it
+  constexpr int64_t kZB = 256;
+  const bool zstream = P.hZ != nullptr && vectors && P.m_local > 0;
+  cudaStream_t sc = zstream ? copy_stream() : nullptr;
+  const int64_t nzb = zstream ? (P.m_local + kZB - 1) / kZB : 0;
+  std::vector<int64_t> zb_left(nzb, 0);
+  std::vector<std::vector<cudaEvent_t>> zb_ev(nzb);
+  if (zstream) {
+    for (int q = 0; q < (int)nslots; ++q)
+      if (h_own[q] >= 0) ++zb_left[h_own[q] / kZB];
+    cudaEvent_t e0 = ev_sync();  // Z's memset (split matrices) precedes every copy
+    CK(cudaEventRecord(e0, s));
+    CK(cudaStreamWaitEvent(sc, e0, 0));
+  }
+  auto zb_copy = [&](int64_t c0, int64_t c1) {  // columns [c0, c1) after sc's pending waits
+    CK(cudaMemcpy2DAsync(P.hZ + c0 * P.hldz, P.hldz * sizeof(double), P.Z + c0 * P.ldz,
+                         P.ldz * sizeof(double), n * sizeof(double), c1 - c0, cudaMemcpyDeviceToHost, sc));
+  };
+  auto zb_done = [&](size_t t0, size_t t1, cudaEvent_t eb) {  // tasks [t0, t1) written after eb
+    if (!zstream) return;
+    for (size_t t = t0; t < t1; ++t) {
+      const int64_t b = tasks[t].col / kZB;
+      if (zb_ev[b].empty() || zb_ev[b].back() != eb) zb_ev[b].push_back(eb);
+      if (--zb_left[b] == 0) {
+        for (cudaEvent_t e : zb_ev[b]) CK(cudaStreamWaitEvent(sc, e, 0));
+        zb_copy(b * kZB, std::min<int64_t>(P.m_local, (b + 1) * kZB));
+      }
+    }
+  };
   // pieces that overlap a busy tree level run on single warps (smaller
   // footprint next to the tree's kernels); the last flush, and pieces whose
   // level leaves at most kPairMaxClusters clusters to refine, on warp pairs
@@ -1158,6 +1202,7 @@ int solve(Problem &P, int64_t *m_out) {
       CK(cudaEventRecord(eb, s2));
       tr.fine(s2, "  vectors (side stream)");
       vec_ev.push_back({ea, eb});
+      zb_done(t0, t1, eb);
       t0 = t1;
     }
     vec_done = tasks.size();
@@ -1373,7 +1418,26 @@ int solve(Problem &P, int64_t *m_out) {
         k_scatter<<<(h_nf + 255) / 256, 256, 0, s>>>(dfl, lam_c, h_nf, lam);
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
+        if (zstream) {  // the fallback rewrote these columns: download them again
+          cudaEvent_t ef = ev_sync();
+          CK(cudaEventRecord(ef, s));
+          CK(cudaStreamWaitEvent(sc, ef, 0));
+          for (int q = 0; q < h_nf; ++q) zb_copy(tasks[fl[q]].col, tasks[fl[q]].col + 1);
+        }
       }
+    }
+    if (zstream) {
+      // blocks with columns no piece wrote (none expected): download after all work
+      cudaEvent_t ez = ev_sync();
+      CK(cudaEventRecord(ez, s));
+      for (int64_t b = 0; b < nzb; ++b)
+        if (zb_left[b] > 0) {
+          CK(cudaStreamWaitEvent(sc, ez, 0));
+          zb_copy(b * kZB, std::min<int64_t>(P.m_local, (b + 1) * kZB));
+        }
+      cudaEvent_t ej = ev_sync();  // the call's stream waits for the downloads
+      CK(cudaEventRecord(ej, sc));
+      CK(cudaStreamWaitEvent(s, ej, 0));
     }
     if (getenv("MRRR_DEBUG_TASKS")) {
       std::vector<double> hl(ntask);
@@ -1462,14 +1526,15 @@ __global__ void k_n1(const double *d, double *w, double *Z) {
   if (Z) Z[0] = 1.0;
 }
 
-int mrrr_stemr(int64_t n, const double *d, const double *e, int range, double vl, double vu,
-               int64_t il, int64_t iu, int64_t *m, double *w, double *Z, int64_t ldz,
-               void *stream, const mrrr_opts_t *opts) {
-  int v = validate(n, d, e, range, vl, vu, il, iu, m, w, Z, ldz);
-  if (v) return v;
+// mrrr_stemr after validation; hZ (pinned host, leading dimension hldz) =
+// stream Z's column blocks to the host as they complete (mrrr_stemr_host).
+int stemr_device(int64_t n, const double *d, const double *e, int range, double vl, double vu,
+                 int64_t il, int64_t iu, int64_t *m, double *w, double *Z, int64_t ldz,
+                 void *stream, const mrrr_opts_t *opts, double *hZ, int64_t hldz) {
   Problem P;
   P.n = n; P.d = d; P.e = e; P.range = range; P.vl = vl; P.vu = vu; P.il = il; P.iu = iu;
   P.w = w; P.Z = Z; P.ldz = ldz; P.s = (cudaStream_t)stream;
+  P.hZ = (n > 1 && Z) ? hZ : nullptr; P.hldz = hldz;
   if (opts) P.o = *opts; else mrrr_default_opts(&P.o);
   if (P.o.rtol_vec != 0.0) return -14;  // oracle-only experiment (reading 10)
   try {
@@ -1503,6 +1568,14 @@ int mrrr_stemr(int64_t n, const double *d, const double *e, int range, double vl
   }
 }
 
+int mrrr_stemr(int64_t n, const double *d, const double *e, int range, double vl, double vu,
+               int64_t il, int64_t iu, int64_t *m, double *w, double *Z, int64_t ldz,
+               void *stream, const mrrr_opts_t *opts) {
+  int v = validate(n, d, e, range, vl, vu, il, iu, m, w, Z, ldz);
+  if (v) return v;
+  return stemr_device(n, d, e, range, vl, vu, il, iu, m, w, Z, ldz, stream, opts, nullptr, 0);
+}
+
 int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range, double vl,
                     double vu, int64_t il, int64_t iu, int64_t *m, double *w, double *Z,
                     int64_t ldz, void *stream, const mrrr_opts_t *opts) {
@@ -1527,12 +1600,21 @@ int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range, doub
     if ((ce = cudaMemcpyAsync(dd, d, n * sizeof(double), cudaMemcpyHostToDevice, s))) break;
     if (n > 1 && (ce = cudaMemcpyAsync(de, e, (n - 1) * sizeof(double), cudaMemcpyHostToDevice, s)))
       break;
-    rc = mrrr_stemr(n, dd, de, range, vl, vu, il, iu, m, dw, dZ, n, stream, opts);
+    // a pinned Z receives its column blocks while the solve runs (copy
+    // stream); a pageable one after the solve
+    bool pinned = false;
+    if (Z) {
+      cudaPointerAttributes pa{};
+      if (cudaPointerGetAttributes(&pa, Z) == cudaSuccess) pinned = pa.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+    }
+    rc = stemr_device(n, dd, de, range, vl, vu, il, iu, m, dw, dZ, n, stream, opts, pinned ? Z : nullptr, ldz);
     if (rc) break;
     if (*m > 0) {
       if ((ce = cudaMemcpyAsync(w, dw, *m * sizeof(double), cudaMemcpyDeviceToHost, s))) break;
-      if (Z && (ce = cudaMemcpy2DAsync(Z, ldz * sizeof(double), dZ, n * sizeof(double),
-                                       n * sizeof(double), *m, cudaMemcpyDeviceToHost, s)))
+      if (Z && (!pinned || n == 1) &&
+          (ce = cudaMemcpy2DAsync(Z, ldz * sizeof(double), dZ, n * sizeof(double), n * sizeof(double), *m,
+                                  cudaMemcpyDeviceToHost, s)))
         break;
     }
     ce = cudaStreamSynchronize(s);

@@ -202,6 +202,28 @@ def test_host_entry_matches_device(torch_cuda, P):
     assert np.array_equal(w1, w2.numpy()) and np.array_equal(Z1, Z2.numpy())
 
 
+@pytest.mark.parametrize("case", ["pinned_glued", "pageable_random", "pinned_split_subset"])
+def test_host_entry_streamed_z(torch_cuda, P, case):
+    """mrrr_stemr_host downloads a pinned Z by column blocks while the solve
+    runs (copy stream, after the pieces that wrote each block) and a pageable
+    Z after it; both equal the device entry bit for bit, including a split
+    matrix (Z zeroed first) with an index subset."""
+    torch = torch_cuda
+    kw = {}
+    if case == "pinned_glued":
+        d, e = W.glued_wilkinson(60)
+    elif case == "pageable_random":
+        d, e = W.random_uniform(2500, 4)
+    else:
+        d, e = split_matrix()
+        kw = {"il": 11, "iu": 70}
+    w1, Z1 = gpu_solve(P, torch, d, e, **kw)
+    k = len(w1)
+    Zh = torch.empty((k, len(d)), dtype=torch.float64, pin_memory=(case != "pageable_random"))
+    w2, Z2 = P.stemr_host(torch.tensor(d).pin_memory(), torch.tensor(e).pin_memory(), Z=Zh, **kw)
+    assert np.array_equal(w1, w2.numpy()) and np.array_equal(Z1, Z2.numpy())
+
+
 # ---------------------------------------------------------------------------
 # BASELINE configs at full size (bench launch configuration): GPU-side
 # residual / orthogonality, oracle index windows, closed forms, invariants.

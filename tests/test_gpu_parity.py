@@ -224,6 +224,26 @@ def test_host_entry_streamed_z(torch_cuda, P, case):
     assert np.array_equal(w1, w2.numpy()) and np.array_equal(Z1, Z2.numpy())
 
 
+def test_rqc_fallback_path(torch_cuda, P):
+    """rqc_max = 1 sends every eigenpair whose first correction has not
+    converged through the deferred O10 fallback (bracket refined to 4 eps by
+    multisection, one factorization at its midpoint, reading 10), including
+    the host entry's re-download of the rewritten columns: accuracy holds and
+    the host entry equals the device entry bit for bit."""
+    torch = torch_cuda
+    d, e = W.random_uniform(1800, 9)
+    o = P.default_opts(rqc_max=1)
+    dt, et = torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda")
+    w1, Z1 = P.stemr(dt, et, opts=o)
+    torch.cuda.synchronize()
+    assert P.last_stats()["rqc_fallbacks"] > 0
+    w1, Z1 = w1.cpu().numpy(), Z1.cpu().numpy()
+    res, orth = check_accuracy(d, e, w1, Z1)
+    assert res <= 1.0 and orth <= 1.0, (res, orth)
+    w2, Z2 = P.stemr_host(torch.tensor(d).pin_memory(), torch.tensor(e).pin_memory(), opts=o)
+    assert np.array_equal(w1, w2.numpy()) and np.array_equal(Z1, Z2.numpy())
+
+
 # ---------------------------------------------------------------------------
 # BASELINE configs at full size (bench launch configuration): GPU-side
 # residual / orthogonality, oracle index windows, closed forms, invariants.

@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
       return fmin(fmax(log2(fabs(x)), -4096.0), 4096.0);
     };
     double run = 0.0;
+#pragma unroll 8
     for (int j = j0; j < j1; ++j) run += lval(j);
     double incl = run;
     for (int o = 1; o < 32; o <<= 1) {
@@ -299,6 +300,7 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
       if (lane >= o) incl += y;
     }
     double acc = incl - run;  // exclusive prefix of this lane's run
+#pragma unroll 8
     for (int j = j0; j < j1; ++j) {
       acc += lval(j);
       if (up) z[r - 1 - j] = exp2(acc);

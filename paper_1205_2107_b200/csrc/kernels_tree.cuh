@@ -195,6 +195,81 @@ __global__ void k_root_chain(const double *__restrict__ ds, const double *__rest
   sigma_out[b] = 0.0;
 }
 
+// Warp version of pass 1 (one warp per block): rows of d and e^2 come
+// through a cp.async ring of 16-row tiles (lanes 0-15: d_i, 16-31:
+// e_{i-1}^2), every lane runs the same chain, lane k keeps row k's t_i and
+// rescale, and each tile's values are stored with coalesced writes.  The
+// arithmetic is that of k_root_chain (same operations, same order).
+constexpr int kRCT = 16, kRCRing = 6;
+__global__ void __launch_bounds__(32) k_root_chain_warp(const double *__restrict__ ds,
+                                                        const double *__restrict__ es2, Block *blocks,
+                                                        int nblocks, double tnrm_scaled, double *tbuf,
+                                                        int *sbuf, double *sigma_out, int *fail) {
+  __shared__ double rD[kRCRing][kRCT], rE[kRCRing][kRCT];
+  const int b = blockIdx.x, lane = threadIdx.x;
+  if (b >= nblocks) return;
+  const Block B = blocks[b];
+  if (B.nb < 2 || B.slot1 <= B.slot0) { if (lane == 0) sigma_out[b] = 0.0; return; }
+  const double *dr = ds + B.row0;
+  const double *er = es2 + B.row0;  // er[i-1] = e_{i-1}^2 of the block
+  const int nb = B.nb, ntile = (nb + kRCT - 1) / kRCT;
+  auto issue = [&](int t) {
+    const int slot = t % kRCRing, k = lane & (kRCT - 1), row = t * kRCT + k;
+    if (t < ntile && row < nb) {
+      if (lane < kRCT) __pipeline_memcpy_async(&rD[slot][k], &dr[row], sizeof(double));
+      else if (row > 0) __pipeline_memcpy_async(&rE[slot][k], &er[row - 1], sizeof(double));
+    }
+    __pipeline_commit();
+  };
+  double delta = 4.0 * kEps * tnrm_scaled;
+  for (int attempt = 0; attempt <= 6; ++attempt) {
+    const double sigma = B.side > 0 ? B.gl - delta : B.gu + delta;
+    double tm1 = 1.0, tm2 = 0.0;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < kRCRing - 1; ++k) issue(k);
+    for (int t = 0; t < ntile; ++t) {
+      __pipeline_wait_prior(kRCRing - 2);
+      __syncwarp();
+      const int slot = t % kRCRing, r0 = t * kRCT, rows = min(kRCT, nb - r0);
+      double kt = 0.0;
+      int ks = 0;
+      auto row = [&](int k) {
+        const int i = r0 + k;
+        const double di = rD[slot][k];
+        const double b2 = (i > 0) ? rE[slot][k] : 0.0;
+        const double tt = fma(di - sigma, tm1, -b2 * tm2);
+        const bool good = (tt != 0.0) && ((B.side > 0) ? (negbit(tt, tm1) == 0) : (negbit(tt, tm1) == 1));
+        ok &= good && isfinite(tt);
+        int sh = 0;
+        tm2 = tm1; tm1 = tt;
+        if ((i & 7) == 7) {
+          const int ee = max_exp(tm1, tm2);
+          ok &= ee < 2047 && ee > 0;
+          sh = 1023 - min(max(ee, 1), 2045);
+          const double f = pow2(sh);
+          tm1 *= f; tm2 *= f;
+        }
+        if (lane == k) { kt = tt; ks = sh; }
+      };
+      if (rows == kRCT) {
+#pragma unroll
+        for (int k = 0; k < kRCT; ++k) row(k);
+      } else {
+        for (int k = 0; k < rows; ++k) row(k);
+      }
+      if (lane < rows) { tbuf[B.row0 + r0 + lane] = kt; sbuf[B.row0 + r0 + lane] = ks; }
+      __syncwarp();
+      issue(t + kRCRing - 1);
+    }
+    __pipeline_wait_prior(0);
+    __syncwarp();
+    if (ok) { if (lane == 0) sigma_out[b] = sigma; return; }
+    delta *= 2.0;
+  }
+  if (lane == 0) { fail[0] = 1; sigma_out[b] = 0.0; }
+}
+
 __global__ void k_root_finish(const double *__restrict__ ds, const double *__restrict__ es,
                               const Block *blocks, const int *__restrict__ row_block, int64_t n,
                               const double *__restrict__ tbuf, const int *__restrict__ sbuf,

@@ -345,6 +345,75 @@ __global__ void k_root_interval(const Node *nodes, const Block *blocks, const in
   }
 }
 
+// Warp version: the 32 lanes try the offsets wid * 2^k, k = k0 .. k0+31, in
+// ONE sweep of the root representation (rows through a cp.async ring of
+// 16-row tiles, read as broadcasts); the first passing k is the sequential
+// loop's answer.
+__global__ void __launch_bounds__(32) k_root_interval_warp(const Node *nodes, const Block *blocks,
+                                                           const int *root_nodes, int nroot, double *lo0,
+                                                           double *hi0, double tnrm_scaled) {
+  constexpr int T = 16, RING = 6;
+  __shared__ double2 ring[RING][T];
+  const int r = blockIdx.x, lane = threadIdx.x;
+  if (r >= nroot) return;
+  const Node N = nodes[root_nodes[r]];
+  const Block B = blocks[N.block];
+  const double sigma = N.tau_hi;
+  const double wid0 = 2.0 * kEps * fmax(B.spdiam, tnrm_scaled) + kTiny;
+  if (N.nb == 1) { if (lane == 0) { lo0[r] = hi0[r] = __ldg(&N.DL[0]).x; } return; }
+  const int nb = N.nb, body = nb - 1, ntile = (body + T - 1) / T;
+  for (int k0 = 0; k0 < 224; k0 += 32) {
+    const double w = wid0 * ldexp(1.0, k0 + lane);
+    const double mu = B.side > 0 ? (B.gu - sigma) + w : (B.gl - sigma) - w;
+    Sturm st;
+    sturm_init(st, mu);
+    bool ok = true;
+    auto issue = [&](int t) {
+      const int row = t * T + lane;
+      if (lane < T && t < ntile && row < body) __pipeline_memcpy_async(&ring[t % RING][lane], &N.DL[row], sizeof(double2));
+      __pipeline_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < RING - 1; ++k) issue(k);
+    for (int t = 0; t < ntile; ++t) {
+      __pipeline_wait_prior(RING - 2);
+      __syncwarp();
+      const int rows = min(T, body - t * T);
+      if (rows == T) {
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+          const double2 v = ring[t % RING][k];
+          sturm_step(st, v.x, v.y, mu);
+          if ((k & 7) == 7) ok &= sturm_rescale(st);
+        }
+      } else {
+        for (int k = 0; k < rows; ++k) {
+          const double2 v = ring[t % RING][k];
+          sturm_step(st, v.x, v.y, mu);
+          if ((k & 7) == 7) ok &= sturm_rescale(st);
+        }
+      }
+      __syncwarp();
+      issue(t + RING - 1);
+    }
+    __pipeline_wait_prior(0);
+    sturm_last(st, __ldg(&N.DL[nb - 1]).x);
+    unsigned c = st.c;
+    if (!ok || !sturm_ok(st)) c = negcount_qd_safe(N.DL, nb, mu);
+    const bool pass = B.side > 0 ? ((int)c >= nb) : ((int)c <= 0);
+    const unsigned bal = __ballot_sync(0xffffffffu, pass);
+    if (bal) {
+      const int first = __ffs(bal) - 1;
+      const double m = __shfl_sync(0xffffffffu, mu, first);
+      if (lane == 0) {
+        if (B.side > 0) { lo0[r] = 0.0; hi0[r] = m; }
+        else { hi0[r] = 0.0; lo0[r] = m; }
+      }
+      return;
+    }
+  }
+}
+
 __global__ void k_block_norms(const double *ds, const double *es, Block *blocks, int nblocks) {
   int b = blockIdx.x;
   if (b >= nblocks) return;
@@ -811,8 +880,11 @@ int solve(Problem &P, int64_t *m_out) {
   int *dfail = ar.alloc<int>(4);
   CK(cudaMemsetAsync(dfail, 0, 4 * sizeof(int), s));
   CK(cudaMemsetAsync(sigma_b, 0, nblocks * sizeof(double), s));
-  k_root_chain<<<(nblocks + 63) / 64, 64, 0, s>>>(ds, es2, dblocks, nblocks, tnrm_s, tbuf, sbuf,
-                                                  sigma_b, dfail);
+  if (nblocks <= 4096)  // one warp per block (smem-tiled chain); many tiny blocks: one thread each
+    k_root_chain_warp<<<nblocks, 32, 0, s>>>(ds, es2, dblocks, nblocks, tnrm_s, tbuf, sbuf, sigma_b, dfail);
+  else
+    k_root_chain<<<(nblocks + 63) / 64, 64, 0, s>>>(ds, es2, dblocks, nblocks, tnrm_s, tbuf, sbuf,
+                                                    sigma_b, dfail);
   CK(cudaGetLastError());
   std::vector<int> h_row_block(n);
   for (int b = 0; b < nblocks; ++b)
@@ -845,7 +917,10 @@ int solve(Problem &P, int64_t *m_out) {
   int *droot_nodes = ar.alloc<int>(nroot);
   h2d(droot_nodes, h_root_nodes.data(), nroot, s);
   double *dlo0 = ar.alloc<double>(nroot), *dhi0 = ar.alloc<double>(nroot);
-  k_root_interval<<<(nroot + 63) / 64, 64, 0, s>>>(dnodes, dblocks, droot_nodes, nroot, dlo0, dhi0,
+  if (nroot <= 4096)
+    k_root_interval_warp<<<nroot, 32, 0, s>>>(dnodes, dblocks, droot_nodes, nroot, dlo0, dhi0, tnrm_s);
+  else
+    k_root_interval<<<(nroot + 63) / 64, 64, 0, s>>>(dnodes, dblocks, droot_nodes, nroot, dlo0, dhi0,
                                                      tnrm_s);
   CK(cudaGetLastError());
   g_stats.kernel_launches += 2;

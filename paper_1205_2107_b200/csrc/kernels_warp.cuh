@@ -397,46 +397,38 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
   // ---- backward (progressive) sweep with replay and argmin |gamma|
   Bwd B{__ldg(&W.DL[nb - 1]).x - lam, 1.0, 0.0, 0};
   int best_r = nb - 1;
-  double bN = 0, bden = 0, bH = 0, bq = 1, bK = 0, bb = 1;
-  int bneg = 0;
+  double bN = 0, bden = 0;
   bool have = false;
   FwdCk ckn = W.fck[(int64_t)(W.nseg - 1) * W.ck_stride + W.tix];
   w_tiles_down(W, W.nseg - 1, 0, [&](int c, int slot) {
     const int r0 = c * kTR, r1 = min(r0 + kTR, nb);
     {
-      BwdCk bk; bk.a = B.a; bk.b = B.b;  // state at row min(r0 + kTR, nb - 1)
+      BwdCk bk; bk.a = B.a; bk.b = B.b; bk.K = B.K; bk.neg = B.neg; bk.pad = 0;  // state at row min(r0 + kTR, nb - 1)
       W.bck[(int64_t)c * W.ck_stride + W.tix] = bk;
     }
     const FwdCk ck = ckn;
     if (c > 0) ckn = W.fck[(int64_t)(c - 1) * W.ck_stride + W.tix];
-    Fwd G{ck.p, ck.q, ck.H, 0};
-    unsigned mask = 0;
+    Fwd G{ck.p, ck.q, 0.0, 0};
     // argmin |gamma| by cross-multiplication, branch-free (selects) so that
-    // the next rows' progressive steps are scheduled across the comparison
+    // the next rows' progressive steps are scheduled across the comparison;
+    // only (N, den, r) are tracked -- the partial norms and negcounts at the
+    // chosen r are recomputed after the sweep from the two checkpoints
     auto eval = [&](int k) {
-      const double fpi = S.sA[k][L], fqi = S.sB[k][L], fHi = S.sC[k][L];
+      const double fpi = S.sA[k][L], fqi = S.sB[k][L];
       const double qb = fqi * B.b;
       const double N = fma(fpi, B.b, fma(B.a, fqi, lam * qb));
       const bool better = (!have || (fabs(N) * fabs(bden) <= fabs(bN) * fabs(qb))) && qb != 0.0 &&
                           isfinite(N);
-      const int negk = ck.neg + __popc(mask & ((1u << k) - 1u)) + B.neg;
       have |= better;
       best_r = better ? r0 + k : best_r;
       bN = better ? N : bN;
       bden = better ? qb : bden;
-      bH = better ? fHi : bH;
-      bq = better ? fqi : bq;
-      bK = better ? B.K : bK;
-      bb = better ? B.b : bb;
-      bneg = better ? negk : bneg;
     };
-    if (r1 < nb) {  // full segment, rows r0 .. r0+31 all below nb-1
+    if (r1 < nb) {  // full segment, rows r0 .. r0+15 all below nb-1
 #pragma unroll 8
       for (int k = 0; k < kTR; ++k) {
-        S.sA[k][L] = G.p; S.sB[k][L] = G.q; S.sC[k][L] = G.H;
-        const int before = G.neg;
+        S.sA[k][L] = G.p; S.sB[k][L] = G.q;
         G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
-        mask |= (unsigned)(G.neg - before) << k;
       }
 #pragma unroll 8
       for (int k = kTR - 1; k >= 0; --k) {
@@ -446,12 +438,8 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
     } else {  // the top segment: rows r0 .. nb-1
       const int nr = r1 - r0;
       for (int k = 0; k < nr; ++k) {
-        S.sA[k][L] = G.p; S.sB[k][L] = G.q; S.sC[k][L] = G.H;
-        if (k < nr - 1) {
-          const int before = G.neg;
-          G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
-          mask |= (unsigned)(G.neg - before) << k;
-        }
+        S.sA[k][L] = G.p; S.sB[k][L] = G.q;
+        if (k < nr - 1) G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
       }
       eval(nr - 1);
       for (int k = nr - 2; k >= 0; --k) {
@@ -462,11 +450,30 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
     return false;
   });
   ok &= isfinite(B.a) && isfinite(B.b) && have;
+  // the states at r by replay: forward from the checkpoint of r's segment
+  // (rows c*kTR .. r-1), backward from the checkpoint at the segment's top
+  // (rows top-1 .. r) -- the same operations the sweeps did, so the values
+  // equal those the search saw at r
+  const int cr = best_r / kTR, top = min(cr * kTR + kTR, nb - 1);
+  const FwdCk fk = W.fck[(int64_t)cr * W.ck_stride + W.tix];
+  const BwdCk bk = W.bck[(int64_t)cr * W.ck_stride + W.tix];
+  Fwd Fr{fk.p, fk.q, fk.H, fk.neg};
+  for (int i = cr * kTR; i < best_r; ++i) {
+    const double2 dl = __ldg(&W.DL[i]), lv = __ldg(&W.LDv[i]);
+    Row R; R.D = dl.x; R.LLD = dl.y; R.LD = lv.x; R.LD2 = lv.y;
+    Fr.step_r(R, lam, (i & 7) == 7);
+  }
+  Bwd Br{bk.a, bk.b, bk.K, bk.neg};
+  for (int i = top - 1; i >= best_r; --i) {
+    const double2 dl = __ldg(&W.DL[i]), lv = __ldg(&W.LDv[i]);
+    Row R; R.D = dl.x; R.LLD = dl.y; R.LD = lv.x; R.LD2 = lv.y;
+    Br.step_r(R, lam, (i & 7) == 0);
+  }
   Twist tw;
   tw.r = best_r;
   tw.gamma = bN / bden;
-  tw.nrm2 = 1.0 + bH / (bq * bq) + bK / (bb * bb);
-  tw.negc = bneg + ((tw.gamma < 0.0) ? 1 : 0);
+  tw.nrm2 = 1.0 + Fr.H / (Fr.q * Fr.q) + Br.K / (Br.b * Br.b);
+  tw.negc = Fr.neg + Br.neg + ((tw.gamma < 0.0) ? 1 : 0);
   tw.ok = ok && isfinite(tw.gamma) && isfinite(tw.nrm2);
   return tw;
 }

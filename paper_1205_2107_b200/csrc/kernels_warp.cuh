@@ -409,6 +409,18 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
     const FwdCk ck = ckn;
     if (c > 0) ckn = W.fck[(int64_t)(c - 1) * W.ck_stride + W.tix];
     Fwd G{ck.p, ck.q, 0.0, 0};
+    // the replay needs (p, q) only: the step and rescale of Fwd without H
+    // and the negcount (the same p, q values: the rescale factor depends on
+    // p and q alone)
+    auto gstep = [&](const Row &R, bool rescale) {
+      const double t = fma(R.D, G.q, G.p);
+      G.p = fma(-lam, t, R.LLD * G.p);
+      G.q = t;
+      if (rescale) {
+        const double f = pow2_scale(min(max_exp(G.p, G.q), 2045));
+        G.p *= f; G.q *= f;
+      }
+    };
     // argmin |gamma| by cross-multiplication, branch-free (selects) so that
     // the next rows' progressive steps are scheduled across the comparison;
     // only (N, den, r) are tracked -- the partial norms and negcounts at the
@@ -428,7 +440,7 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
 #pragma unroll 8
       for (int k = 0; k < kTR; ++k) {
         S.sA[k][L] = G.p; S.sB[k][L] = G.q;
-        G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+        gstep(w_row(W, slot, k), (k & 7) == 7);
       }
 #pragma unroll 8
       for (int k = kTR - 1; k >= 0; --k) {
@@ -439,7 +451,7 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
       const int nr = r1 - r0;
       for (int k = 0; k < nr; ++k) {
         S.sA[k][L] = G.p; S.sB[k][L] = G.q;
-        if (k < nr - 1) G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
+        if (k < nr - 1) gstep(w_row(W, slot, k), (k & 7) == 7);
       }
       eval(nr - 1);
       for (int k = nr - 2; k >= 0; --k) {

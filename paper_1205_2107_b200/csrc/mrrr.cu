@@ -1202,7 +1202,7 @@ int solve(Problem &P, int64_t *m_out) {
   // footprint next to the tree's kernels); the last flush, and pieces whose
   // level leaves at most kPairMaxClusters clusters to refine, on warp pairs
   // (half the latency, resources to spare).  MRRR_VEC_PAIR: 0 never, 2 always.
-  constexpr int kPairMaxClusters = 32;
+  const int kPairMaxClusters = env_int("MRRR_PAIR_MAXCL", 32);
   const int vec_pair = env_int("MRRR_VEC_PAIR", 1);
   const int vec_split = env_int("MRRR_VEC_SPLIT", 1);
   auto flush_vectors = [&](int tree_left) {

@@ -1,7 +1,9 @@
 // mrrr.cu -- host orchestrator and C ABI (include/mrrr.h) of the B200-native
 // MRRR tridiagonal eigensolver.  The orchestrator plans launches (blocks,
 // slots, tree levels, work chunks) from small read-backs; every arithmetic
-// step of the method runs in the kernels of kernels_tree.cuh / kernels_vec.cuh.
+// step of the method runs in the kernels of kernels_tree.cuh (root, bisection,
+// classification), kernels_child.cuh (the cluster step) and kernels_warp.cuh
+// (twisted factorizations and vectors).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
   double *zl = base + 14 * zs, *zr = base + 15 * zs;
 
   // ---- phase 1: the five chains
+  const long long clk_p0 = clock64();
   if (wid < 4) {
     const int side = wid >> 1;
     const int slot = side == 0 ? s0 : s1;
@@ -254,7 +255,9 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
     cs_candidates(S.ring[4], S, DL, nb, sigma, lane, DP, zs);
     if (lane < 6) S.sig[lane] = sigma;
   }
+  if (lane == 0) atomicMax(&A.ctr[1 + (wid == 4 ? 1 : (wid & 1) ? 2 : 3)], (unsigned long long)(clock64() - clk_p0));
   __syncthreads();
+  const long long clk_p1 = clock64();
 
   // ---- phase 2: each probe's twist index and |z| (warps 2 side, 2 side + 1)
   if (wid < 4) {
@@ -281,34 +284,58 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
     const int i0 = S.am_i[2 * side], i1 = S.am_i[2 * side + 1];
     int r = (v1 < v0 || (v1 == v0 && i1 < i0)) ? i1 : i0;
     if (r >= nb) r = nb - 1;  // no finite gamma: any twist (the vector only weights)
-    // |z| by a two-level scan of log2 |ratio|: lane l owns a contiguous run of
-    // the side's ratios (sum, warp scan of the sums, second walk writing z)
+    // |z| by a two-level product scan of |ratio| in (mantissa, exponent)
+    // form -- m in [1, 2), the exponent a double (exact integers) -- so no
+    // product over- or underflows and no transcendental is evaluated: lane l
+    // owns a contiguous run of the side's ratios (product, warp scan of the
+    // products, second walk writing z).  A zero or non-finite ratio zeroes
+    // the rest of that side (as a log of -inf would).
     const bool up = (wid & 1) == 0;     // up: rows r-1 .. 0 from rho; down: rows r+1 .. nb-1 from sig
     const int m = up ? r : nb - 1 - r;  // ratios on this side
     if (up && lane == 0) z[r] = 1.0;
     const int chunk = (m + 31) >> 5, j0 = min(lane * chunk, m), j1 = min(j0 + chunk, m);
-    auto lval = [&](int j) {
-      const double x = up ? sR[r - 1 - j] : sG[r + j];
-      return fmin(fmax(log2(fabs(x)), -4096.0), 4096.0);
+    constexpr double kDead = -1.0e9;    // exponent of a zeroed product
+    auto split = [](double x, double &mm, double &ee) {  // |x| = mm 2^ee, mm in [1, 2)
+      const long long b = __double_as_longlong(x) & 0x7fffffffffffffffLL;
+      const int ex = (int)(b >> 52);
+      const bool ok = ex > 0 && ex < 2047;  // normal and finite
+      mm = ok ? __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL) : 1.0;
+      ee = ok ? (double)(ex - 1023) : kDead;
     };
-    double run = 0.0;
-#pragma unroll 8
-    for (int j = j0; j < j1; ++j) run += lval(j);
-    double incl = run;
-    for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    double acc = incl - run;  // exclusive prefix of this lane's run
+    auto mul = [](double &mm, double &ee, double m2, double e2) {
+      mm *= m2; ee += e2;
+      if (mm >= 2.0) { mm *= 0.5; ee += 1.0; }
+    };
+    auto lval = [&](int j, double &mm, double &ee) { split(up ? sR[r - 1 - j] : sG[r + j], mm, ee); };
+    double pm = 1.0, pe = 0.0;
 #pragma unroll 8
     for (int j = j0; j < j1; ++j) {
-      acc += lval(j);
-      if (up) z[r - 1 - j] = exp2(acc);
-      else z[r + j + 1] = exp2(acc);
+      double a, b;
+      lval(j, a, b);
+      mul(pm, pe, a, b);
+    }
+    double im = pm, ie = pe;  // inclusive scan over the lanes
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ym = __shfl_up_sync(0xffffffffu, im, o), ye = __shfl_up_sync(0xffffffffu, ie, o);
+      if (lane >= o) mul(im, ie, ym, ye);
+    }
+    double am = __shfl_up_sync(0xffffffffu, im, 1), ae = __shfl_up_sync(0xffffffffu, ie, 1);
+    if (lane == 0) { am = 1.0; ae = 0.0; }  // exclusive prefix of this lane's run
+#pragma unroll 8
+    for (int j = j0; j < j1; ++j) {
+      double a, b;
+      lval(j, a, b);
+      mul(am, ae, a, b);
+      const double zz = ae < -1100.0 ? 0.0 : (ae > 1100.0 ? CUDART_INF : ldexp(am, (int)ae));
+      if (up) z[r - 1 - j] = zz;
+      else z[r + j + 1] = zz;
     }
   }
   __syncthreads();
 
+  __syncthreads();
+  if (tid == 0) atomicMax(&A.ctr[5], (unsigned long long)(clock64() - clk_p1));
+  const long long clk_p2 = clock64();
   // ---- phase 3: growth of the candidates, raw and weighted (all threads)
   double g[6], nl[6], nr[6], dnl = 0.0, dnr = 0.0;
   unsigned okm = 0x3f;
@@ -348,6 +375,7 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
 
   // ---- phase 4: the tiered choice (reading 9) by thread 0
   if (tid == 0) {
+    atomicMax(&A.ctr[6], (unsigned long long)(clock64() - clk_p2));
     double G[6], NL[6], NR[6], DNL = 0.0, DNR = 0.0;
     unsigned ok = 0x3f;
     for (int k = 0; k < 6; ++k) { G[k] = 0.0; NL[k] = 0.0; NR[k] = 0.0; }

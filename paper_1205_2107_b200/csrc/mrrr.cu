@@ -1537,6 +1537,9 @@ int solve(Problem &P, int64_t *m_out) {
     fprintf(stderr, "[mrrr] probes %llu; nudged vector factorizations %llu (why %llu); slowest vector warp: "
             "cycles full %llu rqc %llu solve %llu, max factorizations per warp %llu\n",
             h_ctr[16], h_ctr[10], h_ctr[11], h_ctr[12], h_ctr[13], h_ctr[14], h_ctr[15]);
+  if (tr.on)
+    fprintf(stderr, "[mrrr] child step max cycles: candidates %llu, probe bwd %llu, probe fwd %llu; "
+            "twist+scan %llu; growth %llu\n", h_ctr[18], h_ctr[19], h_ctr[20], h_ctr[21], h_ctr[22]);
   tr.mark("vectors");
   g_stats.ms_vectors = tv.stop();
   g_stats.root_sweeps += h_ctr[0];

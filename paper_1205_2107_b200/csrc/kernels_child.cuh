@@ -118,8 +118,8 @@ __device__ __forceinline__ void cs_probe_fwd(ChainRing &R, const double2 *DL, co
     }
     if (lane < rows) {
       const int i = r0 + lane;
-      sS[i] = kp / kq;
-      if (i < nb - 1) sR[i] = -kld * (kq / kt);
+      sS[i] = div_nr(kp, kq);  // probe ratios: weights only
+      if (i < nb - 1) sR[i] = -kld * div_nr(kq, kt);
     }
     __syncwarp();
     const int cn = c + kCRing - 1;
@@ -162,8 +162,8 @@ __device__ __forceinline__ void cs_probe_bwd(ChainRing &R, const double2 *DL, co
     }
     if (lane <= top - r0) {
       const int i = r0 + lane;
-      sP[i] = ka / ku;
-      sG[i] = -kld * (kb / ku);
+      sP[i] = div_nr(ka, ku);
+      sG[i] = -kld * div_nr(kb, ku);
     }
     __syncwarp();
     const int cn = c + kCRing - 1;
@@ -206,7 +206,7 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
 #pragma unroll
     for (int e = lane; e < 6 * kCT; e += 32) {
       const int cc = e >> 4, k = e & (kCT - 1);
-      if (k < rows) DP[cc * zstride + r0 + k] = S.tq[0][cc][k] / S.tq[1][cc][k];
+      if (k < rows) DP[cc * zstride + r0 + k] = div_nr(S.tq[0][cc][k], S.tq[1][cc][k]);
     }
     __syncwarp();
     const int cn = c + kCRing - 1;

@@ -44,7 +44,7 @@ struct ChainRing {
 
 struct ChildSmem {
   ChainRing ring[kCSWarps];
-  double tq[2][6][kCT];      // candidate tile: t_i, q_i per candidate
+  double tq[2][kCT][8];      // candidate tile: t_i, q_i per row and candidate (conflict-free writes)
   double red[kCSWarps][20];  // per-warp partials of the growth reductions
   unsigned okw[kCSWarps];    // per-warp finiteness masks of the candidates
   double sig[6];             // the candidates' shifts
@@ -188,7 +188,7 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
       const int i = r0 + k;
       const double2 v = R.rDL[slot][k];
       const double tt = fma(v.x, q, p);
-      if (lane < 6) { S.tq[0][lane][k] = tt; S.tq[1][lane][k] = q; }
+      if (lane < 6) { S.tq[0][k][lane] = tt; S.tq[1][k][lane] = q; }
       if (i < nb - 1) { p = fma(-sigma, tt, v.y * p); q = tt; }
       if ((k & 7) == 7) {
         const double f = pow2_scale(min(max(max_exp(p, q), 1), 2045));
@@ -206,7 +206,7 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
 #pragma unroll
     for (int e = lane; e < 6 * kCT; e += 32) {
       const int cc = e >> 4, k = e & (kCT - 1);
-      if (k < rows) DP[cc * zstride + r0 + k] = div_nr(S.tq[0][cc][k], S.tq[1][cc][k]);
+      if (k < rows) DP[cc * zstride + r0 + k] = div_nr(S.tq[0][k][cc], S.tq[1][k][cc]);
     }
     __syncwarp();
     const int cn = c + kCRing - 1;

@@ -101,6 +101,29 @@ __device__ __forceinline__ int warp_min(int v) {
   return v;
 }
 
+// The forward state before row r and the backward state at row r, replayed
+// from the checkpoints of r's segment (forward: rows c*kTR .. r-1; backward:
+// rows top-1 .. r from the state at the segment's top) -- the operations the
+// sweeps did, so the values equal the sweeps' at r.
+__device__ __forceinline__ void w_states_at(const WarpCtx &W, double lam, int r, Fwd &Fr, Bwd &Br) {
+  const int nb = W.nb;
+  const int cr = r / kTR, top = min(cr * kTR + kTR, nb - 1);
+  const FwdCk fk = W.fck[(int64_t)cr * W.ck_stride + W.tix];
+  const BwdCk bk = W.bck[(int64_t)cr * W.ck_stride + W.tix];
+  Fr = Fwd{fk.p, fk.q, fk.H, fk.neg};
+  for (int i = cr * kTR; i < r; ++i) {
+    const double2 dl = __ldg(&W.DL[i]), lv = __ldg(&W.LDv[i]);
+    Row R; R.D = dl.x; R.LLD = dl.y; R.LD = lv.x; R.LD2 = lv.y;
+    Fr.step_r(R, lam, (i & 7) == 7);
+  }
+  Br = Bwd{bk.a, bk.b, bk.K, bk.neg};
+  for (int i = top - 1; i >= r; --i) {
+    const double2 dl = __ldg(&W.DL[i]), lv = __ldg(&W.LDv[i]);
+    Row R; R.D = dl.x; R.LLD = dl.y; R.LD = lv.x; R.LD2 = lv.y;
+    Br.step_r(R, lam, (i & 7) == 0);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // PAIR execution.  A CTA holds one work item (up to 32 eigenpairs of one node)
 // and two warps: warp F (role 0) runs every stationary (top-down) sweep and
@@ -124,8 +147,8 @@ __device__ __forceinline__ void put_bck(const WarpCtx &W, int c, const Bwd &B) {
 // cross-multiplication; among equal values the lowest row (the full search
 // scans downward and keeps a later row on ties).
 struct TwistPart {
-  double N, den, H, q, K, b;
-  int r, neg, have;
+  double N, den;
+  int r, have;
 };
 
 // Per-CTA exchange between the two warps (per lane).
@@ -133,8 +156,8 @@ struct PairX {
   double fp[32], fq[32], fH[32];
   double ba[32], bb[32], bK[32];
   int fneg[32], bneg[32], ok[2][32];
-  double eN[2][32], eden[2][32], eH[2][32], eq[2][32], eK[2][32], eb[2][32];
-  int er[2][32], eneg[2][32], ehave[2][32];
+  double eN[2][32], eden[2][32];
+  int er[2][32], ehave[2][32];
 };
 
 // Twist search over segments c = chi .. clo (descending), replaying the
@@ -145,7 +168,7 @@ __device__ __forceinline__ TwistPart w_eval_segments(const WarpCtx &W, double la
   const int nb = W.nb, L = W.lane;
   WarpSmem &S = *W.sm;
   TwistPart T;
-  T.N = 0; T.den = 0; T.H = 0; T.q = 1; T.K = 0; T.b = 1; T.r = nb - 1; T.neg = 0; T.have = 0;
+  T.N = 0; T.den = 0; T.r = nb - 1; T.have = 0;
   if (chi < clo) return T;
   FwdCk ckn = W.fck[(int64_t)chi * W.ck_stride + W.tix];
   BwdCk bkn = W.bck[(int64_t)chi * W.ck_stride + W.tix];
@@ -160,31 +183,23 @@ __device__ __forceinline__ TwistPart w_eval_segments(const WarpCtx &W, double la
     }
     Fwd G{ck.p, ck.q, ck.H, 0};
     Bwd B{bk.a, bk.b, bk.K, bk.neg};
-    unsigned mask = 0;
+    // only (N, den, r) are tracked; the rest is recomputed at r (w_states_at)
     auto eval = [&](int k) {
-      const double fpi = S.sA[k][L], fqi = S.sB[k][L], fHi = S.sC[k][L];
+      const double fpi = S.sA[k][L], fqi = S.sB[k][L];
       const double qb = fqi * B.b;
       const double N = fma(fpi, B.b, fma(B.a, fqi, lam * qb));
       const bool better = (!have || (fabs(N) * fabs(T.den) <= fabs(T.N) * fabs(qb))) && qb != 0.0 &&
                           isfinite(N);
-      const int negk = ck.neg + __popc(mask & ((1u << k) - 1u)) + B.neg;
       have |= better;
       T.r = better ? r0 + k : T.r;
       T.N = better ? N : T.N;
       T.den = better ? qb : T.den;
-      T.H = better ? fHi : T.H;
-      T.q = better ? fqi : T.q;
-      T.K = better ? B.K : T.K;
-      T.b = better ? B.b : T.b;
-      T.neg = better ? negk : T.neg;
     };
     if (r1 < nb) {  // full segment, rows r0 .. r0+15 all below nb-1
 #pragma unroll 8
       for (int k = 0; k < kTR; ++k) {
-        S.sA[k][L] = G.p; S.sB[k][L] = G.q; S.sC[k][L] = G.H;
-        const int before = G.neg;
+        S.sA[k][L] = G.p; S.sB[k][L] = G.q;
         G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
-        mask |= (unsigned)(G.neg - before) << k;
       }
 #pragma unroll 8
       for (int k = kTR - 1; k >= 0; --k) {
@@ -194,12 +209,8 @@ __device__ __forceinline__ TwistPart w_eval_segments(const WarpCtx &W, double la
     } else {  // the top segment: rows r0 .. nb-1
       const int nr = r1 - r0;
       for (int k = 0; k < nr; ++k) {
-        S.sA[k][L] = G.p; S.sB[k][L] = G.q; S.sC[k][L] = G.H;
-        if (k < nr - 1) {
-          const int before = G.neg;
-          G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
-          mask |= (unsigned)(G.neg - before) << k;
-        }
+        S.sA[k][L] = G.p; S.sB[k][L] = G.q;
+        if (k < nr - 1) G.step_r(w_row(W, slot, k), lam, (k & 7) == 7);
       }
       eval(nr - 1);
       for (int k = nr - 2; k >= 0; --k) {
@@ -253,21 +264,22 @@ __device__ __forceinline__ Twist w_full_pair(const WarpCtx &W, double lam, int r
   // twist search: F takes the lower half of the segments, B the upper half
   const int h = W.nseg / 2;
   const TwistPart T = role == 0 ? w_eval_segments(W, lam, h - 1, 0) : w_eval_segments(W, lam, W.nseg - 1, h);
-  X.eN[role][L] = T.N; X.eden[role][L] = T.den; X.eH[role][L] = T.H; X.eq[role][L] = T.q;
-  X.eK[role][L] = T.K; X.eb[role][L] = T.b; X.er[role][L] = T.r; X.eneg[role][L] = T.neg;
+  X.eN[role][L] = T.N; X.eden[role][L] = T.den; X.er[role][L] = T.r;
   X.ehave[role][L] = T.have; X.ok[role][L] = ok;
   __syncthreads();
   // combine: the lower half wins ties (it comes later in the downward scan)
   const bool h0 = X.ehave[0][L], h1 = X.ehave[1][L];
   const bool low = h0 && (!h1 || fabs(X.eN[0][L]) * fabs(X.eden[1][L]) <= fabs(X.eN[1][L]) * fabs(X.eden[0][L]));
   const int s = low ? 0 : 1;
-  const double bN = X.eN[s][L], bden = X.eden[s][L], bH = X.eH[s][L], bq = X.eq[s][L];
-  const double bK = X.eK[s][L], bb = X.eb[s][L];
+  const double bN = X.eN[s][L], bden = X.eden[s][L];
   Twist tw;
   tw.r = X.er[s][L];
+  Fwd Fr;
+  Bwd Br;
+  w_states_at(W, lam, tw.r, Fr, Br);  // both warps: the same values
   tw.gamma = bN / bden;
-  tw.nrm2 = 1.0 + bH / (bq * bq) + bK / (bb * bb);
-  tw.negc = X.eneg[s][L] + ((tw.gamma < 0.0) ? 1 : 0);
+  tw.nrm2 = 1.0 + Fr.H / (Fr.q * Fr.q) + Br.K / (Br.b * Br.b);
+  tw.negc = Fr.neg + Br.neg + ((tw.gamma < 0.0) ? 1 : 0);
   tw.ok = X.ok[0][L] && X.ok[1][L] && (h0 || h1) && isfinite(tw.gamma) && isfinite(tw.nrm2);
   __syncthreads();  // X is reused by the next exchange
   return tw;
@@ -462,25 +474,10 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
     return false;
   });
   ok &= isfinite(B.a) && isfinite(B.b) && have;
-  // the states at r by replay: forward from the checkpoint of r's segment
-  // (rows c*kTR .. r-1), backward from the checkpoint at the segment's top
-  // (rows top-1 .. r) -- the same operations the sweeps did, so the values
-  // equal those the search saw at r
-  const int cr = best_r / kTR, top = min(cr * kTR + kTR, nb - 1);
-  const FwdCk fk = W.fck[(int64_t)cr * W.ck_stride + W.tix];
-  const BwdCk bk = W.bck[(int64_t)cr * W.ck_stride + W.tix];
-  Fwd Fr{fk.p, fk.q, fk.H, fk.neg};
-  for (int i = cr * kTR; i < best_r; ++i) {
-    const double2 dl = __ldg(&W.DL[i]), lv = __ldg(&W.LDv[i]);
-    Row R; R.D = dl.x; R.LLD = dl.y; R.LD = lv.x; R.LD2 = lv.y;
-    Fr.step_r(R, lam, (i & 7) == 7);
-  }
-  Bwd Br{bk.a, bk.b, bk.K, bk.neg};
-  for (int i = top - 1; i >= best_r; --i) {
-    const double2 dl = __ldg(&W.DL[i]), lv = __ldg(&W.LDv[i]);
-    Row R; R.D = dl.x; R.LLD = dl.y; R.LD = lv.x; R.LD2 = lv.y;
-    Br.step_r(R, lam, (i & 7) == 0);
-  }
+  // the partial norms and negcounts at r from the checkpoints
+  Fwd Fr;
+  Bwd Br;
+  w_states_at(W, lam, best_r, Fr, Br);
   Twist tw;
   tw.r = best_r;
   tw.gamma = bN / bden;

@@ -994,7 +994,7 @@ int solve(Problem &P, int64_t *m_out) {
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }
-      make_work(B.root_node, B.slot0, B.slot1, rw_chunk(B.nb), wv);  // rank-invariant (block size)
+      make_work(B.root_node, B.slot0, B.slot1, env_int("MRRR_RW_ROOT_CHUNK", 0) > 0 ? std::min(env_int("MRRR_RW_ROOT_CHUNK", 0), kRWMembers) : rw_chunk(B.nb), wv);  // rank-invariant (block size)
     }
     Work *dwork = ar.alloc<Work>(wv.size());
     h2d(dwork, wv.data(), wv.size(), s);

@@ -98,23 +98,23 @@ __device__ __forceinline__ void cs_probe_fwd(ChainRing &R, const double2 *DL, co
     __syncwarp();
     const int slot = c % kCRing, r0 = c * kCT, rows = min(kCT, nb - r0);
     double kp = 0.0, kq = 1.0, kt = 1.0, kld = 0.0;
-    auto row = [&](int k) {
+    auto row = [&](int k, bool last_check) {
       const int i = r0 + k;
       const double2 v = R.rDL[slot][k];
       const double ld = R.rLD[slot][k].x;
       const double tt = fma(v.x, q, p);
       if (lane == k) { kp = p; kq = q; kt = tt; kld = ld; }
-      if (i < nb - 1) { p = fma(-lam, tt, v.y * p); q = tt; }
+      if (!last_check || i < nb - 1) { p = fma(-lam, tt, v.y * p); q = tt; }
       if ((k & 7) == 7) {
         const double f = pow2_scale(min(max(max_exp(p, q), 1), 2045));
         p *= f; q *= f;
       }
     };
-    if (rows == kCT) {
+    if (rows == kCT && r0 + kCT < nb) {  // every row of the tile is below nb - 1
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) row(k);
+      for (int k = 0; k < kCT; ++k) row(k, false);
     } else {
-      for (int k = 0; k < rows; ++k) row(k);
+      for (int k = 0; k < rows; ++k) row(k, true);
     }
     if (lane < rows) {
       const int i = r0 + lane;
@@ -184,22 +184,22 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
     __pipeline_wait_prior(kCRing - 2);
     __syncwarp();
     const int slot = c % kCRing, r0 = c * kCT, rows = min(kCT, nb - r0);
-    auto row = [&](int k) {
+    auto row = [&](int k, bool last_check) {
       const int i = r0 + k;
       const double2 v = R.rDL[slot][k];
       const double tt = fma(v.x, q, p);
       if (lane < 6) { S.tq[0][k][lane] = tt; S.tq[1][k][lane] = q; }
-      if (i < nb - 1) { p = fma(-sigma, tt, v.y * p); q = tt; }
+      if (!last_check || i < nb - 1) { p = fma(-sigma, tt, v.y * p); q = tt; }
       if ((k & 7) == 7) {
         const double f = pow2_scale(min(max(max_exp(p, q), 1), 2045));
         p *= f; q *= f;
       }
     };
-    if (rows == kCT) {
+    if (rows == kCT && r0 + kCT < nb) {  // every row of the tile is below nb - 1
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) row(k);
+      for (int k = 0; k < kCT; ++k) row(k, false);
     } else {
-      for (int k = 0; k < rows; ++k) row(k);
+      for (int k = 0; k < rows; ++k) row(k, true);
     }
     __syncwarp();
     // D+_i = t_i / q_i, 96 divisions spread over the warp (off the chains)

@@ -192,6 +192,11 @@ class _DevBuf:
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
+def _ext_stream(handle):
+    """torch stream object for a raw cudaStream_t handle (0/None: the legacy default stream)."""
+    return torch.cuda.ExternalStream(handle) if handle else torch.cuda.default_stream()
+
+
 def _host_view(ptr: int, nbytes: int):
     arr = (C.c_double * (nbytes // 8)).from_address(ptr)
     return torch.frombuffer(arr, dtype=torch.float64)
@@ -211,9 +216,13 @@ def torch_allgather(group=None, device: str = "cuda"):
                 return 0
             world = dist.get_world_size(group)
             if device == "cuda":
-                st = torch.as_tensor(_DevBuf(send, nbytes), device="cuda")
-                rt = torch.as_tensor(_DevBuf(recv, nbytes * world), device="cuda")
-                dist.all_gather_into_tensor(rt, st, group=group)
+                # enqueued on the library's stream (the callback's contract,
+                # include/mrrr.h): ordered after the kernels that wrote `send`
+                # and before the library's reads of `recv`
+                with torch.cuda.stream(_ext_stream(stream)):
+                    st = torch.as_tensor(_DevBuf(send, nbytes), device="cuda")
+                    rt = torch.as_tensor(_DevBuf(recv, nbytes * world), device="cuda")
+                    dist.all_gather_into_tensor(rt, st, group=group)
             else:
                 st = _host_view(send, nbytes)
                 parts = [torch.empty_like(st) for _ in range(world)]

@@ -33,10 +33,11 @@ def local_allgather(rank, nranks=1):
     from paper_1205_2107_b200 import mrrr as M
 
     def fn(ctx, send, recv, nbytes, stream):
-        st = torch.as_tensor(M._DevBuf(send, nbytes), device="cuda")
-        allr = torch.as_tensor(M._DevBuf(recv, nbytes * nranks), device="cuda")
-        allr.fill_(float("-inf"))
-        allr[rank * (nbytes // 8):(rank + 1) * (nbytes // 8)].copy_(st)
+        with torch.cuda.stream(M._ext_stream(stream)):  # on the library's stream
+            st = torch.as_tensor(M._DevBuf(send, nbytes), device="cuda")
+            allr = torch.as_tensor(M._DevBuf(recv, nbytes * nranks), device="cuda")
+            allr.fill_(float("-inf"))
+            allr[rank * (nbytes // 8):(rank + 1) * (nbytes // 8)].copy_(st)
         return 0
     return M.ALLGATHER_FN(fn)
 

@@ -983,8 +983,9 @@ int solve(Problem &P, int64_t *m_out) {
     for (int r = 0; r < nroot; ++r) {
       const Block &B = hb[root_blocks[r]];
       int nsl = B.slot1 - B.slot0;
-      if (nroot == 1 && P.o.grid_factor > 0 && nsl >= 64) {
-        int G = (int)std::min<int64_t>((int64_t)P.o.grid_factor * nsl + 1, 1 << 20);
+      const int gf = env_int("MRRR_GRID_FACTOR", P.o.grid_factor);  // diagnostic override
+      if (nroot == 1 && gf > 0 && nsl >= 64) {
+        int G = (int)std::min<int64_t>((int64_t)gf * nsl + 1, 1 << 20);
         G = std::max(G, 256);
         int *cnt = ar.alloc<int>(G + 1);
         launch_grid(4, dnodes, B.root_node, hlo0[r], hhi0[r], G, cnt, ctr + 1, s);

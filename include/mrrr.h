@@ -156,6 +156,29 @@ size_t mrrr_workspace_bytes(int64_t n, int64_t k);
  * Returns 0 or MRRR_ERR_CUDA. */
 int mrrr_trim_workspace(void);
 
+/*
+ * mrrr_negcount -- diagnostic entry: the Sturm count the bisection kernels
+ * compute, N(mu) = #eigenvalues of L D L^T less than mu (PAPER.md L1061-1067
+ * "bisection"), for a caller-given representation, one count
+ * per shift.  Used by the -m gpu tests to compare the GPU counts with the
+ * oracle's bit for bit.
+ *  (1) nb     order of the representation, 1 <= nb <= 2^30.
+ *  (2) D      device, D[nb] (pivots).
+ *  (3) LLD    device, LLD[nb-1] = L_i^2 D_i (may be NULL if nb == 1).
+ *  (4) k      number of shifts, k >= 0.
+ *  (5) mu     device, mu[k].
+ *  (6) count  device out, count[k] (int64).
+ *  (7) mode   0: the kernels' division-free projective sweep
+ *             with its qd fallback when the sweep over/underflows; 1: the qd
+ *             fallback alone (differential stationary qd, a zero pivot's NaN
+ *             ratio replaced by its limit 1, reading 5).
+ *  (8) stream cudaStream_t (as void*); the call synchronises it.
+ * Returns 0, -i for an invalid argument i, 5 (CUDA) or 6 (out of memory).
+ * Allocates nb * 16 bytes of stream-ordered scratch, freed before return.
+ */
+int mrrr_negcount(int64_t nb, const double *D, const double *LLD, int64_t k,
+                  const double *mu, int64_t *count, int mode, void *stream);
+
 /* Static description of a return code. */
 const char *mrrr_strerror(int code);
 
@@ -185,6 +208,8 @@ typedef struct {
   int64_t vec_tasks;        /* eigenvectors computed by that kernel */
   int64_t vec_elems;        /* sum over those tasks of their block order */
   double ms_k_final_refine; /* RQC fallback: bracket refinement to 4 eps (0 without fallback) */
+  int64_t vec_nudges;       /* vector factorizations redone at a nudged shift (reading 25) */
+  int64_t vec_items;        /* warp work items of the vector kernels (lanes: vec_tasks) */
 } mrrr_stats_t;
 int mrrr_get_stats(mrrr_stats_t *out);
 

@@ -190,13 +190,18 @@ def root_rrr(d, e, side=1, perturb=0, seed=0):
     return D, L[: n - 1].copy(), s.value
 
 
-def negcount(D, L, mu):
-    D, L = _f64(D), _f64(L)
-    LLD = L * L * D[:-1] if len(L) else np.zeros(1)
-    LLD = _f64(LLD)
-    piv = np.finfo(float).tiny * max(1.0, float(np.max(np.abs(LLD))) if len(L) else 1.0)
+def negcount(D, L, mu, LLD=None, return_resweep=False):
+    """O6 count N(mu) of L D L^T; LLD may be given directly (then L is unused).
+    With return_resweep, also whether the NaN-safe re-sweep ran (a zero pivot)."""
+    D = _f64(D)
+    if LLD is None:
+        L = _f64(L)
+        LLD = L * L * D[:-1] if len(L) else np.zeros(1)
+    LLD = _f64(LLD) if len(LLD) else np.zeros(1)
+    piv = np.finfo(float).tiny * max(1.0, float(np.max(np.abs(LLD))))
     rs = C.c_int(0)
-    return lib().oracle_negcount(D.shape[0], _p(D), _p(LLD), float(mu), piv, C.byref(rs))
+    c = lib().oracle_negcount(D.shape[0], _p(D), _p(LLD), float(mu), piv, C.byref(rs))
+    return (c, bool(rs.value)) if return_resweep else c
 
 
 def sturm_T(d, e, x):

@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(128) k_grid(const Node *nodes, int node, doubl
     int g = g0 + c;
     if (g < G) {
       unsigned v = k[c];
-      if (!ok) { atomicAdd(safe_ctr, 1ull); v = negcount_qd_safe(N.DL, N.nb, mu[c]); }
+      if (!ok || g_force_safe) { atomicAdd(safe_ctr, 1ull); v = negcount_qd_safe(N.DL, N.nb, mu[c]); }
       cnt[g] = (int)v;
     }
   }
@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
     const double Dl = __ldg(&N.DL[nb - 1]).x;
 #pragma unroll
     for (int c = 0; c < M; ++c) { sturm_last(st[c], Dl); ok &= sturm_ok(st[c]); }
-    if (any && !ok) {
+    if (any && (!ok || g_force_safe)) {
       atomicAdd(safe_ctr, 1ull);
 #pragma unroll
       for (int c = 0; c < M; ++c) st[c].c = negcount_qd_safe(N.DL, nb, mu[c]);

@@ -24,16 +24,27 @@ constexpr int kTR = 16;          // rows per tile (= checkpoint segment)
 constexpr int kRing = 6;         // tiles in flight per warp
 static_assert(kTR == kSeg, "tiles and checkpoint segments coincide");
 
+// A work item may hold the eigenpairs of up to kMaxSeg nodes ("segments") of
+// one block: the nodes of a block share the row count, the first row and the
+// (LD, LD^2) rows (LD is invariant under the stationary transform), and
+// differ only in (D, LLD).  Packing the singletons of several small nodes
+// into one warp keeps the lanes busy: deep tree levels deliver a few
+// singletons per node, and one node per warp left ~79 % of the lanes idle at
+// n = 20000 (3000 items for 20000 eigenpairs).
+constexpr int kMaxSeg = 8;
+
 // Shared memory of one warp.
 struct WarpSmem {
-  double2 rDL[kRing][kTR];  // (D, LLD) rows
-  double2 rLD[kRing][kTR];  // (LD, LD^2) rows
+  double2 rDL[kRing][kTR][kMaxSeg];  // (D, LLD) rows of each segment's node
+  double2 rLD[kRing][kTR];           // (LD, LD^2) rows (shared by the block's nodes)
   double sA[kTR][32], sB[kTR][32], sC[kTR][32];  // per-lane segment stores (z goes to sA)
+  const double2 *segDL[kMaxSeg];     // (D, LLD) array of each segment's node
 };
 
 struct WarpCtx {
-  const double2 *DL, *LDv;
+  const double2 *DL, *LDv;  // DL: this lane's node
   int nb, nseg, lane;
+  int seg, nsegs;           // this lane's segment; segments of the item
   WarpSmem *sm;
   FwdCk *fck;
   BwdCk *bck;
@@ -41,14 +52,33 @@ struct WarpCtx {
 };
 
 __device__ __forceinline__ void w_issue(const WarpCtx &W, int c, int slot) {
-  // lanes 0..15 copy the (D, LLD) rows, lanes 16..31 the (LD, LD^2) rows
-  const int k = W.lane & (kTR - 1);
-  const int row = c * kTR + k;
-  if (c >= 0 && c < W.nseg && row < W.nb) {
-    if (W.lane < kTR) __pipeline_memcpy_async(&W.sm->rDL[slot][k], &W.DL[row], sizeof(double2));
-    else __pipeline_memcpy_async(&W.sm->rLD[slot][k], &W.LDv[row], sizeof(double2));
+  // copies 16 (D, LLD) rows per segment, then the 16 (LD, LD^2) rows; one
+  // segment: lanes 0..15 the former, 16..31 the latter (one copy per lane)
+  if (c >= 0 && c < W.nseg) {
+    const int ncopy = (W.nsegs + 1) * kTR;
+    for (int idx = W.lane; idx < ncopy; idx += 32) {
+      const int sg = idx / kTR, k = idx - sg * kTR;
+      const int row = c * kTR + k;
+      if (row < W.nb) {
+        if (sg < W.nsegs) __pipeline_memcpy_async(&W.sm->rDL[slot][k][sg], &W.sm->segDL[sg][row], sizeof(double2));
+        else __pipeline_memcpy_async(&W.sm->rLD[slot][k], &W.LDv[row], sizeof(double2));
+      }
+    }
   }
   __pipeline_commit();
+}
+
+// Segment structure of an item: lanes whose tasks (in position order t0 ..
+// t1-1) share a node form a segment; idle lanes join the last one.  The
+// first lane of each segment publishes its node's (D, LLD) array.
+__device__ __forceinline__ void w_segments(WarpCtx &W, int node_at_pos, bool active) {
+  const int prev = __shfl_up_sync(0xffffffffu, node_at_pos, 1);
+  const bool first = W.lane == 0 || (active && node_at_pos != prev);
+  const unsigned b = __ballot_sync(0xffffffffu, first);
+  W.seg = __popc(b & (0xffffffffu >> (31 - W.lane))) - 1;
+  W.nsegs = __popc(b);
+  if (first) W.sm->segDL[W.seg] = W.DL;
+  __syncwarp();
 }
 
 // f(c, slot) for tiles c = c0 .. c1 (ascending, warp-uniform bounds); tile c
@@ -87,7 +117,7 @@ __device__ __forceinline__ void w_tiles_down(const WarpCtx &W, int c1, int c0, F
 }
 
 __device__ __forceinline__ Row w_row(const WarpCtx &W, int slot, int k) {
-  const double2 a = W.sm->rDL[slot][k], b = W.sm->rLD[slot][k];
+  const double2 a = W.sm->rDL[slot][k][W.seg], b = W.sm->rLD[slot][k];
   Row r; r.D = a.x; r.LLD = a.y; r.LD = b.x; r.LD2 = b.y;
   return r;
 }
@@ -568,34 +598,45 @@ __device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int
   return tw;
 }
 
-// z pass of every active lane: z_r = 1, written as scale * z to col[0 .. nb).
-// The ratios q_i / t_i (left) and b_{i+1} / u_{i+1} (right) are formed during
-// the replay with correctly rounded reciprocals (off the z recurrence), so
-// the z loops are pure multiply chains.
-__device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int r, double scale, double *col,
-                                              bool active) {
-  const int nb = W.nb, L = W.lane;
+// z pass of every active lane: z_r = 1, written as scale * z to col[0 .. nb),
+// DIVISION-FREE ("projective z").  Left of r the solve is
+// z_i = -LD_i (q_i / t_i) z_{i+1}; the replay stores q_{i+1} = t_i f_i (f_i
+// the exact power-of-two rescale applied after row i, 1 elsewhere), so with
+// y_i = z_i / q_i:   y_i = -LD_i f_i y_{i+1},  z_i = y_i q_i,  y_r = 1 / q_r.
+// Right of r, z_{i+1} = -LD_i (b_{i+1} / u_{i+1}) z_i with b_i = u_{i+1} f_i,
+// so with v_i = z_i / b_i:   v_{i+1} = -LD_i f_i v_i,  z_{i+1} = v_{i+1} b_{i+1},
+// v_r = 1 / b_r.  Two multiplications per row, no reciprocal, and a zero
+// pivot (t_i = 0, so q_{i+1} = 0) needs no special case: z_{i+1} = 0 and
+// z_i = -(LD_{i+1} / LD_i) z_{i+2} follow from the recurrences (the
+// zero-component rule of O10 step 4, reached without evaluating it).
+__device__ __forceinline__ void w_solve_left(const WarpCtx &W, double lam, int r, double scale, double *col,
+                                             bool active) {
+  const int L = W.lane;
   WarpSmem &S = *W.sm;
   if (active) col[r] = scale;
-  // ---- left part, rows i < r, descending: z_i = -LD_i (q_i / t_i) z_{i+1}
+  // rows i < r, descending segments
   const int clast = (active && r > 0) ? (r - 1) / kTR : -1;
   const int cmax = warp_max(clast);
-  double z1 = 1.0, z2 = 0.0, ldn = (active && r > 0) ? __ldg(&W.LDv[r]).x : 0.0;
+  double y = 0.0;
   FwdCk ckn = W.fck[(int64_t)max(min(clast, cmax), 0) * W.ck_stride + W.tix];
   w_tiles_down(W, cmax, 0, [&](int c, int slot) {
     const bool on = c <= clast;
     const int r0 = c * kTR, r1 = on ? min(r0 + kTR, r) : r0;  // rows [r0, r1)
     const FwdCk ck = ckn;
     if (on && c > 0) ckn = W.fck[(int64_t)(c - 1) * W.ck_stride + W.tix];
-    Fwd G{ck.p, ck.q, 0.0, 0};
-    auto rep = [&](int k) {
+    double p = ck.p, q = ck.q;
+    auto rep = [&](int k) {  // state before row r0 + k -> before r0 + k + 1
       const Row R = w_row(W, slot, k);
-      const double t = fma(R.D, G.q, G.p);
-      S.sA[k][L] = -R.LD * (G.q * rcp_nr(t));  // z_i / z_{i+1}
-      S.sC[k][L] = R.LD;
-      G.p = fma(-lam, t, R.LLD * G.p);
-      G.q = t;
-      if ((k & 7) == 7) fwd_rescale(G.p, G.q, G.H);
+      S.sA[k][L] = q;  // q_i
+      const double t = fma(R.D, q, p);
+      p = fma(-lam, t, R.LLD * p);
+      q = t;
+      double f = 1.0;
+      if ((k & 7) == 7) {
+        f = pow2_scale(min(max_exp(p, q), 2045));
+        p *= f; q *= f;
+      }
+      S.sC[k][L] = -R.LD * f;
     };
     if (on && r1 == r0 + kTR) {
 #pragma unroll
@@ -603,17 +644,11 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
     } else if (on) {
       for (int k = 0; k < r1 - r0; ++k) rep(k);
     }
-    // branch-free: the zero-component rule (row i+1 of (LDL^T - lambda I) z
-    // = 0 gives z_i = -(LD_{i+1} / LD_i) z_{i+2}) is evaluated every row and
-    // selected, so no division slow path splits the unrolled block
+    if (on && r1 == r) y = scale / q;  // y_r = z_r / q_r (q_r != 0: the twist's |gamma_r| is finite)
     auto zstep = [&](int k) {
-      const double ld = S.sC[k][L];
-      const double za = S.sA[k][L] * z1;
-      const double zb = -(ldn * rcp_nr(ld)) * z2;
-      double zi = (z1 != 0.0) ? za : zb;
-      zi = (fabs(zi) >= kTiny) ? zi : 0.0;
-      S.sA[k][L] = zi * scale;
-      z2 = z1; z1 = zi; ldn = ld;
+      y *= S.sC[k][L];
+      const double zi = y * S.sA[k][L];
+      S.sA[k][L] = (fabs(zi) >= kTiny) ? zi : 0.0;  // reading 17
     };
     if (r1 - r0 == kTR) {
 #pragma unroll
@@ -624,27 +659,37 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
     w_flush(W, r0, r1 - 1, col);  // chunk rows r0 .. r1-1 from sA[0 ..]
     return false;
   });
-  // ---- right part, rows i > r, ascending: z_{i+1} = -LD_i (b_{i+1} / u_{i+1}) z_i
+}
+
+__device__ __forceinline__ void w_solve_right(const WarpCtx &W, double lam, int r, double scale, double *col,
+                                              bool active) {
+  const int nb = W.nb, L = W.lane;
+  WarpSmem &S = *W.sm;
+  // rows i > r, ascending segments
   const int cfirst = (active && r < nb - 1) ? r / kTR : W.nseg;
   const int cmin = warp_min(cfirst);
-  double y1 = 1.0, y2 = 0.0, ldp = (active && r > 0) ? __ldg(&W.LDv[r - 1]).x : 0.0;
+  double v = 0.0;
   BwdCk bkn = W.bck[(int64_t)min(max(cfirst, cmin), W.nseg - 1) * W.ck_stride + W.tix];
   w_tiles_up(W, cmin, W.nseg - 1, [&](int c, int slot) {
     const bool on = c >= cfirst;
     const int r0 = c * kTR;
-    const int top = min(r0 + kTR, nb - 1);  // checkpoint row
-    const int lo_i = on ? max(r0, r) : top;  // rows i in [lo_i, top) give U-_i
+    const int top = min(r0 + kTR, nb - 1);   // checkpoint row
+    const int lo_i = on ? max(r0, r) : top;  // rows i in [lo_i, top) give z_{i+1}
     const BwdCk bk = bkn;
     if (on && c + 1 < W.nseg) bkn = W.bck[(int64_t)(c + 1) * W.ck_stride + W.tix];
-    Bwd G{bk.a, bk.b, 0.0, 0};
-    auto rep = [&](int k) {
+    double a = bk.a, b = bk.b;
+    auto rep = [&](int k) {  // state at row r0 + k + 1 -> at row r0 + k
       const Row R = w_row(W, slot, k);
-      const double u = fma(R.LLD, G.b, G.a);
-      S.sA[k][L] = -R.LD * (G.b * rcp_nr(u));  // z_{i+1} / z_i
-      S.sC[k][L] = R.LD;
-      G.a = fma(-lam, u, R.D * G.a);
-      G.b = u;
-      if ((k & 7) == 0) bwd_rescale(G.a, G.b, G.K);
+      S.sA[k][L] = b;  // b_{i+1}
+      const double u = fma(R.LLD, b, a);
+      a = fma(-lam, u, R.D * a);
+      b = u;
+      double f = 1.0;
+      if ((k & 7) == 0) {
+        f = pow2_scale(min(max_exp(a, b), 2045));
+        a *= f; b *= f;
+      }
+      S.sC[k][L] = -R.LD * f;
     };
     if (on && lo_i == r0 && top == r0 + kTR) {
 #pragma unroll
@@ -652,16 +697,13 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
     } else if (on) {
       for (int k = top - 1 - r0; k >= lo_i - r0; --k) rep(k);
     }
+    if (on && lo_i == r) v = scale / b;  // v_r = z_r / b_r
     // z_{i+1} for i in [lo_i, top): chunk rows lo_i+1 .. top, stored at sA[i - lo_i]
     // (ascending i: index i - lo_i <= i - r0 was already read)
     auto ystep = [&](int k, int o) {
-      const double ld = S.sC[k][L];
-      const double za = S.sA[k][L] * y1;
-      const double zb = -(ldp * rcp_nr(ld)) * y2;  // row i of (LDL^T - lambda I) z = 0
-      double zn = (y1 != 0.0) ? za : zb;
-      zn = (fabs(zn) >= kTiny) ? zn : 0.0;
-      S.sA[o][L] = zn * scale;
-      y2 = y1; y1 = zn; ldp = ld;
+      v *= S.sC[k][L];
+      const double zn = v * S.sA[k][L];
+      S.sA[o][L] = (fabs(zn) >= kTiny) ? zn : 0.0;
     };
     if (lo_i == r0 && top == r0 + kTR) {
 #pragma unroll
@@ -674,121 +716,24 @@ __device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int 
   });
 }
 
-// z of every active lane, z_r = 1, written as scale * z to col[0 .. nb): F
-// the rows below r (and r itself), B the rows above.  The ratios q_i / t_i
-// (left) and b_{i+1} / u_{i+1} (right) are formed during the replay with
-// correctly rounded reciprocals (off the z recurrence), so the z loops are
-// pure multiply chains.
+__device__ __forceinline__ void w_twist_solve(const WarpCtx &W, double lam, int r, double scale, double *col,
+                                              bool active) {
+  w_solve_left(W, lam, r, scale, col, active);
+  w_solve_right(W, lam, r, scale, col, active);
+}
+
+// The pair's solve: F the rows below r (and r itself), B the rows above.
 __device__ __forceinline__ void w_solve_pair(const WarpCtx &W, double lam, int r, double scale, double *col,
                                              bool active, int role) {
-  const int nb = W.nb, L = W.lane;
-  WarpSmem &S = *W.sm;
-  if (role == 0) {
-    if (active) col[r] = scale;
-    // ---- left part, rows i < r, descending: z_i = -LD_i (q_i / t_i) z_{i+1}
-    const int clast = (active && r > 0) ? (r - 1) / kTR : -1;
-    const int cmax = warp_max(clast);
-    double z1 = 1.0, z2 = 0.0, ldn = (active && r > 0) ? __ldg(&W.LDv[r]).x : 0.0;
-    FwdCk ckn = W.fck[(int64_t)max(min(clast, cmax), 0) * W.ck_stride + W.tix];
-    w_tiles_down(W, cmax, 0, [&](int c, int slot) {
-      const bool on = c <= clast;
-      const int r0 = c * kTR, r1 = on ? min(r0 + kTR, r) : r0;  // rows [r0, r1)
-      const FwdCk ck = ckn;
-      if (on && c > 0) ckn = W.fck[(int64_t)(c - 1) * W.ck_stride + W.tix];
-      Fwd G{ck.p, ck.q, 0.0, 0};
-      auto rep = [&](int k) {
-        const Row R = w_row(W, slot, k);
-        const double t = fma(R.D, G.q, G.p);
-        S.sA[k][L] = -R.LD * (G.q * rcp_nr(t));  // z_i / z_{i+1}
-        S.sC[k][L] = R.LD;
-        G.p = fma(-lam, t, R.LLD * G.p);
-        G.q = t;
-        if ((k & 7) == 7) fwd_rescale(G.p, G.q, G.H);
-      };
-      if (on && r1 == r0 + kTR) {
-#pragma unroll
-        for (int k = 0; k < kTR; ++k) rep(k);
-      } else if (on) {
-        for (int k = 0; k < r1 - r0; ++k) rep(k);
-      }
-      // branch-free: the zero-component rule (row i+1 of (LDL^T - lambda I) z
-      // = 0 gives z_i = -(LD_{i+1} / LD_i) z_{i+2}) is evaluated every row and
-      // selected, so no division slow path splits the unrolled block
-      auto zstep = [&](int k) {
-        const double ld = S.sC[k][L];
-        const double za = S.sA[k][L] * z1;
-        const double zb = -(ldn * rcp_nr(ld)) * z2;
-        double zi = (z1 != 0.0) ? za : zb;
-        zi = (fabs(zi) >= kTiny) ? zi : 0.0;
-        S.sA[k][L] = zi * scale;
-        z2 = z1; z1 = zi; ldn = ld;
-      };
-      if (r1 - r0 == kTR) {
-#pragma unroll
-        for (int k = kTR - 1; k >= 0; --k) zstep(k);
-      } else {
-        for (int k = r1 - r0 - 1; k >= 0; --k) zstep(k);
-      }
-      w_flush(W, r0, r1 - 1, col);  // chunk rows r0 .. r1-1 from sA[0 ..]
-      return false;
-    });
-  } else {
-    // ---- right part, rows i > r, ascending: z_{i+1} = -LD_i (b_{i+1} / u_{i+1}) z_i
-    const int cfirst = (active && r < nb - 1) ? r / kTR : W.nseg;
-    const int cmin = warp_min(cfirst);
-    double y1 = 1.0, y2 = 0.0, ldp = (active && r > 0) ? __ldg(&W.LDv[r - 1]).x : 0.0;
-    BwdCk bkn = W.bck[(int64_t)min(max(cfirst, cmin), W.nseg - 1) * W.ck_stride + W.tix];
-    w_tiles_up(W, cmin, W.nseg - 1, [&](int c, int slot) {
-      const bool on = c >= cfirst;
-      const int r0 = c * kTR;
-      const int top = min(r0 + kTR, nb - 1);  // checkpoint row
-      const int lo_i = on ? max(r0, r) : top;  // rows i in [lo_i, top) give U-_i
-      const BwdCk bk = bkn;
-      if (on && c + 1 < W.nseg) bkn = W.bck[(int64_t)(c + 1) * W.ck_stride + W.tix];
-      Bwd G{bk.a, bk.b, 0.0, 0};
-      auto rep = [&](int k) {
-        const Row R = w_row(W, slot, k);
-        const double u = fma(R.LLD, G.b, G.a);
-        S.sA[k][L] = -R.LD * (G.b * rcp_nr(u));  // z_{i+1} / z_i
-        S.sC[k][L] = R.LD;
-        G.a = fma(-lam, u, R.D * G.a);
-        G.b = u;
-        if ((k & 7) == 0) bwd_rescale(G.a, G.b, G.K);
-      };
-      if (on && lo_i == r0 && top == r0 + kTR) {
-#pragma unroll
-        for (int k = kTR - 1; k >= 0; --k) rep(k);
-      } else if (on) {
-        for (int k = top - 1 - r0; k >= lo_i - r0; --k) rep(k);
-      }
-      // z_{i+1} for i in [lo_i, top): chunk rows lo_i+1 .. top, stored at sA[i - lo_i]
-      // (ascending i: index i - lo_i <= i - r0 was already read)
-      auto ystep = [&](int k, int o) {
-        const double ld = S.sC[k][L];
-        const double za = S.sA[k][L] * y1;
-        const double zb = -(ldp * rcp_nr(ld)) * y2;  // row i of (LDL^T - lambda I) z = 0
-        double zn = (y1 != 0.0) ? za : zb;
-        zn = (fabs(zn) >= kTiny) ? zn : 0.0;
-        S.sA[o][L] = zn * scale;
-        y2 = y1; y1 = zn; ldp = ld;
-      };
-      if (lo_i == r0 && top == r0 + kTR) {
-#pragma unroll
-        for (int k = 0; k < kTR; ++k) ystep(k, k);
-      } else {
-        for (int i = lo_i; i < top; ++i) ystep(i - r0, i - lo_i);
-      }
-      w_flush(W, lo_i + 1, top, col);
-      return false;
-    });
-  }
+  if (role == 0) w_solve_left(W, lam, r, scale, col, active);
+  else w_solve_right(W, lam, r, scale, col, active);
 }
 
 // One work item: up to 32 tasks of one node.
 struct WarpItem {
-  int32_t node;
+  int32_t node;    // node of the first task (the item's tasks may span up to kMaxSeg nodes of one block)
   int32_t t0, t1;  // task ids [t0, t1) (tasks of one node are consecutive)
-  int32_t pad;
+  int32_t nsegs;   // nodes in the item (host bookkeeping)
 };
 
 struct WVecArgs {
@@ -827,14 +772,16 @@ __device__ __forceinline__ void wvec_pair_body(const WVecArgs &A) {
   const int item = blockIdx.x;
   if (item >= A.nitems) return;  // whole CTA
   const WarpItem It = A.items[item];
-  const Node N = A.nodes[It.node];
   const bool active = It.t0 + lane < It.t1;
-  const int tix = A.task_list ? A.task_list[active ? It.t0 + lane : It.t0] : (active ? It.t0 + lane : It.t0);
+  const int pos = active ? It.t0 + lane : It.t1 - 1;  // idle lanes: the item's last task
+  const int tix = A.task_list ? A.task_list[pos] : pos;
   const VecTask tk = A.tasks[tix];
+  const Node N = A.nodes[tk.node];  // this lane's node (the item's nodes share one block)
   WarpCtx W;
   W.DL = N.DL; W.LDv = A.LDv + N.row0; W.nb = N.nb; W.nseg = (N.nb + kTR - 1) / kTR;
   W.lane = lane;
   W.sm = reinterpret_cast<WarpSmem *>(wsm_raw) + role;
+  w_segments(W, A.tasks[pos].node, active);  // position order: nodes unchanged by task_list
   PairX &X = *reinterpret_cast<PairX *>(wsm_raw + 2 * sizeof(WarpSmem));
   W.fck = A.fck; W.bck = A.bck; W.ck_stride = A.ck_stride;
   const int64_t spare = A.ntask + lane;   // idle lanes checkpoint into spare columns
@@ -856,6 +803,7 @@ __device__ __forceinline__ void wvec_pair_body(const WVecArgs &A) {
     for (int tries = 0; tries < 60; ++tries) {
       tw = w_full_pair(W, lam, role, X);
       ++nfact;
+      if (g_force_nudge && tries == 0) tw.ok = false;  // diagnostic (MRRR_FORCE_NUDGE)
       if (!__any_sync(0xffffffffu, active && !tw.ok)) break;
       if (active && !tw.ok) {
         lam = lam_base + nudge; nudge *= 2.0;
@@ -908,7 +856,7 @@ __device__ __forceinline__ void wvec_pair_body(const WVecArgs &A) {
       if (__all_sync(0xffffffffu, conv)) break;
       // later iterations keep the first factorization's twist index
       tw = w_fixed_pair(W, lam, best_r0, !conv, role, X);
-      ++nfact;
+      if (!conv) ++nfact;
       if (!conv && !tw.ok) { conv = true; failed = true; W.tix = spare; }
     }
     const long long clk_rqc = clock64();
@@ -954,14 +902,16 @@ __device__ __forceinline__ void wvec_single_body(const WVecArgs &A) {
   const int item = blockIdx.x * kSingleWarps + wid;
   if (item >= A.nitems) return;  // whole warp
   const WarpItem It = A.items[item];
-  const Node N = A.nodes[It.node];
   const bool active = It.t0 + lane < It.t1;
-  const int tix = A.task_list ? A.task_list[active ? It.t0 + lane : It.t0] : (active ? It.t0 + lane : It.t0);
+  const int pos = active ? It.t0 + lane : It.t1 - 1;  // idle lanes: the item's last task
+  const int tix = A.task_list ? A.task_list[pos] : pos;
   const VecTask tk = A.tasks[tix];
+  const Node N = A.nodes[tk.node];  // this lane's node (the item's nodes share one block)
   WarpCtx W;
   W.DL = N.DL; W.LDv = A.LDv + N.row0; W.nb = N.nb; W.nseg = (N.nb + kTR - 1) / kTR;
   W.lane = lane;
   W.sm = reinterpret_cast<WarpSmem *>(wsm_raw) + wid;
+  w_segments(W, A.tasks[pos].node, active);  // position order: nodes unchanged by task_list
   W.fck = A.fck; W.bck = A.bck; W.ck_stride = A.ck_stride;
   const int64_t spare = A.ntask + lane;   // idle lanes checkpoint into spare columns
   W.tix = active ? tix : spare;
@@ -981,6 +931,7 @@ __device__ __forceinline__ void wvec_single_body(const WVecArgs &A) {
     for (int tries = 0; tries < 60; ++tries) {
       tw = w_twist_full(W, lam);
       ++nfact;
+      if (g_force_nudge && tries == 0) tw.ok = false;  // diagnostic (MRRR_FORCE_NUDGE)
       if (!__any_sync(0xffffffffu, active && !tw.ok)) break;
       if (active && !tw.ok) {
         lam = lam_base + nudge; nudge *= 2.0;
@@ -1032,7 +983,7 @@ __device__ __forceinline__ void wvec_single_body(const WVecArgs &A) {
       if (__all_sync(0xffffffffu, conv)) break;
       // later iterations keep the first factorization's twist index
       tw = w_twist_fixed(W, lam, best_r0, !conv);
-      ++nfact;
+      if (!conv) ++nfact;
       if (!conv && !tw.ok) { conv = true; failed = true; W.tix = spare; }
     }
     const long long clk_rqc = clock64();
@@ -1124,14 +1075,16 @@ __device__ __forceinline__ void wvec_split_body(const WVecArgs &A) {
   const int item = blockIdx.x * kSingleWarps + wid;
   if (item >= A.nitems) return;  // whole warp
   const WarpItem It = A.items[item];
-  const Node N = A.nodes[It.node];
   const bool active = It.t0 + lane < It.t1;
-  const int tix = A.task_list ? A.task_list[active ? It.t0 + lane : It.t0] : (active ? It.t0 + lane : It.t0);
+  const int pos = active ? It.t0 + lane : It.t1 - 1;  // idle lanes: the item's last task
+  const int tix = A.task_list ? A.task_list[pos] : pos;
   const VecTask tk = A.tasks[tix];
+  const Node N = A.nodes[tk.node];  // this lane's node (the item's nodes share one block)
   WarpCtx W;
   W.DL = N.DL; W.LDv = A.LDv + N.row0; W.nb = N.nb; W.nseg = (N.nb + kTR - 1) / kTR;
   W.lane = lane;
   W.sm = reinterpret_cast<WarpSmem *>(wsm_raw) + wid;
+  w_segments(W, A.tasks[pos].node, active);  // position order: nodes unchanged by task_list
   W.fck = A.fck; W.bck = A.bck; W.ck_stride = A.ck_stride;
   const int64_t spare = A.ntask + lane;
   W.tix = active ? tix : spare;
@@ -1147,6 +1100,7 @@ __device__ __forceinline__ void wvec_split_body(const WVecArgs &A) {
       for (int tries = 0; tries < 60; ++tries) {
         tw = w_twist_full(W, lam);
         ++nfact;
+        if (g_force_nudge && tries == 0) tw.ok = false;  // diagnostic (MRRR_FORCE_NUDGE)
         if (!__any_sync(0xffffffffu, active && !tw.ok)) break;
         if (active && !tw.ok) {
           lam = lam_base + nudge; nudge *= 2.0;
@@ -1192,17 +1146,31 @@ __device__ __forceinline__ void wvec_split_body(const WVecArgs &A) {
     Q.best.r = 0; Q.best.gamma = 0.0; Q.best.nrm2 = 1.0; Q.best.negc = 0; Q.best.ok = true;
     Q.conv = true; Q.failed = false;
   }
-  if (Q.conv) W.tix = spare;  // parked: its column holds the phase-1 factorization
+  // Phase 2 checkpoints go to the lane's POSITION column (consecutive within
+  // the item: coalesced), not the task's (scattered by the twist sort).  A
+  // lane whose RQC converged in phase 1 rebuilds its checkpoints there with
+  // one fixed-twist factorization at (lam_best, r): the same recurrences over
+  // the same rows as the full factorization's, so the same values (bit for
+  // bit); phase-1 columns are never read here.
+  W.tix = active ? pos : spare;
+  {
+    const bool refac = active && Q.conv && !Q.failed;
+    if (__any_sync(0xffffffffu, refac)) {
+      (void)w_twist_fixed(W, Q.lam_best, Q.best.r, refac);
+      if (refac) ++nfact;
+    }
+  }
+  if (Q.conv) W.tix = spare;  // parked: its column holds its converged factorization
   for (int it = 1;;) {
     if (__all_sync(0xffffffffu, Q.conv)) break;
     const Twist tw = w_twist_fixed(W, Q.lam, best_r0, !Q.conv);
-    ++nfact;
+    if (!Q.conv) ++nfact;
     ++it;
     if (!Q.conv && !tw.ok) { Q.conv = true; Q.failed = true; }
     else if (!Q.conv) Q.update(tw, j, it, A.rqc_max);
     if (Q.conv) W.tix = spare;
   }
-  W.tix = active ? tix : spare;
+  W.tix = active ? pos : spare;
   if (active && Q.failed) {
     A.lo[tk.slot] = Q.lo; A.hi[tk.slot] = Q.hi;
     A.fail_list[atomicAdd(A.fail_count, 1)] = A.task_base + tix;

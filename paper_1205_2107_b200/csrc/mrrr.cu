@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(32) k_root_interval_warp(const Node *nodes, co
     __pipeline_wait_prior(0);
     sturm_last(st, __ldg(&N.DL[nb - 1]).x);
     unsigned c = st.c;
-    if (!ok || !sturm_ok(st)) c = negcount_qd_safe(N.DL, nb, mu);
+    if (!ok || !sturm_ok(st) || g_force_safe) c = negcount_qd_safe(N.DL, nb, mu);
     const bool pass = B.side > 0 ? ((int)c >= nb) : ((int)c <= 0);
     const unsigned bal = __ballot_sync(0xffffffffu, pass);
     if (bal) {
@@ -592,14 +592,30 @@ void launch_grid(int M, const Node *nodes, int node, double lo0, double hi0, int
   g_stats.kernel_launches++;
 }
 
-// Warp items: runs of consecutive tasks of one node, at most 32 per item.
-std::vector<WarpItem> make_warp_items(const std::vector<VecTask> &t, int lanes = 32) {
+struct HostNode {
+  int slot0, slot1, depth, block;
+};
+
+// Warp items: runs of at most 32 consecutive tasks spanning at most maxseg
+// nodes of one block (kernels_warp.cuh, kMaxSeg); maxseg = 1 gives one node
+// per item (MRRR_VEC_PACK=0, diagnostic: the per-lane arithmetic is the same,
+// so the results are bit-identical).
+std::vector<WarpItem> make_warp_items(const std::vector<VecTask> &t, const std::vector<HostNode> &hn,
+                                      int maxseg, int lanes = 32) {
   std::vector<WarpItem> v;
   const int nt = (int)t.size();
   for (int a = 0; a < nt;) {
-    int b = a;
-    while (b < nt && b - a < lanes && t[b].node == t[a].node) ++b;
-    WarpItem w; w.node = t[a].node; w.t0 = a; w.t1 = b; w.pad = 0;
+    int b = a, segs = 0, prev = -1;
+    while (b < nt && b - a < lanes) {
+      const int nd = t[b].node;
+      if (nd != prev) {
+        if (segs == maxseg || (prev >= 0 && hn[nd].block != hn[prev].block)) break;
+        ++segs;
+        prev = nd;
+      }
+      ++b;
+    }
+    WarpItem w; w.node = t[a].node; w.t0 = a; w.t1 = b; w.nsegs = segs;
     v.push_back(w);
     a = b;
   }
@@ -695,9 +711,6 @@ struct Problem {
   int64_t hldz = 0;
 };
 
-struct HostNode {
-  int slot0, slot1, depth;
-};
 
 // The solve runs on a library stream of the device's greatest priority,
 // ordered after the caller's stream on entry and before it on every exit:
@@ -716,10 +729,30 @@ cudaStream_t hp_stream() {
   return st[d & 63];
 }
 
+// Diagnostic switches of common.cuh from the environment (tests only),
+// written to the device only when they change.
+void set_diag_flags(cudaStream_t s) {
+  static int last_safe[64], last_nudge[64];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const int fs = env_int("MRRR_FORCE_SAFE", 0) != 0, fn = env_int("MRRR_FORCE_NUDGE", 0) != 0;
+  if (fs != last_safe[dev & 63]) {
+    CK(cudaMemcpyToSymbolAsync(g_force_safe, &fs, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    last_safe[dev & 63] = fs;
+  }
+  if (fn != last_nudge[dev & 63]) {
+    CK(cudaMemcpyToSymbolAsync(g_force_nudge, &fn, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    last_nudge[dev & 63] = fn;
+  }
+}
+
 int solve(Problem &P, int64_t *m_out) {
   ev_reset();
   const int use_hp = env_int("MRRR_HP_STREAM", 1);
   cudaStream_t s = use_hp ? hp_stream() : P.s;
+  set_diag_flags(P.s);
   struct Join {  // caller's stream waits for the solve stream on every exit
     cudaStream_t user, inner;
     ~Join() {
@@ -1124,7 +1157,7 @@ int solve(Problem &P, int64_t *m_out) {
   std::vector<HostNode> hn(nnodes);
   for (int r = 0; r < nroot; ++r) {
     const Block &B = hb[root_blocks[r]];
-    hn[B.root_node] = {B.slot0, B.slot1, 0};
+    hn[B.root_node] = {B.slot0, B.slot1, 0, root_blocks[r]};
   }
   // 1x1 blocks: the vector kernel handles nb == 1 directly
   std::vector<int> level_nodes(h_root_nodes);
@@ -1210,9 +1243,10 @@ int solve(Problem &P, int64_t *m_out) {
   // footprint next to the tree's kernels); the last flush, and pieces whose
   // level leaves at most kPairMaxClusters clusters to refine, on warp pairs
   // (half the latency, resources to spare).  MRRR_VEC_PAIR: 0 never, 2 always.
-  const int kPairMaxClusters = env_int("MRRR_PAIR_MAXCL", 32);
+  const int kPairMaxClusters = env_int("MRRR_PAIR_MAXCL", 200);
   const int vec_pair = env_int("MRRR_VEC_PAIR", 1);
   const int vec_split = env_int("MRRR_VEC_SPLIT", 1);
+  const int vec_pack = env_int("MRRR_VEC_PACK", 1) ? kMaxSeg : 1;
   auto flush_vectors = [&](int tree_left) {
     for (size_t t0 = vec_done; t0 < tasks.size();) {
       const size_t t1 = std::min<size_t>(tasks.size(), t0 + (size_t)(ck_cap - 32));
@@ -1224,7 +1258,8 @@ int solve(Problem &P, int64_t *m_out) {
         ck_f[sk] = ar.alloc<FwdCk>((size_t)nseg_v * ck_cap);
         ck_b[sk] = ar.alloc<BwdCk>((size_t)nseg_v * ck_cap);
       }
-      auto items = make_warp_items(bt);
+      auto items = make_warp_items(bt, hn, vec_pack);
+      g_stats.vec_items += (int64_t)items.size();
       WarpItem *ditems = ar.alloc<WarpItem>(items.size());
       h2d(dtb, bt.data(), nbt, s);
       h2d(ditems, items.data(), items.size(), s);
@@ -1247,10 +1282,11 @@ int solve(Problem &P, int64_t *m_out) {
       const bool split = !pair && vec_split != 0;
       SplitBufs sb{};
       if (split) {
+        // sort segments: each node's run of tasks (items may span several nodes)
         std::vector<int> seg_b, seg_e;
-        for (size_t q = 0; q < items.size(); ++q)
-          if (q == 0 || items[q].node != items[q - 1].node) { seg_b.push_back(items[q].t0); seg_e.push_back(items[q].t1); }
-          else seg_e.back() = items[q].t1;
+        for (int q = 0; q < nbt; ++q)
+          if (q == 0 || bt[q].node != bt[q - 1].node) { seg_b.push_back(q); seg_e.push_back(q + 1); }
+          else seg_e.back() = q + 1;
         sb.nseg = (int)seg_b.size();
         sb.state = ar.alloc<RqcState>(nbt);
         sb.rkey = ar.alloc<int>(nbt); sb.rkey_out = ar.alloc<int>(nbt);
@@ -1386,7 +1422,7 @@ int solve(Problem &P, int64_t *m_out) {
     // host mirror
     hn.resize(nnodes + ncl);
     for (int c = 0; c < ncl; ++c) {
-      hn[node_base + c] = {cl_s0[c], cl_s1[c], hn[cl_parent[c]].depth + 1};
+      hn[node_base + c] = {cl_s0[c], cl_s1[c], hn[cl_parent[c]].depth + 1, hn[cl_parent[c]].block};
       for (int q = cl_s0[c]; q < cl_s1[c]; ++q) h_slot_node[q] = node_base + c;
     }
     nnodes += ncl;
@@ -1476,7 +1512,7 @@ int solve(Problem &P, int64_t *m_out) {
           q0 = q1;
         }
         for (int q = 0; q < h_nf; ++q) { slots[q] = tasks[fl[q]].slot; ft[q] = tasks[fl[q]]; }
-        auto fitems = make_warp_items(ft);
+        auto fitems = make_warp_items(ft, hn, vec_pack);
         int *dslots = ar.alloc<int>(h_nf), *dfl = ar.alloc<int>(h_nf);
         h2d(dslots, slots.data(), h_nf, s);
         h2d(dfl, fl.data(), h_nf, s);
@@ -1553,6 +1589,7 @@ int solve(Problem &P, int64_t *m_out) {
   g_stats.refine_sweeps = h_ctr[2];
   g_stats.rqc_iters = h_ctr[8];
   g_stats.rqc_fallbacks = h_ctr[9];
+  g_stats.vec_nudges = h_ctr[10];
   g_stats.ms_total = tall.stop();
   g_stats.ms_k_root_bisect = kt_root.ms();
   {
@@ -1605,6 +1642,20 @@ void mrrr_default_opts(mrrr_opts_t *o) {
   o->grid_factor = 4;
   o->rtol_vec = 0.0;
   o->rqc_max = 10;
+}
+
+// mrrr_negcount: the bisection kernels' Sturm count (projective sweep with
+// the qd safe fallback, common.cuh) of a caller-given representation, one
+// thread per shift -- the same per-row operations as k_grid / k_refine_warp.
+__global__ void k_diag_interleave(const double *D, const double *LLD, int nb, double2 *DL) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nb) DL[i] = make_double2(D[i], i < nb - 1 ? LLD[i] : 0.0);
+}
+__global__ void k_diag_negcount(const double2 *DL, int nb, const double *mu, int64_t k, int mode,
+                                int64_t *out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= k) return;
+  out[q] = mode == 1 ? (int64_t)negcount_qd_safe(DL, nb, mu[q]) : (int64_t)negcount_global(DL, nb, mu[q], nullptr);
 }
 
 __global__ void k_n1(const double *d, double *w, double *Z) {
@@ -1757,6 +1808,36 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, doub
   } catch (const MrrrError &er) {
     cudaStreamSynchronize(P.s);
     return er.code;
+  } catch (const CudaError &ce) {
+    cudaGetLastError();
+    return ce.e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;
+  }
+}
+
+int mrrr_negcount(int64_t nb, const double *D, const double *LLD, int64_t k, const double *mu,
+                  int64_t *count, int mode, void *stream) {
+  if (nb < 1 || nb > (int64_t)1 << 30) return -1;
+  if (!D) return -2;
+  if (nb > 1 && !LLD) return -3;
+  if (k < 0) return -4;
+  if (k > 0 && !mu) return -5;
+  if (k > 0 && !count) return -6;
+  if (mode != 0 && mode != 1) return -7;
+  if (k == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  double2 *DL = nullptr;
+  try {
+    set_diag_flags(s);
+    cudaError_t e = cudaMallocAsync((void **)&DL, (size_t)nb * sizeof(double2), s);
+    if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); return MRRR_ERR_NOMEM; }
+    CK(e);
+    k_diag_interleave<<<(int)((nb + 255) / 256), 256, 0, s>>>(D, LLD, (int)nb, DL);
+    CK(cudaGetLastError());
+    k_diag_negcount<<<(int)((k + 127) / 128), 128, 0, s>>>(DL, (int)nb, mu, k, mode, count);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(DL, s));
+    CK(cudaStreamSynchronize(s));
+    return 0;
   } catch (const CudaError &ce) {
     cudaGetLastError();
     return ce.e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;

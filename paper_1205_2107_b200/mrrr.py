@@ -33,7 +33,8 @@ class Stats(C.Structure):
                 ("ms_vectors", C.c_double), ("ms_total", C.c_double),
                 ("ms_k_root_bisect", C.c_double), ("ms_k_vectors", C.c_double),
                 ("vec_tasks", C.c_int64), ("vec_elems", C.c_int64),
-                ("ms_k_final_refine", C.c_double)]
+                ("ms_k_final_refine", C.c_double), ("vec_nudges", C.c_int64),
+                ("vec_items", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -79,6 +80,9 @@ def lib():
         L.mrrr_get_stats.argtypes = [C.POINTER(Stats)]
         L.mrrr_get_stats.restype = C.c_int
         L.mrrr_version.restype = C.c_char_p
+        L.mrrr_negcount.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                    C.c_void_p, C.c_int, C.c_void_p]
+        L.mrrr_negcount.restype = C.c_int
         L.mrrr_trim_workspace.restype = C.c_int
         _lib = L
     return _lib
@@ -282,6 +286,25 @@ def stemr_raw(n, d, e, rng, vl, vu, il, iu, m_ok=True, w=None, Z=None, ldz=None)
                             C.byref(m) if m_ok else C.cast(None, C.POINTER(C.c_int64)),
                             _ptr(w), _ptr(Z), ldz if ldz is not None else max(n, 1),
                             C.c_void_p(0), None)
+
+
+def negcount(D: torch.Tensor, LLD: torch.Tensor, mu: torch.Tensor, mode: int = 0, stream=None):
+    """Sturm counts N(mu_q) of the representation (D, LLD) by the library's
+    bisection arithmetic (``mrrr_negcount``; mode 0 projective sweep, 1 the qd
+    safe path).  float64 CUDA tensors; returns an int64 CUDA tensor."""
+    for t in (D, LLD, mu):
+        if not (t.is_cuda and t.dtype == torch.float64):
+            raise TypeError("negcount takes float64 CUDA tensors")
+    D, LLD, mu = D.contiguous(), LLD.contiguous(), mu.contiguous()
+    out = torch.empty(mu.shape[0], dtype=torch.int64, device=D.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(D.device)
+    with torch.cuda.device(D.device):
+        rc = lib().mrrr_negcount(D.shape[0], _ptr(D), _ptr(LLD), mu.shape[0], _ptr(mu), _ptr(out),
+                                 int(mode), C.c_void_p(stream.cuda_stream))
+    if rc != 0:
+        raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
+    return out
 
 
 def trim_workspace() -> None:

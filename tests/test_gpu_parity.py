@@ -171,7 +171,8 @@ def test_deterministic(torch_cuda, P):
 
 
 @pytest.mark.parametrize("env", [{"MRRR_CS_GROUP": "3"}, {"MRRR_VEC_MODE": "1"}, {"MRRR_VEC_PAIR": "0"},
-                                 {"MRRR_VEC_PAIR": "2"}, {"MRRR_HP_STREAM": "0"}, {"MRRR_VEC_SPLIT": "0"}])
+                                 {"MRRR_VEC_PAIR": "2"}, {"MRRR_HP_STREAM": "0"}, {"MRRR_VEC_SPLIT": "0"},
+                                 {"MRRR_VEC_PACK": "0"}])
 def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     """The launch schedule does not change a single bit: cluster steps in
     groups that reuse the scratch (MRRR_CS_GROUP, the n = 1e5 memory cap's
@@ -181,7 +182,9 @@ def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     split over two warps), the caller's stream instead of the library's
     high-priority one (MRRR_HP_STREAM=0), the single-warp RQC in one kernel
     instead of two phases with the lanes regrouped by twist index
-    (MRRR_VEC_SPLIT=0) -- against the default schedule.
+    (MRRR_VEC_SPLIT=0), one node per vector work item instead of up to
+    kMaxSeg nodes of a block packed into a warp (MRRR_VEC_PACK=0) -- against
+    the default schedule.
     Each cluster's step and each eigenpair's RQC depend on their own data only."""
     for d, e in (W.glued_wilkinson(40), W.random_uniform(3000, 2)):
         w1, Z1 = gpu_solve(P, torch_cuda, d, e)
@@ -317,7 +320,11 @@ def test_config2_random_20000(torch_cuda, P, oracle_mod):
     assert abs(w.sum() - d.sum()) <= n * tol
     assert sturm_placement(d, e, w, np.arange(n), tol)
     Z = Zt.cpu().numpy()
-    oracle_windows(oracle_mod, d, e, w, Z, [(1, 60), (9971, 10030), (19941, 20000)])
+    # 14 oracle index windows of 40 pairs: both spectrum ends, and windows
+    # spread through the giant root cluster (~70 % of the spectrum, SURVEY
+    # [A2]) where the eigenpairs come from tree levels 1-5
+    starts = [1] + [int(x) for x in np.linspace(1500, 18500, 12)] + [n - 39]
+    oracle_windows(oracle_mod, d, e, w, Z, [(a, a + 39) for a in starts])
 
 
 def test_config3_glued_wilkinson_21000(torch_cuda, P, oracle_mod):
@@ -348,12 +355,22 @@ def test_config4_clement_50000(torch_cuda, P, oracle_mod, subset):
     assert np.max(np.abs(w - lam)) <= 4 * n * EPS * tnorm1(d, e)
     res, orth = gpu_metrics(torch, d, e, wt, Zt)
     assert res <= 1 and orth <= 1, (res, orth)
-    cols = [0, 1, 2, 2499, 4999]
-    Zs = Zt[:, cols].cpu().numpy()
-    wo, Zo = oracle_mod.stemr(d, e, il=1, iu=3)
-    ok = dk_comparable(wo, residuals(d, e, w[:3], Zs[:, :3]), residuals(d, e, wo, Zo))
-    assert ok.all()
-    assert np.max(vec_diff_signfree(Zs[:, :3], Zo)) <= 1e-9
+    # oracle vector windows (all Clement gaps are 2: every vector is
+    # Davis-Kahan comparable); the full spectrum adds windows in the middle
+    # (deep in the end-shift chain of clusters) and at the top
+    wins = [(1, 3), (2499, 2502)] + ([] if subset else [(24999, 25002), (49998, 50000)])
+    for il, iu in wins:
+        Zs = Zt[:, il - 1:iu].cpu().numpy()
+        wo, Zo = oracle_mod.stemr(d, e, il=il, iu=iu)
+        rg, ro = residuals(d, e, w[il - 1:iu], Zs), residuals(d, e, wo, Zo)
+        ok = dk_comparable(wo, rg, ro)
+        if il == 1:
+            assert ok.all()  # the spectrum end: residuals far below 1e-10 * gap
+        if ok.any():
+            assert np.max(vec_diff_signfree(Zs[:, ok], Zo[:, ok])) <= 1e-9
+        # every window: the Davis-Kahan sin-theta bound itself (gap 2 to the
+        # rest of the spectrum): |z_gpu -+ z_oracle| <= sqrt(2) (r_g + r_o) / 2
+        assert np.all(vec_diff_signfree(Zs, Zo) <= np.sqrt(2.0) * (rg + ro) / 2.0 + 1e-12)
 
 
 def test_config5_random_100000(torch_cuda, P, oracle_mod):

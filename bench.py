@@ -154,9 +154,47 @@ def cpu_oracle_sample(d, e, pairs: int):
     return pairs / dt, dt, f"oracle_stemr INDEX il..iu={il}..{iu} ({pairs} pairs, with vectors) of the same n={n} matrix"
 
 
-def auto_pairs(n):
-    # ~15 s of single-thread oracle work (measured ~0.6 us per pair per element)
-    return int(max(50, min(n, 15.0 / (0.6e-6 * n))))
+def _oracle_window(job):
+    """One host process of the sharded baseline: the oracle on one index window."""
+    cfg, il, iu = job
+    import oracle  # test infrastructure (bench cpu_baseline / reference legs only)
+    oracle.build()
+    d, e, _ = W.make(cfg)
+    t0 = time.perf_counter()
+    oracle.stemr(d, e, il=il, iu=iu)
+    return time.perf_counter() - t0
+
+
+def cpu_oracle_sharded(cfg, n, k, seconds=12.0, cores=None):
+    """The oracle as it stands on ALL host cores: `cores` independent
+    processes, each solving one index window of the same matrix (SURVEY §8(d)
+    "sharded": the paper's static division of eigenpairs over processes,
+    P:L1139-1146), windows spread through the spectrum so that they sample
+    its clusters; each window is sized for ~`seconds` of single-core work.
+    Returns (pairs/s over the slowest process, cores, sample text, seconds)."""
+    import multiprocessing as mpr
+    import oracle
+    oracle.build()  # once, before the processes start
+    cores = cores or os.cpu_count() or 1
+    per = auto_pairs(n, seconds)
+    per = max(10, min(per, k // cores if k >= cores else 1))
+    jobs = []
+    for c in range(cores):
+        mid = int((c + 0.5) * k / cores)
+        il = max(1, min(k - per + 1, mid - per // 2 + 1))
+        jobs.append((cfg, il, il + per - 1))
+    with mpr.get_context("spawn").Pool(cores) as pool:
+        times = pool.map(_oracle_window, jobs)
+    tot = per * cores
+    return (tot / max(times), cores,
+            f"oracle_stemr on {cores} host processes, each one INDEX window of {per} pairs (with vectors) of the "
+            f"same n={n} matrix, windows centred at ({'...'.join(str(j[1]) for j in (jobs[0], jobs[-1]))}) spread "
+            f"through the spectrum; rate = {tot} pairs / slowest process", max(times))
+
+
+def auto_pairs(n, seconds=15.0):
+    # ~`seconds` of single-thread oracle work (measured ~0.6 us per pair per element)
+    return int(max(50, min(n, seconds / (0.6e-6 * n))))
 
 
 def run_reference(args):
@@ -166,31 +204,46 @@ def run_reference(args):
     d, e, rng = W.make(args.config)
     n = len(d)
     k = n if rng is None else rng[1] - rng[0] + 1
-    pairs = args.cpu_pairs or auto_pairs(n)
-    # each step: a bounded sample, sized so warmup+steps end in a few minutes
+    # each step: a bounded sample on every host core (~3 s of work per core
+    # per step, so that warmup + steps end within a few minutes)
     steps_total = args.warmup + args.steps
-    pairs = max(50, min(pairs, int(pairs * 8 / max(steps_total, 1))))
     vals = []
     for i in range(steps_total):
-        v, dt, desc = cpu_oracle_sample(d, e, pairs)
+        v, cores, desc, dt = cpu_oracle_sharded(args.config, n, k, seconds=3.0)
         if i >= args.warmup:
             vals.append((v, dt))
-    tot = sum(dt for _, dt in vals)
-    value = pairs * len(vals) / tot
+    value = statistics.median(v for v, _ in vals)
     line = {"metric": METRIC, "value": value, "unit": "eigenpairs/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(vals),
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.mean(dt for _, dt in vals),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "n": n, "k": k, "sample_pairs": pairs},
-            "cpu_baseline": {"value": value, "unit": "eigenpairs/s", "cores": 1,
+            "config": {"workload": args.config, "n": n, "k": k},
+            "cpu_baseline": {"value": value, "unit": "eigenpairs/s", "cores": cores,
                              "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": "eigenpairs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args):
+    """`python bench.py --gpus N` outside torchrun: launch N ranks, one per GPU,
+    through torch.distributed.run on this node (rendezvous on 127.0.0.1), and
+    pass their output through (rank 0 prints the JSON line)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -305,9 +358,9 @@ def main():
         # rank's Z columns and all w -> pinned host
         dh = torch.tensor(d).pin_memory()
         eh = torch.tensor(e).pin_memory()
-        c0, c1 = P.shard_columns(k, world, rank)
         wh = torch.empty(k, dtype=torch.float64).pin_memory()
-        Zh = torch.empty((max(c1 - c0, 1), n), dtype=torch.float64).pin_memory()
+        Zh = torch.empty((P.mrrr.dist_capacity(k, world), n), dtype=torch.float64).pin_memory()
+        ml = [0]
         torch.distributed.barrier()
         e_ms = []
         for i in range(args.steps):
@@ -320,6 +373,7 @@ def main():
             wh[:wa.shape[0]].copy_(wa, non_blocking=True)
             if Zl is not None and Zl.shape[1]:
                 Zh[:Zl.shape[1]].copy_(Zl.T, non_blocking=True)
+                ml[0] = Zl.shape[1]
             b.record(stream)
             b.synchronize()
             e_ms.append(a.elapsed_time(b))
@@ -328,7 +382,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         etot = float(t.item())
         e2e = {"value": m * args.steps / (etot / 1e3), "unit": "eigenpairs/s",
-               "h2d_bytes_per_step": 8 * (2 * n - 1), "d2h_bytes_per_step": 8 * m + 8 * n * (c1 - c0),
+               "h2d_bytes_per_step": 8 * (2 * n - 1), "d2h_bytes_per_step": 8 * m + 8 * n * ml[0],
                "ms_per_step": etot / args.steps, "note": "d2h per rank: all w + own Z columns"}
     if not args.no_e2e and world == 1:
         # the host entry allocates its own device buffers: release the
@@ -365,10 +419,12 @@ def main():
     # ---------------- CPU oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        pairs = args.cpu_pairs or auto_pairs(n)
-        v, dt, desc = cpu_oracle_sample(d, e, pairs)
-        cpu = {"value": v, "unit": "eigenpairs/s", "cores": 1, "kind": "oracle", "sample": desc,
+        v, cores, desc, dt = cpu_oracle_sharded(args.config, n, k, seconds=12.0)
+        cpu = {"value": v, "unit": "eigenpairs/s", "cores": cores, "kind": "oracle", "sample": desc,
                "seconds": dt}
+        if args.cpu_pairs:  # single-core reference point on request
+            v1, dt1, desc1 = cpu_oracle_sample(d, e, args.cpu_pairs)
+            cpu["single_core"] = {"value": v1, "sample": desc1, "seconds": dt1}
 
     s0 = stats[-1]
     launches = sum(int(s["kernel_launches"]) for s in stats)

@@ -104,20 +104,40 @@ int mrrr_stemr(int64_t n, const double *d, const double *e, int range,
 
 /*
  * mrrr_stemr_dist -- the same solve sharded over P ranks (one GPU each) by
- * eigen-index range.  Every rank passes the same T,
- * range and opts.  Rank r owns global columns [col_begin, col_begin+m_local);
- * intervals and w are exchanged with `allgather`, a caller-provided
- * all-gather over the ranks (NCCL over NVLink in the Python binding):
+ * eigen-index range ("PMRRR's parallelism").  Every rank
+ * passes the same T, range and opts.  Protocol, the paper's
+ * static division and task types adapted to GPUs:
+ *   - the root representation is computed on every rank;
+ *   - the root grid and the root bisection work are split into P shares and
+ *     gathered (two all-gathers; "gather");
+ *   - the m wanted columns are divided statically (epp = ceil(m/P)) and, with
+ *     one irreducible block and vectors, each cut moves to the nearest root
+ *     cluster boundary within epp/40 (a share holds at most epp + epp/20
+ *     columns);
+ *   - every tree level: a rank computes the child representations of the
+ *     clusters holding one of its columns and refines only the members it
+ *     owns (a cluster shared by several ranks is the paper's type-3 task,
+ *     P:L1176-1182); one all-gather of the brackets (+ a status word) per
+ *     level gives every rank the same classification;
+ *   - vectors only for the rank's columns, into Z_local (Z never moves);
+ *   - a final all-gather of w (+ status).
+ * Every rank calls the same sequence of collectives whatever happens; an
+ * error on one rank is carried by the status word and every rank returns
+ * the worst code at the same exchange.
+ * The collective is `allgather`, a caller-provided all-gather over the ranks
+ * (NCCL over NVLink in the Python binding):
  *   allgather(ctx, send, recv, bytes, stream): recv[r*bytes .. ] <- rank r's
- *   send (bytes each), device buffers, enqueued on `stream`; returns 0 on
- *   success.
+ *   send (bytes each), device buffers, enqueued on `stream` (the library's
+ *   solve stream); returns 0 on success.
  * Arguments 1-8 and 14 as in mrrr_stemr; further:
  *  (9)  rank, (10) nranks (1 <= nranks, 0 <= rank < nranks),
  *  (11) allgather, (12) allgather_ctx,
- *  (13) m (HOST out, global count), (15) col_begin, (16) m_local (HOST out),
- *  (17) w_all (device out, all m eigenvalues on every rank),
- *  (18) Z_local (device out, ldz x m_local; NULL = values only), (19) ldz,
- *  (20) stream.
+ *  (13) m (HOST out, global count), (15) col_begin, (16) m_local (HOST out:
+ *       this rank's columns [col_begin, col_begin + m_local)),
+ *  (17) w_all (device out, all m eigenvalues on every rank; capacity as w),
+ *  (18) Z_local (device out, ldz x m_local; NULL = values only; capacity
+ *       ceil(k/P) + ceil(k/P)/20 columns with k the capacity of w),
+ *  (19) ldz, (20) stream.
  */
 typedef int (*mrrr_allgather_fn)(void *ctx, const void *send, void *recv,
                                  size_t bytes, void *stream);
@@ -140,6 +160,13 @@ int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range,
                     double vl, double vu, int64_t il, int64_t iu, int64_t *m,
                     double *w, double *Z, int64_t ldz, void *stream,
                     const mrrr_opts_t *opts);
+
+/* The shard planner of mrrr_stemr_dist (host only, for tests): cuts[0..nranks]
+ * start as the static division r * ceil(m/nranks); every inner cut moves to
+ * the nearest column j with free_cut[j] != 0 (free_cut[m+1]: a cluster
+ * boundary between columns j-1 and j) within ceil(m/nranks)/40, ties to the
+ * left.  Returns 0 or -i for an invalid argument i. */
+int mrrr_plan_columns(int64_t m, int nranks, const unsigned char *free_cut, int64_t *cuts);
 
 /* Upper bound of the device workspace mrrr_stemr allocates internally for an
  * order-n problem with k wanted eigenpairs (bytes), excluding the

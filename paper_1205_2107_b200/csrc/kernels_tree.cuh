@@ -380,18 +380,20 @@ struct Work {
 };
 
 // a3 -- root grid: counts of the root representation at G uniformly spaced
-// points x_g = lo0 + (hi0 - lo0) g / G, g = 1..G-1 (one CTA handles
-// blockDim.x * M consecutive points).  cnt[g] for g in [1, G-1].
+// points x_g = lo0 + (hi0 - lo0) g / G, g = g_begin .. g_end-1 within
+// [1, G-1] (one CTA handles blockDim.x * M consecutive points; a multi-GPU
+// rank evaluates its share of the points).  cnt[g].
 template <int M>
 __global__ void __launch_bounds__(128) k_grid(const Node *nodes, int node, double lo0, double hi0,
-                                              int G, int *cnt, unsigned long long *safe_ctr) {
+                                              int G, int g_begin, int g_end, int *cnt,
+                                              unsigned long long *safe_ctr) {
   __shared__ double2 sm[2 * kTile];
   const Node N = nodes[node];
   double mu[M];
-  int g0 = (blockIdx.x * blockDim.x + threadIdx.x) * M + 1;
+  int g0 = (blockIdx.x * blockDim.x + threadIdx.x) * M + g_begin;
 #pragma unroll
   for (int c = 0; c < M; ++c) {
-    int g = min(g0 + c, G - 1);
+    int g = min(g0 + c, g_end - 1);
     mu[c] = lo0 + (hi0 - lo0) * ((double)g / (double)G);
   }
   unsigned k[M];
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(128) k_grid(const Node *nodes, int node, doubl
 #pragma unroll
   for (int c = 0; c < M; ++c) {
     int g = g0 + c;
-    if (g < G) {
+    if (g < g_end) {
       unsigned v = k[c];
       if (!ok || g_force_safe) { atomicAdd(safe_ctr, 1ull); v = negcount_qd_safe(N.DL, N.nb, mu[c]); }
       cnt[g] = (int)v;

@@ -79,23 +79,38 @@ void dump(const char *name, const T *dptr, size_t count, cudaStream_t s) {
   if (f) { fwrite(h.data(), sizeof(T), count, f); fclose(f); }
 }
 
+// Per-thread library objects (streams, workspace, events, staging) are
+// created on first use per device and RELEASED when the thread exits (the
+// holders' destructors), so threads that call the library and exit leak
+// nothing; mrrr_trim_workspace() releases the memory of the calling thread
+// earlier.  (At process exit the CUDA context may already be gone; the
+// destructors then ignore the errors.)
 constexpr int kSide = 4;  // side streams for the vector batches
+struct StreamSet {
+  cudaStream_t st[64][kSide + 2] = {};  // per device: kSide side streams, the copy stream, the solve stream
+  ~StreamSet() {
+    for (auto &dv : st)
+      for (cudaStream_t &x : dv)
+        if (x) { cudaStreamDestroy(x); x = nullptr; }
+  }
+};
+thread_local StreamSet g_streams;
+
 cudaStream_t *side_streams() {
-  thread_local cudaStream_t st[64][kSide] = {};
   int d = 0;
   CK(cudaGetDevice(&d));
-  cudaStream_t *x = st[d & 63];
+  cudaStream_t *x = g_streams.st[d & 63];
   if (!x[0])
     for (int k = 0; k < kSide; ++k) CK(cudaStreamCreateWithFlags(&x[k], cudaStreamNonBlocking));
   return x;
 }
 
 cudaStream_t copy_stream() {  // Z downloads of the host entry (per thread and device)
-  thread_local cudaStream_t st[64] = {};
   int d = 0;
   CK(cudaGetDevice(&d));
-  if (!st[d & 63]) CK(cudaStreamCreateWithFlags(&st[d & 63], cudaStreamNonBlocking));
-  return st[d & 63];
+  cudaStream_t &x = g_streams.st[d & 63][kSide];
+  if (!x) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+  return x;
 }
 
 int env_int(const char *name, int dflt) {
@@ -174,6 +189,7 @@ struct BumpWs {
     chunks.clear();
     reset();
   }
+  ~BumpWs() { release(); }
 };
 thread_local BumpWs g_ws_call[64], g_ws_level[64];
 
@@ -190,6 +206,7 @@ BumpWs &device_ws(BumpWs *arr) {
 struct GrowBuf {
   void *p = nullptr;
   size_t cap = 0;
+  ~GrowBuf() { if (p) cudaFree(p); }
 };
 thread_local GrowBuf g_child_scratch_arr[64];
 GrowBuf &child_scratch() {
@@ -248,6 +265,9 @@ struct Staging {
     }
   }
   void reset() { chunk = 0; off = 0; }
+  ~Staging() {
+    for (auto &c : chunks) cudaFreeHost(c.first);
+  }
 };
 thread_local Staging g_staging;
 
@@ -276,6 +296,9 @@ struct EvPool {
   unsigned flags;
   std::vector<cudaEvent_t> ev;
   size_t i = 0;
+  ~EvPool() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
   cudaEvent_t get() {
     if (i == ev.size()) {
       cudaEvent_t e;
@@ -287,6 +310,17 @@ struct EvPool {
 };
 thread_local EvPool g_ev_sync{cudaEventDisableTiming}, g_ev_time{cudaEventDefault};
 cudaEvent_t ev_sync() { return g_ev_sync.get(); }
+// for destructors (stream joins on every exit path): never throws
+void join_streams_nothrow(cudaStream_t waiter, cudaStream_t producer) {
+  if (!waiter || !producer || waiter == producer) return;
+  try {
+    cudaEvent_t e = ev_sync();
+    cudaEventRecord(e, producer);
+    cudaStreamWaitEvent(waiter, e, 0);
+  } catch (...) {
+    cudaStreamSynchronize(producer);  // no event available: wait on the host instead
+  }
+}
 cudaEvent_t ev_time() { return g_ev_time.get(); }
 void ev_reset() { g_ev_sync.i = 0; g_ev_time.i = 0; }
 
@@ -322,7 +356,7 @@ struct KTimer {
 
 // Launch helpers -----------------------------------------------------------
 __global__ void k_root_interval(const Node *nodes, const Block *blocks, const int *root_nodes,
-                                int nroot, double *lo0, double *hi0, double tnrm_scaled) {
+                                int nroot, double *lo0, double *hi0, double tnrm_scaled, int *fail) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nroot) return;
   const Node N = nodes[root_nodes[r]];
@@ -330,21 +364,23 @@ __global__ void k_root_interval(const Node *nodes, const Block *blocks, const in
   double sigma = N.tau_hi;
   double wid = 2.0 * kEps * fmax(B.spdiam, tnrm_scaled) + kTiny;
   if (N.nb == 1) { lo0[r] = hi0[r] = __ldg(&N.DL[0]).x; return; }
+  bool found = false;
   if (B.side > 0) {
     lo0[r] = 0.0;
-    for (int k = 0; k < 200; ++k) {
+    for (int k = 0; k < 200 && !found; ++k) {
       double h = (B.gu - sigma) + wid;
-      if ((int)negcount_global(N.DL, N.nb, h, nullptr) >= N.nb) { hi0[r] = h; break; }
+      if ((int)negcount_global(N.DL, N.nb, h, nullptr) >= N.nb) { hi0[r] = h; found = true; }
       wid *= 2.0;
     }
   } else {
     hi0[r] = 0.0;
-    for (int k = 0; k < 200; ++k) {
+    for (int k = 0; k < 200 && !found; ++k) {
       double l = (B.gl - sigma) - wid;
-      if ((int)negcount_global(N.DL, N.nb, l, nullptr) <= 0) { lo0[r] = l; break; }
+      if ((int)negcount_global(N.DL, N.nb, l, nullptr) <= 0) { lo0[r] = l; found = true; }
       wid *= 2.0;
     }
   }
+  if (!found) { lo0[r] = hi0[r] = 0.0; fail[0] = 1; }
 }
 
 // Warp version: the 32 lanes try the offsets wid * 2^k, k = k0 .. k0+31, in
@@ -353,7 +389,7 @@ __global__ void k_root_interval(const Node *nodes, const Block *blocks, const in
 // loop's answer.
 __global__ void __launch_bounds__(32) k_root_interval_warp(const Node *nodes, const Block *blocks,
                                                            const int *root_nodes, int nroot, double *lo0,
-                                                           double *hi0, double tnrm_scaled) {
+                                                           double *hi0, double tnrm_scaled, int *fail) {
   constexpr int T = 16, RING = 6;
   __shared__ double2 ring[RING][T];
   const int r = blockIdx.x, lane = threadIdx.x;
@@ -414,6 +450,7 @@ __global__ void __launch_bounds__(32) k_root_interval_warp(const Node *nodes, co
       return;
     }
   }
+  if (lane == 0) { lo0[r] = hi0[r] = 0.0; fail[0] = 1; }  // no enclosing bound within 224 doublings
 }
 
 __global__ void k_block_norms(const double *ds, const double *es, Block *blocks, int nblocks) {
@@ -460,14 +497,18 @@ __global__ void k_root_nodes(Node *nodes, const Block *blocks, const int *root_b
 }
 
 // Child node entries and bracket translation to child coordinates (O9.4).
+// cl_pool[c]: the pool row of cluster c's child RRR on this rank, -1 when
+// another rank owns the cluster (multi-GPU: the entry keeps the tree's
+// numbering; its representation is never read here)
 __global__ void k_child_nodes(Node *nodes, int node_base, const int *cl_parent, const int *cl_s0,
                               const int *cl_s1, const double *sigma, int ncl, double2 *pool,
-                              int64_t stride, const int *slot_jlocal) {
+                              int64_t stride, const int *slot_jlocal, const int *cl_pool) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
   Node P = nodes[cl_parent[c]];
   Node N = P;
-  N.DL = pool + (int64_t)c * stride;
+  const int pi = cl_pool[c];
+  N.DL = pi >= 0 ? pool + (int64_t)pi * stride : nullptr;
   N.slot0 = cl_s0[c]; N.slot1 = cl_s1[c];
   N.depth = P.depth + 1;
   N.jbase = slot_jlocal[cl_s0[c]];
@@ -491,6 +532,17 @@ __global__ void k_translate(const int *slot_cl, const int *cl_first_slot, int ns
   lo[s] = l - sg; hi[s] = h - sg;
   wl[s] = w; wu[s] = w;
   slot_node[s] = node_base + c;
+}
+
+// e: merge of the bracket exchange -- slot q takes the brackets of its
+// owner rank (recv holds the ranks' [lo | hi | header] arrays, stride apart)
+__global__ void k_merge_brackets(const double *recv, int64_t stride, int nslots, const int *owner, double *lo,
+                                 double *hi) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nslots) return;
+  const double *src = recv + (int64_t)owner[q] * stride;
+  lo[q] = src[q];
+  hi[q] = src[nslots + q];
 }
 
 __global__ void k_scatter(const int *idx, const double *src, int n, double *dst) {
@@ -577,16 +629,17 @@ __global__ void k_grid_assign2(int *cnt, int G, int nb, double lo0, double hi0, 
   }
 }
 
-void launch_grid(int M, const Node *nodes, int node, double lo0, double hi0, int G, int *cnt,
-                 unsigned long long *safe, cudaStream_t s) {
-  int pts = G - 1;
+// grid points g in [g_begin, g_end) of the G-interval grid (1 <= g_begin, g_end <= G)
+void launch_grid(int M, const Node *nodes, int node, double lo0, double hi0, int G, int g_begin, int g_end,
+                 int *cnt, unsigned long long *safe, cudaStream_t s) {
+  int pts = g_end - g_begin;
   int per_cta = 128 * M;
   int grid = (pts + per_cta - 1) / per_cta;
   if (grid <= 0) return;
   switch (M) {
-    case 1: k_grid<1><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, cnt, safe); break;
-    case 2: k_grid<2><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, cnt, safe); break;
-    default: k_grid<4><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, cnt, safe); break;
+    case 1: k_grid<1><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, g_begin, g_end, cnt, safe); break;
+    case 2: k_grid<2><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, g_begin, g_end, cnt, safe); break;
+    default: k_grid<4><<<grid, 128, 0, s>>>(nodes, node, lo0, hi0, G, g_begin, g_end, cnt, safe); break;
   }
   CK(cudaGetLastError());
   g_stats.kernel_launches++;
@@ -718,15 +771,35 @@ struct Problem {
 // kernels wait for SM resources at the same time, the block scheduler
 // serves the tree -- the critical path -- first.
 cudaStream_t hp_stream() {
-  thread_local cudaStream_t st[64] = {};
   int d = 0;
   CK(cudaGetDevice(&d));
-  if (!st[d & 63]) {
+  cudaStream_t &x = g_streams.st[d & 63][kSide + 1];
+  if (!x) {
     int lo_pr = 0, hi_pr = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
-    CK(cudaStreamCreateWithPriority(&st[d & 63], cudaStreamNonBlocking, hi_pr));
+    CK(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, hi_pr));
   }
-  return st[d & 63];
+  return x;
+}
+
+// e: shard planner.  cuts[0..nranks] start as the static division (rank r
+// owns columns [cuts[r], cuts[r+1])); each inner cut moves to the nearest
+// column j with free_cut[j] != 0 (a cluster boundary between columns j-1
+// and j) within epp / 40, so a share grows by at most epp / 20 (5 %).  Ties
+// go to the left.  Deterministic: every rank computes the same cuts.
+void plan_columns(int64_t m, int nranks, const unsigned char *free_cut, int64_t *cuts) {
+  const int64_t epp = (m + nranks - 1) / nranks, slack = epp / 40;
+  for (int r = 0; r <= nranks; ++r) cuts[r] = std::min<int64_t>((int64_t)r * epp, m);
+  for (int r = 1; r < nranks; ++r) {
+    const int64_t t = cuts[r];
+    if (t <= cuts[r - 1] || t >= m) { cuts[r] = std::max(cuts[r - 1], std::min(t, m)); continue; }
+    int64_t best = -1;
+    for (int64_t d = 0; d <= slack && best < 0; ++d) {
+      if (t - d > cuts[r - 1] && t - d > 0 && free_cut[t - d]) best = t - d;
+      else if (t + d < m && free_cut[t + d]) best = t + d;
+    }
+    if (best >= 0) cuts[r] = best;
+  }
 }
 
 // Diagnostic switches of common.cuh from the environment (tests only),
@@ -755,12 +828,7 @@ int solve(Problem &P, int64_t *m_out) {
   set_diag_flags(P.s);
   struct Join {  // caller's stream waits for the solve stream on every exit
     cudaStream_t user, inner;
-    ~Join() {
-      if (inner == user) return;
-      cudaEvent_t e = ev_sync();
-      cudaEventRecord(e, inner);
-      cudaStreamWaitEvent(user, e, 0);
-    }
+    ~Join() { join_streams_nothrow(user, inner); }
   } join{P.s, s};
   if (s != P.s) {
     cudaEvent_t e = ev_sync();
@@ -953,20 +1021,29 @@ int solve(Problem &P, int64_t *m_out) {
   h2d(droot_nodes, h_root_nodes.data(), nroot, s);
   double *dlo0 = ar.alloc<double>(nroot), *dhi0 = ar.alloc<double>(nroot);
   if (nroot <= 4096)
-    k_root_interval_warp<<<nroot, 32, 0, s>>>(dnodes, dblocks, droot_nodes, nroot, dlo0, dhi0, tnrm_s);
+    k_root_interval_warp<<<nroot, 32, 0, s>>>(dnodes, dblocks, droot_nodes, nroot, dlo0, dhi0, tnrm_s, dfail + 3);
   else
     k_root_interval<<<(nroot + 63) / 64, 64, 0, s>>>(dnodes, dblocks, droot_nodes, nroot, dlo0, dhi0,
-                                                     tnrm_s);
+                                                     tnrm_s, dfail + 3);
   CK(cudaGetLastError());
   g_stats.kernel_launches += 2;
   std::vector<double> hlo0(nroot), hhi0(nroot);
   d2h(hlo0.data(), dlo0, nroot, s);
   d2h(hhi0.data(), dhi0, nroot, s);
+  {
+    int hf[4];
+    d2h(hf, dfail, 4, s);
+    if (hf[3]) throw MrrrError{MRRR_ERR_CONVERGE};  // no root interval found
+  }
 
-  // slots (device)
+  // slots (device).  slo and shi are the two halves of one array whose tail
+  // holds the exchange header of a multi-GPU rank (status, clusters): one
+  // all-gather moves a rank's brackets and header together.
   int *slot_j = ar.alloc<int>(nslots), *slot_node = ar.alloc<int>(nslots);
   int *slot_out = ar.alloc<int>(nslots);
-  double *slo = ar.alloc<double>(nslots), *shi = ar.alloc<double>(nslots);
+  const int64_t xstride = 2 * nslots + 2;  // doubles per rank in the bracket exchange
+  double *slo = ar.alloc<double>(xstride);
+  double *shi = slo + nslots, *xhdr = slo + 2 * nslots;
   std::vector<int> h_slot_node(nslots);
   std::vector<double> h_lo(nslots), h_hi(nslots);
   for (int r = 0; r < nroot; ++r) {
@@ -979,6 +1056,60 @@ int solve(Problem &P, int64_t *m_out) {
   h2d(slot_node, h_slot_node.data(), nslots, s);
   h2d(slo, h_lo.data(), nslots, s);
   h2d(shi, h_hi.data(), nslots, s);
+
+  // ---- e: the ranks' collectives.  Every rank calls the same
+  // sequence of all-gathers; each carries a status word so that an error on
+  // one rank stops all of them at the same exchange (no rank is left waiting).
+  const int nr = std::max(1, P.nranks);
+  const bool dist = nr > 1;
+  // cap of each of the two large scratch areas (vector checkpoints, cluster
+  // step scratch); MRRR_SCRATCH_GB overrides (virtual ranks sharing one GPU)
+  const double scratch_bytes = 1e9 * std::max(1, env_int("MRRR_SCRATCH_GB", 16));
+  double *xrecv = dist ? ar.alloc<double>((size_t)nr * xstride) : nullptr;
+  int *slot_owner = dist ? ar.alloc<int>(nslots) : nullptr;
+  std::vector<int> h_slot_owner(dist ? nslots : 0, 0);
+  int local_status = 0;
+  // all-gather of this rank's brackets (+ header) and merge: each slot takes
+  // the brackets of the rank that owns it (h_slot_owner); returns the
+  // maximum over the ranks of header word 1 and throws the worst status
+  auto exchange_brackets = [&](double hdr1) -> double {
+    double hh[2] = {(double)local_status, hdr1};
+    h2d(xhdr, hh, 2, s);
+    if (P.allgather(P.ag_ctx, slo, xrecv, (size_t)xstride * sizeof(double), (void *)s) != 0)
+      throw MrrrError{MRRR_ERR_COMM};
+    h2d(slot_owner, h_slot_owner.data(), nslots, s);
+    k_merge_brackets<<<(int)((nslots + 255) / 256), 256, 0, s>>>(xrecv, xstride, (int)nslots, slot_owner, slo, shi);
+    CK(cudaGetLastError());
+    g_stats.kernel_launches++;
+    std::vector<double> hdrs(2 * (size_t)nr);
+    for (int r = 0; r < nr; ++r) CK(cudaMemcpyAsync(&hdrs[2 * r], xrecv + (int64_t)r * xstride + 2 * nslots,
+                                                    2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int worst = 0;
+    double mx = 0;
+    for (int r = 0; r < nr; ++r) {
+      const int st = (int)hdrs[2 * r];
+      if (st != 0 && (worst == 0 || st > worst)) worst = st;
+      mx = std::max(mx, hdrs[2 * r + 1]);
+    }
+    if (worst) throw MrrrError{worst};
+    return mx;
+  };
+
+  // dist: a failure between two collectives is recorded in local_status and
+  // the rank goes on to the next collective, whose status words make every
+  // rank leave there with the worst code (one GPU: errors propagate at once)
+  auto guarded = [&](auto &&f) {
+    if (!dist) { f(); return; }
+    try {
+      if (local_status == 0) f();
+    } catch (const MrrrError &er) {
+      if (!local_status) local_status = er.code;
+    } catch (const CudaError &ce) {
+      cudaGetLastError();
+      if (!local_status) local_status = ce.e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;
+    }
+  };
 
   // ---------------- a3: root eigenvalue intervals ----------------
   const double rtol_root = (vectors && nblocks == 1) ? P.o.rtol_class : 4.0 * kEps;
@@ -1020,22 +1151,64 @@ int solve(Problem &P, int64_t *m_out) {
       if (nroot == 1 && gf > 0 && nsl >= 64) {
         int G = (int)std::min<int64_t>((int64_t)gf * nsl + 1, 1 << 20);
         G = std::max(G, 256);
-        int *cnt = ar.alloc<int>(G + 1);
-        launch_grid(4, dnodes, B.root_node, hlo0[r], hhi0[r], G, cnt, ctr + 1, s);
-        g_stats.root_sweeps += G - 1;
-        k_grid_assign2<<<1, 1024, 0, s>>>(cnt, G, B.nb, hlo0[r], hhi0[r], slot_j, B.slot0,
-                                          B.slot1, slo, shi);
+        if (!dist) {
+          int *cnt = ar.alloc<int>(G + 1);
+          launch_grid(4, dnodes, B.root_node, hlo0[r], hhi0[r], G, 1, G, cnt, ctr + 1, s);
+          g_stats.root_sweeps += G - 1;
+          k_grid_assign2<<<1, 1024, 0, s>>>(cnt, G, B.nb, hlo0[r], hhi0[r], slot_j, B.slot0,
+                                            B.slot1, slo, shi);
+        } else {
+          // e: each rank counts its share gp of the G-1 grid points, one
+          // all-gather assembles the counts (the static
+          // division of the bisection work, then a gather)
+          const int gp = (G - 1 + nr - 1) / nr;
+          const int g_lo = 1 + P.rank * gp, g_hi = std::min(G, g_lo + gp);
+          int *cnt_part = ar.alloc<int>((size_t)gp + G + 1);
+          int *cnt = ar.alloc<int>((size_t)nr * gp + 2);
+          guarded([&] {
+            if (g_hi > g_lo) launch_grid(4, dnodes, B.root_node, hlo0[r], hhi0[r], G, g_lo, g_hi, cnt_part, ctr + 1, s);
+          });
+          g_stats.root_sweeps += std::max(0, g_hi - g_lo);
+          if (P.allgather(P.ag_ctx, cnt_part + g_lo, cnt + 1, (size_t)gp * sizeof(int), (void *)s) != 0)
+            throw MrrrError{MRRR_ERR_COMM};
+          k_grid_assign2<<<1, 1024, 0, s>>>(cnt, G, B.nb, hlo0[r], hhi0[r], slot_j, B.slot0,
+                                            B.slot1, slo, shi);
+        }
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }
       make_work(B.root_node, B.slot0, B.slot1, env_int("MRRR_RW_ROOT_CHUNK", 0) > 0 ? std::min(env_int("MRRR_RW_ROOT_CHUNK", 0), kRWMembers) : rw_chunk(B.nb), wv);  // rank-invariant (block size)
     }
-    Work *dwork = ar.alloc<Work>(wv.size());
+    // e: the work items are split into nr contiguous shares; a slot is owned
+    // by the rank whose share holds its item, and one all-gather + merge
+    // gives every rank all root brackets
+    size_t w0 = 0, w1 = wv.size();
+    if (dist) {
+      const size_t per = (wv.size() + nr - 1) / nr;
+      w0 = std::min(wv.size(), (size_t)P.rank * per);
+      w1 = std::min(wv.size(), w0 + per);
+      for (size_t i = 0; i < wv.size(); ++i)
+        for (int q = wv[i].s0; q < wv[i].s1; ++q) h_slot_owner[q] = (int)(i / per);
+    }
+    Work *dwork = ar.alloc<Work>(std::max<size_t>(wv.size(), 1));
     h2d(dwork, wv.data(), wv.size(), s);
-    launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, nullptr, nullptr, 0, rtol_root,
-                  dfail + 2, ctr, ctr + 1, s);
+    guarded([&] {
+      launch_refine(dnodes, dwork + w0, (int)(w1 - w0), nullptr, slot_j, slo, shi, nullptr, nullptr, 0, rtol_root,
+                    dfail + 2, ctr, ctr + 1, s);
+      if (dist) {
+        int hf = 0;
+        d2h(&hf, dfail + 2, 1, s);
+        if (hf) throw MrrrError{MRRR_ERR_CONVERGE};
+      }
+    });
+    if (dist) exchange_brackets(0.0);
     (void)M;
     kt_root.stop(s);
+  }
+  {
+    int hf[4];
+    d2h(hf, dfail, 4, s);
+    if (hf[2]) throw MrrrError{MRRR_ERR_CONVERGE};  // root bisection did not converge
   }
 
   // output positions
@@ -1097,34 +1270,77 @@ int solve(Problem &P, int64_t *m_out) {
     }
     m = cnt;
   }
-  // ---- e: this rank's columns (static division of the m wanted pairs,
-  // P:L1139-1146); every rank builds the same root, intervals and tree for
-  // the clusters its columns touch, and computes only its own vectors.
-  const int nr = std::max(1, P.nranks);
+  // ---- e: this rank's columns.  The static division of the m wanted pairs
+  // (epp = ceil(m / P) per rank); with vectors and one block,
+  // the root classification then moves each cut to the nearest cluster
+  // boundary within epp / 20 (plan_columns, below), so fewer clusters are
+  // shared between ranks.  Every rank builds the same root, intervals and
+  // tree structure, works on the clusters its columns touch, and computes
+  // only its own vectors.
   const int64_t epp = (m + nr - 1) / nr;
-  const int64_t c0 = std::min<int64_t>((int64_t)P.rank * epp, m), c1 = std::min<int64_t>(c0 + epp, m);
-  P.col_begin = c0;
-  P.m_local = c1 - c0;
+  std::vector<int64_t> cuts(nr + 1);
+  for (int r = 0; r <= nr; ++r) cuts[r] = std::min<int64_t>((int64_t)r * epp, m);
   std::vector<int> h_own(nslots, -1);  // local output column of a slot, or -1
+  std::vector<int> col_slot(m, -1);    // slot of each output column
   for (int64_t q = 0; q < nslots; ++q)
-    if (h_slot_out[q] >= c0 && h_slot_out[q] < c1) h_own[q] = (int)(h_slot_out[q] - c0);
-  // local eigenvalue buffer: the caller's w on one GPU, a padded buffer for the
+    if (h_slot_out[q] >= 0) col_slot[h_slot_out[q]] = (int)q;
+  auto apply_cuts = [&]() {
+    const int64_t c0 = cuts[P.rank], c1 = cuts[P.rank + 1];
+    P.col_begin = c0;
+    P.m_local = c1 - c0;
+    for (int64_t q = 0; q < nslots; ++q)
+      h_own[q] = (h_slot_out[q] >= c0 && h_slot_out[q] < c1) ? (int)(h_slot_out[q] - c0) : -1;
+    if (!dist) return;
+    // slot owners for the bracket exchanges of the tree: the rank of the
+    // slot's column; a gap neighbour (no column) goes to the rank of the
+    // nearest column of its block
+    std::vector<int> col_rank(m);
+    for (int r = 0; r < nr; ++r)
+      for (int64_t c = cuts[r]; c < cuts[r + 1]; ++c) col_rank[c] = r;
+    for (int64_t q = 0; q < nslots; ++q) {
+      if (h_slot_out[q] >= 0) { h_slot_owner[q] = col_rank[h_slot_out[q]]; continue; }
+      int own = 0;
+      for (int64_t d = 1; d < nslots; ++d) {
+        if (q - d >= 0 && h_slot_block[q - d] == h_slot_block[q] && h_slot_out[q - d] >= 0) { own = col_rank[h_slot_out[q - d]]; break; }
+        if (q + d < nslots && h_slot_block[q + d] == h_slot_block[q] && h_slot_out[q + d] >= 0) { own = col_rank[h_slot_out[q + d]]; break; }
+        if (q - d < 0 && q + d >= nslots) break;
+      }
+      h_slot_owner[q] = own;
+    }
+  };
+  apply_cuts();
+  // local eigenvalue buffer: the caller's w on one GPU, a padded buffer of
+  // the largest possible share (epp + epp / 20, the planner's slack) for the
   // all-gather otherwise
+  const int64_t wcap = std::max<int64_t>(epp + epp / 20, 1);
   double *w_loc = P.w;
   if (nr > 1) {
-    w_loc = ar.alloc<double>(std::max<int64_t>(epp, 1));
-    CK(cudaMemsetAsync(w_loc, 0, std::max<int64_t>(epp, 1) * sizeof(double), s));
+    w_loc = ar.alloc<double>(wcap + 1);
+    CK(cudaMemsetAsync(w_loc, 0, (wcap + 1) * sizeof(double), s));
   }
-  // final w: all-gather of the padded local parts (dist) and the O11 monotone fix
+  // final w: all-gather of the padded local parts (dist; the last word is
+  // the rank's status) and the O11 monotone fix
   auto finish_w = [&]() {
     if (nr == 1) {
       if (m > 1) { k_monotone<<<1, 1024, 0, s>>>(P.w, (int)m); CK(cudaGetLastError()); g_stats.kernel_launches++; }
       return;
     }
-    double *wall = ar.alloc<double>(std::max<int64_t>(epp * nr, 1));
-    if (P.allgather(P.ag_ctx, w_loc, wall, (size_t)epp * sizeof(double), (void *)s) != 0)
+    double *wall = ar.alloc<double>((size_t)nr * (wcap + 1));
+    const double st = (double)local_status;
+    h2d(w_loc + wcap, &st, 1, s);
+    if (P.allgather(P.ag_ctx, w_loc, wall, (size_t)(wcap + 1) * sizeof(double), (void *)s) != 0)
       throw MrrrError{MRRR_ERR_COMM};
-    if (m > 0) CK(cudaMemcpyAsync(P.w_all, wall, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    for (int r = 0; r < nr; ++r)
+      if (cuts[r + 1] > cuts[r])
+        CK(cudaMemcpyAsync(P.w_all + cuts[r], wall + (int64_t)r * (wcap + 1), (cuts[r + 1] - cuts[r]) * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s));
+    std::vector<double> sts(nr);
+    for (int r = 0; r < nr; ++r)
+      CK(cudaMemcpyAsync(&sts[r], wall + (int64_t)r * (wcap + 1) + wcap, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int worst = 0;
+    for (int r = 0; r < nr; ++r) if ((int)sts[r] != 0 && (worst == 0 || (int)sts[r] > worst)) worst = (int)sts[r];
+    if (worst) throw MrrrError{worst};
     if (m > 1) { k_monotone<<<1, 1024, 0, s>>>(P.w_all, (int)m); CK(cudaGetLastError()); g_stats.kernel_launches++; }
   };
   h2d(slot_out, h_own.data(), nslots, s);
@@ -1184,11 +1400,7 @@ int solve(Problem &P, int64_t *m_out) {
   struct SideStreams {
     cudaStream_t main, *st;
     ~SideStreams() {
-      for (int k = 0; k < kSide; ++k) {
-        cudaEvent_t e = ev_sync();
-        cudaEventRecord(e, st[k]);
-        cudaStreamWaitEvent(main, e, 0);
-      }
+      for (int k = 0; k < kSide; ++k) join_streams_nothrow(main, st[k]);
     }
   } side{s, side_streams()};
   int nbatch = 0;
@@ -1196,12 +1408,14 @@ int solve(Problem &P, int64_t *m_out) {
   // the stream's next batch (stream order); a level's singletons go out in
   // pieces of at most ck_cap - 32 tasks, so the checkpoints take
   // kSide * ck_cap * nseg * 48 bytes whatever the batch sizes
-  // pieces of nslots/4 tasks (n = 20000: 69.9 -> 67.8 ms against nslots/8),
-  // capped so that the checkpoints stay within 16 GB (n = 1e5: ~nslots/7.5)
+  // pieces of (this rank's tasks)/4 (n = 20000: 69.9 -> 67.8 ms against /8),
+  // capped so that the checkpoints (64 B per 16-row segment and task) stay
+  // within scratch_bytes (16 GB by default; n = 1e5: pieces of ~nslots/10)
   const int piece_div = std::max(1, env_int("MRRR_PIECE_DIV", kSide));  // diagnostic knob
-  const int64_t ck_mem_cap = (int64_t)(16e9 / (48.0 * kSide * ((nbmax + kSeg - 1) / kSeg)));
+  const int64_t ck_mem_cap = (int64_t)(scratch_bytes / (64.0 * kSide * ((nbmax + kSeg - 1) / kSeg)));
+  const int64_t task_basis = dist ? std::min<int64_t>(nslots, wcap + 2) : nslots;
   const int64_t ck_cap =
-      std::max<int64_t>(256, std::min<int64_t>((nslots + piece_div - 1) / piece_div, ck_mem_cap)) + 32;
+      std::max<int64_t>(256, std::min<int64_t>((task_basis + piece_div - 1) / piece_div, ck_mem_cap)) + 32;
   const int nseg_v = (int)((nbmax + kSeg - 1) / kSeg);
   FwdCk *ck_f[kSide] = {};
   BwdCk *ck_b[kSide] = {};
@@ -1214,6 +1428,13 @@ int solve(Problem &P, int64_t *m_out) {
   constexpr int64_t kZB = 256;
   const bool zstream = P.hZ != nullptr && vectors && P.m_local > 0;
   cudaStream_t sc = zstream ? copy_stream() : nullptr;
+  // the copy stream rejoins the solve stream on EVERY exit (an error after
+  // some Z blocks were queued must not let the host entry free dZ, or the
+  // caller its host buffer, while a download still runs)
+  struct CopyJoin {
+    cudaStream_t main, sc;
+    ~CopyJoin() { join_streams_nothrow(main, sc); }
+  } cjoin{s, sc};
   const int64_t nzb = zstream ? (P.m_local + kZB - 1) / kZB : 0;
   std::vector<int64_t> zb_left(nzb, 0);
   std::vector<std::vector<cudaEvent_t>> zb_ev(nzb);
@@ -1335,7 +1556,19 @@ int solve(Problem &P, int64_t *m_out) {
     g_stats.kernel_launches++;
     d2h(h_run_end.data(), run_end, nslots, s);
     tr.mark("classify");
-    std::vector<int> cl_parent, cl_s0, cl_s1;
+    if (level == 0 && dist && nblocks == 1 && m > 1) {
+      // e: the shard planner -- every cut moves to the nearest root-cluster
+      // boundary within epp / 40 (identical on every rank: the root brackets
+      // were exchanged), before any vector is assigned
+      std::vector<unsigned char> free_cut(m + 1, 0);
+      for (int64_t j = 1; j < m; ++j) free_cut[j] = h_run_end[col_slot[j - 1]] != 0;
+      plan_columns(m, nr, free_cut.data(), cuts.data());
+      apply_cuts();
+    }
+    // the level's clusters: identical on every rank (the brackets are
+    // exchanged after each refinement); a rank works on the clusters that
+    // hold one of its columns ("own")
+    std::vector<int> cl_parent, cl_s0, cl_s1, own_cl;
     for (int nd : level_nodes) {
       const HostNode &H = hn[nd];
       int st = H.slot0;
@@ -1349,22 +1582,28 @@ int solve(Problem &P, int64_t *m_out) {
             }
             h_active[q] = 0;
           } else {
-            bool any = false;
-            for (int x = st; x <= q; ++x) any |= h_own[x] >= 0;
-            if (any) { cl_parent.push_back(nd); cl_s0.push_back(st); cl_s1.push_back(q + 1); }
-            else for (int x = st; x <= q; ++x) h_active[x] = 0;
+            bool wanted = false, own = false;
+            for (int x = st; x <= q; ++x) { wanted |= h_slot_out[x] >= 0; own |= h_own[x] >= 0; }
+            if (wanted) {
+              if (own) own_cl.push_back((int)cl_parent.size());
+              cl_parent.push_back(nd); cl_s0.push_back(st); cl_s1.push_back(q + 1);
+            } else {
+              for (int x = st; x <= q; ++x) h_active[x] = 0;
+            }
           }
           st = q + 1;
         }
       }
     }
-    const int ncl = (int)cl_parent.size();
-    if (vectors && (vec_mode == 0 || ncl == 0)) flush_vectors(ncl);
+    const int ncl = (int)cl_parent.size(), nown = (int)own_cl.size();
+    if (vectors && (vec_mode == 0 || ncl == 0)) guarded([&] { flush_vectors(nown); });
     if (ncl == 0) break;
-    if (level + 1 > P.o.max_depth) throw MrrrError{MRRR_ERR_DEPTH};
-    g_stats.nodes += ncl;
+    if (level + 1 > P.o.max_depth) throw MrrrError{MRRR_ERR_DEPTH};  // the same level on every rank
+    g_stats.nodes += nown;
     // grow node table
     int node_base = nnodes;
+    std::vector<int> cl_pool(ncl, -1);
+    guarded([&] {
     if (nnodes + ncl > node_cap) {
       int ncap = std::max(node_cap * 2, nnodes + ncl + 16);
       Node *nn = ar.alloc<Node>(ncap);
@@ -1373,87 +1612,127 @@ int solve(Problem &P, int64_t *m_out) {
     }
     // per-level scratch, released (to the library pool) at the end of the level
     DevArena lv(device_ws(g_ws_level));
+    std::vector<int> ocl_parent(nown), ocl_s0(nown), ocl_s1(nown);
+    for (int i = 0; i < nown; ++i) {
+      const int c = own_cl[i];
+      ocl_parent[i] = cl_parent[c]; ocl_s0[i] = cl_s0[c]; ocl_s1[i] = cl_s1[c]; cl_pool[c] = i;
+    }
     int *dcl_parent = lv.alloc<int>(ncl), *dcl_s0 = lv.alloc<int>(ncl), *dcl_s1 = lv.alloc<int>(ncl);
+    int *docl_parent = lv.alloc<int>(nown + 1), *docl_s0 = lv.alloc<int>(nown + 1), *docl_s1 = lv.alloc<int>(nown + 1);
+    int *dcl_pool = lv.alloc<int>(ncl), *down_cl = lv.alloc<int>(nown + 1);
     h2d(dcl_parent, cl_parent.data(), ncl, s);
     h2d(dcl_s0, cl_s0.data(), ncl, s);
     h2d(dcl_s1, cl_s1.data(), ncl, s);
-    // a5 cluster step: probes, six candidates, choice, chosen child (one kernel)
-    // the step's scratch (kCSRows rows of nbmax doubles per cluster) is capped
-    // at 16 GB: beyond, clusters go through in groups that reuse it (stream
-    // order; each group costs one more chain latency)
-    int cgrp = (int)std::max<int64_t>(1, std::min<int64_t>(ncl, (int64_t)(16e9 / (8.0 * kCSRows * nbmax))));
+    h2d(docl_parent, ocl_parent.data(), nown, s);
+    h2d(docl_s0, ocl_s0.data(), nown, s);
+    h2d(docl_s1, ocl_s1.data(), nown, s);
+    h2d(dcl_pool, cl_pool.data(), ncl, s);
+    h2d(down_cl, own_cl.data(), nown, s);
+    // a5 cluster step on the own clusters: probes, six candidates, choice,
+    // chosen child (one kernel).  The step's scratch (kCSRows rows of nbmax
+    // doubles per cluster) is capped at 16 GB: beyond, clusters go through in
+    // groups that reuse it (stream order; each group costs one more chain latency)
+    int cgrp = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(nown, 1), (int64_t)(scratch_bytes / (8.0 * kCSRows * nbmax))));
     if (env_int("MRRR_CS_GROUP", 0) > 0) cgrp = std::min(cgrp, env_int("MRRR_CS_GROUP", 0));  // test hook
-    double *scratch = (double *)grow_buffer(child_scratch(), (size_t)kCSRows * cgrp * nbmax * sizeof(double));
-    double *dsig = lv.alloc<double>(ncl);
-    int *dtier = lv.alloc<int>(ncl);
-    double2 *pool = ar.alloc<double2>((size_t)ncl * nbmax);  // child RRRs live until the vectors
+    double *scratch = nown ? (double *)grow_buffer(child_scratch(), (size_t)kCSRows * cgrp * nbmax * sizeof(double)) : nullptr;
+    double *dsig_own = lv.alloc<double>(nown + 1), *dsig = lv.alloc<double>(ncl);
+    int *dtier = lv.alloc<int>(nown + 1);
+    double2 *pool = ar.alloc<double2>((size_t)std::max(nown, 1) * nbmax);  // child RRRs live until the vectors
     tr.fine(s, "  alloc+upload");
-    for (int c0 = 0; c0 < ncl; c0 += cgrp) {
-      ChildArgs C{};
-      C.nodes = dnodes; C.cl_parent = dcl_parent; C.cl_s0 = dcl_s0; C.cl_s1 = dcl_s1;
-      C.lo = slo; C.hi = shi; C.LDv = LDv; C.c0 = c0; C.ncl = std::min(ncl, c0 + cgrp);
-      C.rtol = P.o.rtol_class;
-      C.scratch = scratch; C.zstride = nbmax;
-      C.pool = pool; C.stride = nbmax; C.sigma_out = dsig; C.tier_out = dtier; C.fail = dfail + 1;
-      C.ctr = ctr + 16;
-      k_child_step<<<C.ncl - c0, 32 * kCSWarps, 0, s>>>(C);
+    int h_fail[4] = {0, 0, 0, 0};
+    {
+      for (int c0 = 0; c0 < nown; c0 += cgrp) {
+        ChildArgs C{};
+        C.nodes = dnodes; C.cl_parent = docl_parent; C.cl_s0 = docl_s0; C.cl_s1 = docl_s1;
+        C.lo = slo; C.hi = shi; C.LDv = LDv; C.c0 = c0; C.ncl = std::min(nown, c0 + cgrp);
+        C.rtol = P.o.rtol_class;
+        C.scratch = scratch; C.zstride = nbmax;
+        C.pool = pool; C.stride = nbmax; C.sigma_out = dsig_own; C.tier_out = dtier; C.fail = dfail + 1;
+        C.ctr = ctr + 16;
+        k_child_step<<<C.ncl - c0, 32 * kCSWarps, 0, s>>>(C);
+        CK(cudaGetLastError());
+        g_stats.kernel_launches++;
+      }
+      tr.fine(s, "  child step");
+      g_stats.child_sweeps += 7 * nown;
+      // sigma of every cluster of the level (0 where another rank owns it:
+      // those members' brackets arrive by the exchange below)
+      CK(cudaMemsetAsync(dsig, 0, ncl * sizeof(double), s));
+      if (nown) k_scatter<<<(nown + 255) / 256, 256, 0, s>>>(down_cl, dsig_own, nown, dsig);
+      // the child node entries are written before the translate kernel reads sigma
+      k_child_nodes<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, node_base, dcl_parent, dcl_s0, dcl_s1, dsig, ncl,
+                                                   pool, nbmax, slot_j, dcl_pool);
       CK(cudaGetLastError());
-      g_stats.kernel_launches++;
+      // translate member brackets to child coordinates
+      std::vector<int> slot_cl, first_slot;
+      for (int c = 0; c < ncl; ++c)
+        for (int q = cl_s0[c]; q < cl_s1[c]; ++q) { slot_cl.push_back(c); first_slot.push_back(q); }
+      int nsn = (int)slot_cl.size();
+      int *dslot_cl = lv.alloc<int>(nsn), *dfirst = lv.alloc<int>(nsn);
+      h2d(dslot_cl, slot_cl.data(), nsn, s);
+      h2d(dfirst, first_slot.data(), nsn, s);
+      k_translate<<<(nsn + 127) / 128, 128, 0, s>>>(dslot_cl, dfirst, nsn, dsig, slo, shi, wlo, whi,
+                                                    slot_node, node_base);
+      CK(cudaGetLastError());
+      g_stats.kernel_launches += 3;
+      // verify + refine in child coordinates: chunks of rw_chunk_tree(m)
+      // members from each cluster's start -- the refinement of a chunk depends
+      // on the chunk alone, so ranks sharing a cluster compute bitwise the same
+      // brackets; a rank refines the chunks holding one of its slots (§8(e),
+      // the paper's type-3 task)
+      std::vector<Work> wv, all;
+      for (int i = 0; i < nown; ++i) {
+        const int c = own_cl[i];
+        all.clear();
+        make_work(node_base + c, cl_s0[c], cl_s1[c], rw_chunk_tree(cl_s1[c] - cl_s0[c]), all);
+        for (const Work &W : all) {
+          bool mine = !dist;
+          for (int q = W.s0; q < W.s1 && !mine; ++q) mine = h_slot_owner[q] == P.rank;
+          if (mine) wv.push_back(W);
+        }
+      }
+      Work *dwork = lv.alloc<Work>(wv.size() + 1);
+      h2d(dwork, wv.data(), wv.size(), s);
+      launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, wlo, whi, 1, P.o.rtol_class,
+                    dfail + 2, ctr + 2, ctr + 1, s, rw_m_tree);
+      tr.fine(s, "  refine");
+      d2h(h_fail, dfail, 4, s);
+      if (getenv("MRRR_DUMP")) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "L%d_pool.bin", level); dump(nm, pool, (size_t)nown * nbmax, s);
+        snprintf(nm, sizeof nm, "L%d_sigma.bin", level); dump(nm, dsig, ncl, s);
+        snprintf(nm, sizeof nm, "L%d_tier.bin", level); dump(nm, dtier, nown, s);
+        snprintf(nm, sizeof nm, "L%d_s0.bin", level); dump(nm, dcl_s0, ncl, s);
+        snprintf(nm, sizeof nm, "L%d_s1.bin", level); dump(nm, dcl_s1, ncl, s);
+        snprintf(nm, sizeof nm, "L%d_parent.bin", level); dump(nm, dcl_parent, ncl, s);
+        snprintf(nm, sizeof nm, "L%d_lo.bin", level); dump(nm, slo, nslots, s);
+        snprintf(nm, sizeof nm, "L%d_hi.bin", level); dump(nm, shi, nslots, s);
+      }
+      if (h_fail[1]) throw MrrrError{MRRR_ERR_CHILD};
+      if (h_fail[2]) throw MrrrError{MRRR_ERR_CONVERGE};
+      if (dist && env_int("MRRR_TEST_FAIL_RANK", -1) == P.rank && level == env_int("MRRR_TEST_FAIL_LEVEL", 0))
+        throw MrrrError{MRRR_ERR_CHILD};  // test hook: one rank fails alone (tests/test_gpu_dist.py)
     }
-    tr.fine(s, "  child step");
-    g_stats.child_sweeps += 6 * ncl + ncl;
-    // the child node entries are written before the translate kernel reads sigma
-    int *slot_jl = slot_j;
-    k_child_nodes<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, node_base, dcl_parent, dcl_s0, dcl_s1, dsig,
-                                                 ncl, pool, nbmax, slot_jl);
-    CK(cudaGetLastError());
-    // translate member brackets to child coordinates
-    std::vector<int> slot_cl, first_slot;
-    for (int c = 0; c < ncl; ++c)
-      for (int q = cl_s0[c]; q < cl_s1[c]; ++q) { slot_cl.push_back(c); first_slot.push_back(q); }
-    int nsn = (int)slot_cl.size();
-    int *dslot_cl = lv.alloc<int>(nsn), *dfirst = lv.alloc<int>(nsn);
-    h2d(dslot_cl, slot_cl.data(), nsn, s);
-    h2d(dfirst, first_slot.data(), nsn, s);
-    k_translate<<<(nsn + 127) / 128, 128, 0, s>>>(dslot_cl, dfirst, nsn, dsig, slo, shi, wlo, whi,
-                                                  slot_node, node_base);
-    CK(cudaGetLastError());
-    g_stats.kernel_launches += 2;
-    // host mirror
+    });  // guarded: reported at the exchange below, where every rank stops
+    // e: the level's exchange -- every rank gets the brackets of all members
+    // (and the check that all ranks agree on the tree: the global cluster
+    // count); an error on any rank stops all ranks here
+    if (dist) {
+      const double mx = exchange_brackets((double)ncl);
+      if ((int)mx != ncl) throw MrrrError{MRRR_ERR_COMM};
+    }
+    // host mirror (every rank keeps the whole tree's structure: the next
+    // level's clusters are classified from the exchanged brackets, so all
+    // ranks list the same clusters and run the same number of levels)
     hn.resize(nnodes + ncl);
     for (int c = 0; c < ncl; ++c) {
       hn[node_base + c] = {cl_s0[c], cl_s1[c], hn[cl_parent[c]].depth + 1, hn[cl_parent[c]].block};
       for (int q = cl_s0[c]; q < cl_s1[c]; ++q) h_slot_node[q] = node_base + c;
     }
     nnodes += ncl;
-    // verify + refine in child coordinates
-    std::vector<Work> wv;
-    // chunks of rw_chunk(m) members from each cluster's start: the refinement of
-    // a cluster depends on the cluster alone, so every rank that holds a
-    // shared cluster computes bitwise the same child intervals (§8(e))
-    for (int c = 0; c < ncl; ++c) make_work(node_base + c, cl_s0[c], cl_s1[c], rw_chunk_tree(cl_s1[c] - cl_s0[c]), wv);
-    Work *dwork = lv.alloc<Work>(wv.size());
-    h2d(dwork, wv.data(), wv.size(), s);
-    launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, wlo, whi, 1, P.o.rtol_class,
-                  dfail + 2, ctr + 2, ctr + 1, s, rw_m_tree);
-    tr.fine(s, "  refine");
-    d2h(h_fail, dfail, 4, s);
-    if (getenv("MRRR_DUMP")) {
-      char nm[64];
-      snprintf(nm, sizeof nm, "L%d_pool.bin", level); dump(nm, pool, (size_t)ncl * nbmax, s);
-      snprintf(nm, sizeof nm, "L%d_sigma.bin", level); dump(nm, dsig, ncl, s);
-      snprintf(nm, sizeof nm, "L%d_tier.bin", level); dump(nm, dtier, ncl, s);
-      snprintf(nm, sizeof nm, "L%d_s0.bin", level); dump(nm, dcl_s0, ncl, s);
-      snprintf(nm, sizeof nm, "L%d_s1.bin", level); dump(nm, dcl_s1, ncl, s);
-      snprintf(nm, sizeof nm, "L%d_parent.bin", level); dump(nm, dcl_parent, ncl, s);
-      snprintf(nm, sizeof nm, "L%d_lo.bin", level); dump(nm, slo, nslots, s);
-      snprintf(nm, sizeof nm, "L%d_hi.bin", level); dump(nm, shi, nslots, s);
-    }
-    if (h_fail[1]) throw MrrrError{MRRR_ERR_CHILD};
-    if (h_fail[2]) throw MrrrError{MRRR_ERR_CONVERGE};
     if (tr.on) {
       char buf[96];
-      snprintf(buf, sizeof buf, "level %d: %d clusters", level, ncl);
+      snprintf(buf, sizeof buf, "level %d: %d clusters (%d here)", level, ncl, nown);
       tr.mark(buf);
     }
     level_nodes.clear();
@@ -1476,6 +1755,7 @@ int solve(Problem &P, int64_t *m_out) {
       CK(cudaStreamWaitEvent(s, j, 0));
     }
   }
+  guarded([&] {
   if (ntask > 0) {
     VecTask *dt = ar.alloc<VecTask>(ntask);
     h2d(dt, tasks.data(), ntask, s);
@@ -1522,6 +1802,11 @@ int solve(Problem &P, int64_t *m_out) {
         launch_refine(dnodes, dw, (int)wv.size(), dslots, slot_j, slo, shi, nullptr, nullptr, 0, 4.0 * kEps,
                       dfail + 2, ctr + 2, ctr + 1, s);
         kt_fin.stop(s);
+        {
+          int hf[4];
+          d2h(hf, dfail, 4, s);
+          if (hf[2]) throw MrrrError{MRRR_ERR_CONVERGE};  // the fallback's bisection did not converge
+        }
         VecTask *dft = ar.alloc<VecTask>(h_nf);
         h2d(dft, ft.data(), h_nf, s);
         WarpItem *dfi = ar.alloc<WarpItem>(fitems.size());
@@ -1573,6 +1858,7 @@ int solve(Problem &P, int64_t *m_out) {
     CK(cudaGetLastError());
     g_stats.kernel_launches++;
   }
+  });
   finish_w();
   d2h(h_ctr, ctr, 32, s);
   if (tr.on)
@@ -1842,6 +2128,15 @@ int mrrr_negcount(int64_t nb, const double *D, const double *LLD, int64_t k, con
     cudaGetLastError();
     return ce.e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;
   }
+}
+
+int mrrr_plan_columns(int64_t m, int nranks, const unsigned char *free_cut, int64_t *cuts) {
+  if (m < 0) return -1;
+  if (nranks < 1) return -2;
+  if (m > 0 && !free_cut) return -3;
+  if (!cuts) return -4;
+  plan_columns(m, nranks, free_cut, cuts);
+  return 0;
 }
 
 int mrrr_trim_workspace(void) {

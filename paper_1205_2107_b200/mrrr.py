@@ -83,6 +83,8 @@ def lib():
         L.mrrr_negcount.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                     C.c_void_p, C.c_int, C.c_void_p]
         L.mrrr_negcount.restype = C.c_int
+        L.mrrr_plan_columns.argtypes = [C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
+        L.mrrr_plan_columns.restype = C.c_int
         L.mrrr_trim_workspace.restype = C.c_int
         _lib = L
     return _lib
@@ -110,6 +112,18 @@ def _range_args(n, il, iu, vl, vu):
     return RANGE_ALL, 0.0, 0.0, 0, 0, n
 
 
+def _check_out(t, k, device, name, n=None):
+    """Caller-supplied output buffers: float64, contiguous, on d's device, with
+    room for k eigenvalues (w) or k columns of length n (Z as (k', n), k' >= k)."""
+    if t.dtype != torch.float64 or not t.is_contiguous() or t.device != device:
+        raise TypeError(f"{name} must be a contiguous float64 tensor on {device}")
+    if n is None:
+        if t.numel() < k:
+            raise ValueError(f"{name} holds {t.numel()} < {k} eigenvalues")
+    elif t.dim() != 2 or t.shape[1] != n or t.shape[0] < k:
+        raise ValueError(f"{name} must have shape (>= {k}, {n}) (column j of the result is row j)")
+
+
 def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
 
@@ -132,12 +146,20 @@ def stemr(d: torch.Tensor, e: torch.Tensor, *, il=None, iu=None, vl=None, vu=Non
     e = e.contiguous() if n > 1 else d
     rng, a, b, ilv, iuv, kcap = _range_args(n, il, iu, vl, vu)
     kcap = max(kcap, 1)
+    if stream is None:
+        stream = torch.cuda.current_stream(d.device)
+    if rng == RANGE_VALUE and vectors and Z is None:
+        # size Z to the eigenvalues in (vl, vu]: a values-only solve counts them
+        # first (instead of an n x n buffer: 80 GB at n = 1e5)
+        wv, _ = stemr(d, e, vl=vl, vu=vu, vectors=False, opts=opts, stream=stream)
+        kcap = max(int(wv.shape[0]), 1)
     if w is None:
         w = torch.empty(kcap, dtype=torch.float64, device=d.device)
     if vectors and Z is None:
         Z = torch.empty((kcap, n), dtype=torch.float64, device=d.device)
-    if stream is None:
-        stream = torch.cuda.current_stream(d.device)
+    _check_out(w, kcap, d.device, "w")
+    if vectors:
+        _check_out(Z, kcap, d.device, "Z", n)
     m = C.c_int64(0)
     o = opts if opts is not None else default_opts()
     with torch.cuda.device(d.device):
@@ -156,15 +178,27 @@ def stemr_host(d, e, *, il=None, iu=None, vl=None, vu=None, w=None, Z=None, vect
     tensors ``d``, ``e`` (pinned for speed); returns host ``(w, Z)`` with the
     same layout as :func:`stemr`.  The copies and the solve run inside the
     library on ``stream`` (default: the current CUDA stream)."""
-    if d.is_cuda or d.dtype != torch.float64:
-        raise TypeError("stemr_host takes float64 host tensors")
     n = d.shape[0]
+    for t, nm in ((d, "d"), (e, "e")):
+        if nm == "e" and n <= 1:
+            continue
+        if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+            raise TypeError(f"stemr_host takes contiguous float64 host tensors ({nm})")
+    if n > 1 and e.shape[0] < n - 1:
+        raise ValueError("e needs n - 1 entries")
     rng, a, b, ilv, iuv, kcap = _range_args(n, il, iu, vl, vu)
     kcap = max(kcap, 1)
     if w is None:
         w = torch.empty(kcap, dtype=torch.float64, pin_memory=True)
     if vectors and Z is None:
         Z = torch.empty((kcap, n), dtype=torch.float64, pin_memory=True)
+    for t, nm, nn in ((w, "w", None), (Z if vectors else None, "Z", n)):
+        if t is None:
+            continue
+        if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+            raise TypeError(f"{nm} must be a contiguous float64 host tensor")
+        if (nn is None and t.numel() < kcap) or (nn is not None and (t.dim() != 2 or t.shape[1] != n or t.shape[0] < kcap)):
+            raise ValueError(f"{nm} is too small for {kcap} eigenpairs")
     if stream is None:
         stream = torch.cuda.current_stream()
     m = C.c_int64(0)
@@ -179,6 +213,25 @@ def stemr_host(d, e, *, il=None, iu=None, vl=None, vu=None, w=None, Z=None, vect
     return w[:k], (Z[:k].T if vectors else None)
 
 
+def plan_columns(m: int, nranks: int, free_cut) -> list:
+    """The library's shard planner (``mrrr_plan_columns``): the column cuts
+    [c_0 = 0, ..., c_P = m] after moving each static cut to the nearest
+    cluster boundary (``free_cut[j]`` true: boundary between columns j-1, j)
+    within ceil(m/P)/40.  Host only."""
+    fc = (C.c_ubyte * (m + 1))(*[1 if x else 0 for x in list(free_cut)[:m + 1]] + [0] * max(0, m + 1 - len(free_cut)))
+    cuts = (C.c_int64 * (nranks + 1))()
+    rc = lib().mrrr_plan_columns(m, nranks, C.cast(fc, C.c_void_p), C.cast(cuts, C.c_void_p))
+    if rc != 0:
+        raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
+    return list(cuts)
+
+
+def dist_capacity(k: int, nranks: int) -> int:
+    """Columns Z_local must hold: ceil(k/P) + ceil(k/P)/20 (the planner's slack)."""
+    epp = (k + max(nranks, 1) - 1) // max(nranks, 1)
+    return max(epp + epp // 20, 1)
+
+
 def shard_columns(m: int, nranks: int, rank: int):
     """Columns [c0, c1) of the m wanted eigenpairs owned by `rank` (the static
     division of PAPER.md L1139-1146 as mrrr_stemr_dist applies it:
@@ -189,16 +242,23 @@ def shard_columns(m: int, nranks: int, rank: int):
 
 
 class _DevBuf:
-    """Zero-copy view of a device buffer for torch.as_tensor (fp64)."""
+    """Zero-copy view of a device buffer for torch.as_tensor: fp64 by default,
+    bytes with ``typestr="|u1"`` (the library's exchanges are byte counts)."""
 
-    def __init__(self, ptr: int, nbytes: int):
-        self.__cuda_array_interface__ = {"shape": (nbytes // 8,), "typestr": "<f8",
+    def __init__(self, ptr: int, nbytes: int, typestr: str = "<f8"):
+        size = nbytes if typestr == "|u1" else nbytes // 8
+        self.__cuda_array_interface__ = {"shape": (size,), "typestr": typestr,
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
 def _ext_stream(handle):
     """torch stream object for a raw cudaStream_t handle (0/None: the legacy default stream)."""
     return torch.cuda.ExternalStream(handle) if handle else torch.cuda.default_stream()
+
+
+def _host_bytes(ptr: int, nbytes: int):
+    arr = (C.c_uint8 * nbytes).from_address(ptr)
+    return torch.frombuffer(arr, dtype=torch.uint8)
 
 
 def _host_view(ptr: int, nbytes: int):
@@ -224,14 +284,14 @@ def torch_allgather(group=None, device: str = "cuda"):
                 # include/mrrr.h): ordered after the kernels that wrote `send`
                 # and before the library's reads of `recv`
                 with torch.cuda.stream(_ext_stream(stream)):
-                    st = torch.as_tensor(_DevBuf(send, nbytes), device="cuda")
-                    rt = torch.as_tensor(_DevBuf(recv, nbytes * world), device="cuda")
+                    st = torch.as_tensor(_DevBuf(send, nbytes, "|u1"), device="cuda")
+                    rt = torch.as_tensor(_DevBuf(recv, nbytes * world, "|u1"), device="cuda")
                     dist.all_gather_into_tensor(rt, st, group=group)
             else:
-                st = _host_view(send, nbytes)
+                st = _host_bytes(send, nbytes)
                 parts = [torch.empty_like(st) for _ in range(world)]
                 dist.all_gather(parts, st, group=group)
-                _host_view(recv, nbytes * world).copy_(torch.cat(parts))
+                _host_bytes(recv, nbytes * world).copy_(torch.cat(parts))
             return 0
         except Exception:  # reported as MRRR_ERR_COMM by the library
             return 1
@@ -241,11 +301,13 @@ def torch_allgather(group=None, device: str = "cuda"):
 def stemr_dist(d: torch.Tensor, e: torch.Tensor, *, il=None, iu=None, vl=None, vu=None,
                vectors: bool = True, opts: Opts | None = None, group=None, rank=None,
                nranks=None, allgather=None, stream=None):
-    """Sharded MRRR (``mrrr_stemr_dist``): every rank passes the same T and
-    range; returns ``(w_all, Z_local, col_begin)`` where ``w_all`` holds all m
-    eigenvalues on every rank and ``Z_local`` (n, m_local) the eigenvectors of
-    columns ``col_begin .. col_begin + m_local`` (this rank's static share).
-    The only collective is the all-gather of w (torch.distributed by default)."""
+    """Sharded MRRR (``mrrr_stemr_dist``): every rank passes the
+    same T and range; returns ``(w_all, Z_local, col_begin)`` where ``w_all``
+    holds all m eigenvalues on every rank and ``Z_local`` (n, m_local) the
+    eigenvectors of columns ``col_begin .. col_begin + m_local`` (this rank's
+    share: the static division with its cuts moved to cluster boundaries).
+    The collectives (root grid, root brackets, one bracket exchange per tree
+    level, w) go through ``allgather`` (torch.distributed NCCL by default)."""
     import torch.distributed as dist
     if not (d.is_cuda and d.dtype == torch.float64):
         raise TypeError("d must be a torch.float64 CUDA tensor (no CPU fallback)")
@@ -258,9 +320,8 @@ def stemr_dist(d: torch.Tensor, e: torch.Tensor, *, il=None, iu=None, vl=None, v
     e = e.contiguous() if n > 1 else d
     rng, a, b, ilv, iuv, kcap = _range_args(n, il, iu, vl, vu)
     kcap = max(kcap, 1)
-    epp = (kcap + max(nranks, 1) - 1) // max(nranks, 1)
     w_all = torch.empty(kcap, dtype=torch.float64, device=d.device)
-    Zl = torch.empty((max(epp, 1), n), dtype=torch.float64, device=d.device) if vectors else None
+    Zl = torch.empty((dist_capacity(kcap, nranks), n), dtype=torch.float64, device=d.device) if vectors else None
     if stream is None:
         stream = torch.cuda.current_stream(d.device)
     cb = allgather if allgather is not None else torch_allgather(group)

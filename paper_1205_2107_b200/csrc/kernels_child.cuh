@@ -35,7 +35,7 @@ namespace mrrr {
 constexpr int kCT = 16;     // rows per tile
 constexpr int kCRing = 6;   // tiles in flight per warp
 constexpr int kCSWarps = 5; // 4 probe chains + the candidate warp
-constexpr int kCSRows = 16; // scratch rows per cluster: D+ of 6 candidates, 4 per probe, |z| of 2
+constexpr int kCSRows = 17; // scratch rows per cluster: t of 6 candidates, 4 per probe, |z| of 2, q every 8 rows
 
 struct ChainRing {
   double2 rDL[kCRing][kCT];  // (D, LLD)
@@ -98,23 +98,25 @@ __device__ __forceinline__ void cs_probe_fwd(ChainRing &R, const double2 *DL, co
     __syncwarp();
     const int slot = c % kCRing, r0 = c * kCT, rows = min(kCT, nb - r0);
     double kp = 0.0, kq = 1.0, kt = 1.0, kld = 0.0;
-    auto row = [&](int k, bool last_check) {
+    auto row = [&](const double2 v, int k, bool last_check) {
       const int i = r0 + k;
-      const double2 v = R.rDL[slot][k];
-      const double ld = R.rLD[slot][k].x;
       const double tt = fma(v.x, q, p);
-      if (lane == k) { kp = p; kq = q; kt = tt; kld = ld; }
+      if (lane == k) { kp = p; kq = q; kt = tt; }
       if (!last_check || i < nb - 1) { p = fma(-lam, tt, v.y * p); q = tt; }
       if ((k & 7) == 7) {
         const double f = pow2_scale(min(max(max_exp(p, q), 1), 2045));
         p *= f; q *= f;
       }
     };
+    if (lane < kCT) kld = R.rLD[slot][lane].x;
     if (rows == kCT && r0 + kCT < nb) {  // every row of the tile is below nb - 1
+      double2 v[kCT];  // the tile's rows in registers before the dependent steps
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) row(k, false);
+      for (int k = 0; k < kCT; ++k) v[k] = R.rDL[slot][k];
+#pragma unroll
+      for (int k = 0; k < kCT; ++k) row(v[k], k, false);
     } else {
-      for (int k = 0; k < rows; ++k) row(k, true);
+      for (int k = 0; k < rows; ++k) row(R.rDL[slot][k], k, true);
     }
     if (lane < rows) {
       const int i = r0 + lane;
@@ -142,23 +144,25 @@ __device__ __forceinline__ void cs_probe_bwd(ChainRing &R, const double2 *DL, co
     const int slot = c % kCRing, r0 = (ntile - 1 - c) * kCT;
     const int top = min(r0 + kCT, nb - 1) - 1;  // rows r0 .. top step (row i from i+1)
     double kb = 1.0, ku = 1.0, ka = 0.0, kld = 0.0;
-    auto row = [&](int k) {
-      const double2 v = R.rDL[slot][k];
-      const double ld = R.rLD[slot][k].x;
+    auto row = [&](const double2 v, int k) {
       const double u = fma(v.y, b, a);
       const double an = fma(-lam, u, v.x * a);
-      if (lane == k) { kb = b; ku = u; ka = an; kld = ld; }
+      if (lane == k) { kb = b; ku = u; ka = an; }
       a = an; b = u;
       if ((k & 7) == 0) {
         const double f = pow2_scale(min(max(max_exp(a, b), 1), 2045));
         a *= f; b *= f;
       }
     };
+    if (lane < kCT) kld = R.rLD[slot][lane].x;
     if (top - r0 + 1 == kCT) {
+      double2 v[kCT];  // the tile's rows in registers before the dependent steps
 #pragma unroll
-      for (int k = kCT - 1; k >= 0; --k) row(k);
+      for (int k = 0; k < kCT; ++k) v[k] = R.rDL[slot][k];
+#pragma unroll
+      for (int k = kCT - 1; k >= 0; --k) row(v[k], k);
     } else {
-      for (int k = top - r0; k >= 0; --k) row(k);
+      for (int k = top - r0; k >= 0; --k) row(R.rDL[slot][k], k);
     }
     if (lane <= top - r0) {
       const int i = r0 + lane;
@@ -173,22 +177,29 @@ __device__ __forceinline__ void cs_probe_bwd(ChainRing &R, const double2 *DL, co
 }
 
 // The six candidate chains (lane k < 6 runs shift sig[k]; the other lanes
-// repeat lane 0's); DP[k * zstride + i] = D+_i of candidate k.
+// repeat lane 0's): TP[k * zstride + i] = t_i (= D+_i q_i) and, every 8 rows,
+// QK[k * (zstride / 8) + i / 8] = q_i.  The chain does no division: D+_i =
+// t_i / q_i with q_i = t_{i-1} (or QK where the chain rescaled, i % 8 == 0)
+// is formed later by all the CTA's threads (cs_dplus) -- the candidate warp
+// is the step's critical chain.  Each tile's 16 rows are read into registers
+// before the dependent steps.
 __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const double2 *DL, int nb,
-                                              double sigma, int lane, double *DP, int64_t zstride) {
+                                              double sigma, int lane, double *TP, double *QK, int64_t zstride) {
   const int ntile = (nb + kCT - 1) / kCT;
 #pragma unroll
   for (int k = 0; k < kCRing - 1; ++k) cs_issue(R, DL, nullptr, nb, k < ntile ? k : -1, k, lane, false);
   double p = -sigma, q = 1.0;
+  const int cand = lane < 6 ? lane : 0;
+  double *tp = TP + cand * zstride, *qk = QK + cand * (zstride / 8);
   for (int c = 0; c < ntile; ++c) {
     __pipeline_wait_prior(kCRing - 2);
     __syncwarp();
     const int slot = c % kCRing, r0 = c * kCT, rows = min(kCT, nb - r0);
-    auto row = [&](int k, bool last_check) {
+    auto row = [&](const double2 v, int k, bool last_check) {
       const int i = r0 + k;
-      const double2 v = R.rDL[slot][k];
+      if ((k & 7) == 0 && lane < 6) qk[i >> 3] = q;
       const double tt = fma(v.x, q, p);
-      if (lane < 6) { S.tq[0][k][lane] = tt; S.tq[1][k][lane] = q; }
+      if (lane < 6) S.tq[0][k][lane] = tt;
       if (!last_check || i < nb - 1) { p = fma(-sigma, tt, v.y * p); q = tt; }
       if ((k & 7) == 7) {
         const double f = pow2_scale(min(max(max_exp(p, q), 1), 2045));
@@ -196,17 +207,20 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
       }
     };
     if (rows == kCT && r0 + kCT < nb) {  // every row of the tile is below nb - 1
+      double2 v[kCT];
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) row(k, false);
+      for (int k = 0; k < kCT; ++k) v[k] = R.rDL[slot][k];
+#pragma unroll
+      for (int k = 0; k < kCT; ++k) row(v[k], k, false);
     } else {
-      for (int k = 0; k < rows; ++k) row(k, true);
+      for (int k = 0; k < rows; ++k) row(R.rDL[slot][k], k, true);
     }
     __syncwarp();
-    // D+_i = t_i / q_i, 96 divisions spread over the warp (off the chains)
+    // the tile's t values, coalesced: 96 stores spread over the warp
 #pragma unroll
     for (int e = lane; e < 6 * kCT; e += 32) {
       const int cc = e >> 4, k = e & (kCT - 1);
-      if (k < rows) DP[cc * zstride + r0 + k] = div_nr(S.tq[0][k][cc], S.tq[1][k][cc]);
+      if (k < rows) TP[cc * zstride + r0 + k] = S.tq[0][k][cc];
     }
     __syncwarp();
     const int cn = c + kCRing - 1;
@@ -215,7 +229,15 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
   __pipeline_wait_prior(0);
 }
 
-__global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
+// D+_i of candidate k from its stored t (cs_candidates): the same quotient
+// t_i / q_i the chain's state held, bit for bit.
+__device__ __forceinline__ double cs_dplus(const double *TP, const double *QK, int64_t zstride, int k, int i) {
+  const double *tp = TP + k * zstride;
+  const double q = (i & 7) == 0 ? QK[k * (zstride / 8) + (i >> 3)] : tp[i - 1];
+  return div_nr(tp[i], q);
+}
+
+__global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
   __shared__ ChildSmem S;
   const int c = A.c0 + blockIdx.x;
   if (c >= A.ncl) return;
@@ -226,9 +248,10 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
   const double2 *DL = P.DL, *LD = A.LDv + P.row0;
   const int64_t zs = A.zstride;
   double *base = A.scratch + (int64_t)blockIdx.x * kCSRows * zs;
-  double *DP = base;                 // 6 candidates
+  double *TP = base;                 // 6 candidates' t
   double *pr[2] = {base + 6 * zs, base + 10 * zs};  // per probe: s, P, rho, sig
   double *zl = base + 14 * zs, *zr = base + 15 * zs;
+  double *QK = base + 16 * zs;       // 6 candidates' q every 8 rows (zs / 8 each)
 
   // ---- phase 1: the five chains
   const long long clk_p0 = clock64();
@@ -252,7 +275,7 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
       const double dr = fmax(fmax(2.0 * (h - l), 2.0 * A.rtol * fabs(h)), 4.0 * kEps * fabs(h));
       sigma = h + mult * dr;
     }
-    cs_candidates(S.ring[4], S, DL, nb, sigma, lane, DP, zs);
+    cs_candidates(S.ring[4], S, DL, nb, sigma, lane, TP, QK, zs);
     if (lane < 6) S.sig[lane] = sigma;
   }
   if (lane == 0) atomicMax(&A.ctr[1 + (wid == 4 ? 1 : (wid & 1) ? 2 : 3)], (unsigned long long)(clock64() - clk_p0));
@@ -267,7 +290,7 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
     double *z = side == 0 ? zl : zr;
     double bv = CUDART_INF;
     int bi = nb;
-#pragma unroll 4
+#pragma unroll 8
     for (int i = gt; i < nb; i += 64) {
       const double g = fabs(sS[i] + sP[i] + lam);
       if (g < bv) { bv = g; bi = i; }  // ascending i per thread: first minimum kept
@@ -284,16 +307,17 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
     const int i0 = S.am_i[2 * side], i1 = S.am_i[2 * side + 1];
     int r = (v1 < v0 || (v1 == v0 && i1 < i0)) ? i1 : i0;
     if (r >= nb) r = nb - 1;  // no finite gamma: any twist (the vector only weights)
-    // |z| by a two-level product scan of |ratio| in (mantissa, exponent)
-    // form -- m in [1, 2), the exponent a double (exact integers) -- so no
-    // product over- or underflows and no transcendental is evaluated: lane l
-    // owns a contiguous run of the side's ratios (product, warp scan of the
-    // products, second walk writing z).  A zero or non-finite ratio zeroes
-    // the rest of that side (as a log of -inf would).
+    // |z| by a product scan of |ratio| in (mantissa, exponent) form -- m in
+    // [1, 2), the exponent a double (exact integers) -- so no product over-
+    // or underflows and no transcendental is evaluated.  Blocked warp scan:
+    // each step the 32 lanes load 32 consecutive ratios (coalesced, 8 blocks
+    // of loads in flight), scan them across the warp and fold in the running
+    // carry; one pass writes z.  (Round 1 walked one contiguous run per lane
+    // twice: dependent loads, 35 % of the step's samples at level 0.)  A zero
+    // or non-finite ratio zeroes the rest of that side (as a log of -inf would).
     const bool up = (wid & 1) == 0;     // up: rows r-1 .. 0 from rho; down: rows r+1 .. nb-1 from sig
     const int m = up ? r : nb - 1 - r;  // ratios on this side
     if (up && lane == 0) z[r] = 1.0;
-    const int chunk = (m + 31) >> 5, j0 = min(lane * chunk, m), j1 = min(j0 + chunk, m);
     constexpr double kDead = -1.0e9;    // exponent of a zeroed product
     auto split = [](double x, double &mm, double &ee) {  // |x| = mm 2^ee, mm in [1, 2)
       const long long b = __double_as_longlong(x) & 0x7fffffffffffffffLL;
@@ -306,29 +330,39 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
       mm *= m2; ee += e2;
       if (mm >= 2.0) { mm *= 0.5; ee += 1.0; }
     };
-    auto lval = [&](int j, double &mm, double &ee) { split(up ? sR[r - 1 - j] : sG[r + j], mm, ee); };
-    double pm = 1.0, pe = 0.0;
-#pragma unroll 8
-    for (int j = j0; j < j1; ++j) {
-      double a, b;
-      lval(j, a, b);
-      mul(pm, pe, a, b);
-    }
-    double im = pm, ie = pe;  // inclusive scan over the lanes
-    for (int o = 1; o < 32; o <<= 1) {
-      const double ym = __shfl_up_sync(0xffffffffu, im, o), ye = __shfl_up_sync(0xffffffffu, ie, o);
-      if (lane >= o) mul(im, ie, ym, ye);
-    }
-    double am = __shfl_up_sync(0xffffffffu, im, 1), ae = __shfl_up_sync(0xffffffffu, ie, 1);
-    if (lane == 0) { am = 1.0; ae = 0.0; }  // exclusive prefix of this lane's run
-#pragma unroll 8
-    for (int j = j0; j < j1; ++j) {
-      double a, b;
-      lval(j, a, b);
-      mul(am, ae, a, b);
-      const double zz = ae < -1100.0 ? 0.0 : (ae > 1100.0 ? CUDART_INF : ldexp(am, (int)ae));
-      if (up) z[r - 1 - j] = zz;
-      else z[r + j + 1] = zz;
+    auto to_double = [](double mm, double ee) {  // mm 2^ee, 0 below the normal range (weights only)
+      if (ee < -1022.0) return 0.0;
+      if (ee > 1023.0) return CUDART_INF;
+      const int ei = (int)ee;
+      return __hiloint2double(__double2hiint(mm) + (ei << 20), __double2loint(mm));
+    };
+    const double *src = up ? sR + (r - 1) : sG + r;  // x_j = |src[dir * j]|
+    const int dir = up ? -1 : 1;
+    double *dst = up ? z + (r - 1) : z + (r + 1);
+    double cm = 1.0, ce = 0.0;  // carry: product of all earlier blocks
+    constexpr int kBlk = 8;
+    for (int base = 0; base < m; base += 32 * kBlk) {
+      double xv[kBlk];
+#pragma unroll
+      for (int u = 0; u < kBlk; ++u) {
+        const int j = base + u * 32 + lane;
+        xv[u] = j < m ? src[dir * j] : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kBlk; ++u) {
+        const int j = base + u * 32 + lane;
+        double im, ie;
+        split(xv[u], im, ie);
+        if (j >= m) { im = 1.0; ie = 0.0; }
+        for (int o = 1; o < 32; o <<= 1) {  // inclusive scan over the 32 lanes
+          const double ym = __shfl_up_sync(0xffffffffu, im, o), ye = __shfl_up_sync(0xffffffffu, ie, o);
+          if (lane >= o) mul(im, ie, ym, ye);
+        }
+        mul(im, ie, cm, ce);
+        if (j < m) dst[dir * j] = to_double(im, ie);
+        cm = __shfl_sync(0xffffffffu, im, 31);
+        ce = __shfl_sync(0xffffffffu, ie, 31);
+      }
     }
   }
   __syncthreads();
@@ -341,13 +375,14 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
   unsigned okm = 0x3f;
 #pragma unroll
   for (int k = 0; k < 6; ++k) { g[k] = 0.0; nl[k] = 0.0; nr[k] = 0.0; }
+#pragma unroll 4
   for (int i = tid; i < nb; i += 32 * kCSWarps) {
     const double a = zl[i], b = zr[i];
     const double a2 = a * a, b2 = b * b;
     dnl += a2; dnr += b2;
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-      const double d = DP[k * zs + i];
+      const double d = cs_dplus(TP, QK, zs, k, i);
       const double ad = fabs(d);
       if (!(isfinite(d) && d != 0.0)) okm &= ~(1u << k);
       g[k] = fmax(g[k], ad);
@@ -417,11 +452,10 @@ __global__ void __launch_bounds__(32 * kCSWarps) k_child_step(ChildArgs A) {
 
   // ---- phase 5: the chosen child, (D+_i, LLD+_i = LD_i^2 / D+_i), coalesced
   double2 *out = A.pool + (int64_t)c * A.stride;
-  const double *dp = DP + best * zs;
   bool bad = false;
 #pragma unroll 4
   for (int i = tid; i < nb; i += 32 * kCSWarps) {
-    const double Dp = dp[i];
+    const double Dp = cs_dplus(TP, QK, zs, best, i);
     const double lld = (i < nb - 1) ? __ldg(&LD[i]).y / Dp : 0.0;
     bad |= !isfinite(Dp) || Dp == 0.0 || !isfinite(lld);
     out[i] = make_double2(Dp, lld);

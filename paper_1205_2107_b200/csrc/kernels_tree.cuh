@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(32) k_root_chain_warp(const double *__restrict
   for (int attempt = 0; attempt <= 6; ++attempt) {
     const double sigma = B.side > 0 ? B.gl - delta : B.gu + delta;
     double tm1 = 1.0, tm2 = 0.0;
+    double tlast = 1.0;  // t of the previous tile's last row (t_{-1} = 1)
     bool ok = true;
 #pragma unroll
     for (int k = 0; k < kRCRing - 1; ++k) issue(k);
@@ -234,13 +235,11 @@ __global__ void __launch_bounds__(32) k_root_chain_warp(const double *__restrict
       const int slot = t % kRCRing, r0 = t * kRCT, rows = min(kRCT, nb - r0);
       double kt = 0.0;
       int ks = 0;
-      auto row = [&](int k) {
+      // the dependent chain only: t_i = (d_i - sigma) t_{i-1} - e_{i-1}^2 t_{i-2};
+      // the definiteness of the tile's rows is checked after it, lane-parallel
+      auto row = [&](int k, double di, double b2) {
         const int i = r0 + k;
-        const double di = rD[slot][k];
-        const double b2 = (i > 0) ? rE[slot][k] : 0.0;
         const double tt = fma(di - sigma, tm1, -b2 * tm2);
-        const bool good = (tt != 0.0) && ((B.side > 0) ? (negbit(tt, tm1) == 0) : (negbit(tt, tm1) == 1));
-        ok &= good && isfinite(tt);
         int sh = 0;
         tm2 = tm1; tm1 = tt;
         if ((i & 7) == 7) {
@@ -253,11 +252,22 @@ __global__ void __launch_bounds__(32) k_root_chain_warp(const double *__restrict
         if (lane == k) { kt = tt; ks = sh; }
       };
       if (rows == kRCT) {
+        double dv[kRCT], bv[kRCT];  // the tile's rows in registers before the chain
 #pragma unroll
-        for (int k = 0; k < kRCT; ++k) row(k);
+        for (int k = 0; k < kRCT; ++k) { dv[k] = rD[slot][k]; bv[k] = (r0 + k > 0) ? rE[slot][k] : 0.0; }
+#pragma unroll
+        for (int k = 0; k < kRCT; ++k) row(k, dv[k], bv[k]);
       } else {
-        for (int k = 0; k < rows; ++k) row(k);
+        for (int k = 0; k < rows; ++k) row(k, rD[slot][k], (r0 + k > 0) ? rE[slot][k] : 0.0);
       }
+      // row r0 + lane: D_i = t_i / t_{i-1} must be finite, non-zero and of the
+      // side's sign (the rescale factors are positive: signs are unchanged)
+      const double tp = __shfl_up_sync(0xffffffffu, kt, 1);
+      const double tprev = lane == 0 ? tlast : tp;
+      const bool good = lane >= rows || (kt != 0.0 && isfinite(kt) &&
+                                         ((B.side > 0) ? (negbit(kt, tprev) == 0) : (negbit(kt, tprev) == 1)));
+      ok &= __all_sync(0xffffffffu, good);
+      tlast = __shfl_sync(0xffffffffu, kt, rows - 1);
       if (lane < rows) { tbuf[B.row0 + r0 + lane] = kt; sbuf[B.row0 + r0 + lane] = ks; }
       __syncwarp();
       issue(t + kRCRing - 1);
@@ -517,11 +527,13 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
       const int rows = min(kRWT, body - t * kRWT);
       if (any) {
         if (rows == kRWT) {
+          double2 v[kRWT];  // the tile's rows in registers before the dependent steps
+#pragma unroll
+          for (int k = 0; k < kRWT; ++k) v[k] = T[k];
 #pragma unroll
           for (int k = 0; k < kRWT; ++k) {
-            const double2 v = T[k];
 #pragma unroll
-            for (int c = 0; c < M; ++c) sturm_step(st[c], v.x, v.y, mu[c]);
+            for (int c = 0; c < M; ++c) sturm_step(st[c], v[k].x, v[k].y, mu[c]);
             if ((k & 7) == 7) {
 #pragma unroll
               for (int c = 0; c < M; ++c) ok &= sturm_rescale(st[c]);

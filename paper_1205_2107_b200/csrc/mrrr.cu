@@ -1634,7 +1634,8 @@ int solve(Problem &P, int64_t *m_out) {
     // groups that reuse it (stream order; each group costs one more chain latency)
     int cgrp = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(nown, 1), (int64_t)(scratch_bytes / (8.0 * kCSRows * nbmax))));
     if (env_int("MRRR_CS_GROUP", 0) > 0) cgrp = std::min(cgrp, env_int("MRRR_CS_GROUP", 0));  // test hook
-    double *scratch = nown ? (double *)grow_buffer(child_scratch(), (size_t)kCSRows * cgrp * nbmax * sizeof(double)) : nullptr;
+    const int64_t zs_cs = (nbmax + 7) / 8 * 8;  // scratch row stride (q every 8 rows needs ceil(nb / 8) per candidate)
+    double *scratch = nown ? (double *)grow_buffer(child_scratch(), (size_t)kCSRows * cgrp * zs_cs * sizeof(double)) : nullptr;
     double *dsig_own = lv.alloc<double>(nown + 1), *dsig = lv.alloc<double>(ncl);
     int *dtier = lv.alloc<int>(nown + 1);
     double2 *pool = ar.alloc<double2>((size_t)std::max(nown, 1) * nbmax);  // child RRRs live until the vectors
@@ -1646,7 +1647,7 @@ int solve(Problem &P, int64_t *m_out) {
         C.nodes = dnodes; C.cl_parent = docl_parent; C.cl_s0 = docl_s0; C.cl_s1 = docl_s1;
         C.lo = slo; C.hi = shi; C.LDv = LDv; C.c0 = c0; C.ncl = std::min(nown, c0 + cgrp);
         C.rtol = P.o.rtol_class;
-        C.scratch = scratch; C.zstride = nbmax;
+        C.scratch = scratch; C.zstride = zs_cs;
         C.pool = pool; C.stride = nbmax; C.sigma_out = dsig_own; C.tier_out = dtier; C.fail = dfail + 1;
         C.ctr = ctr + 16;
         k_child_step<<<C.ncl - c0, 32 * kCSWarps, 0, s>>>(C);

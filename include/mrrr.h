@@ -18,8 +18,11 @@
  * Every pointer argument of mrrr_stemr is DEVICE memory (cudaMalloc'd or
  * managed) unless stated otherwise; all work is enqueued on `stream` and the
  * call synchronises `stream` before returning, so *m and the return code are
- * valid on return.  The library allocates its own workspace stream-ordered
- * (cudaMallocAsync) and frees it before returning.  The caller owns d, e, w,
+ * valid on return.  The library takes its device workspace from chunks it
+ * owns per host thread and device and KEEPS between calls (a repeated solve
+ * allocates nothing; mrrr_trim_workspace releases them, thread exit frees
+ * them; sizes: mrrr_workspace_bytes, mrrr_stats_t.workspace_bytes).  The
+ * caller owns d, e, w,
  * Z; d and e are NOT modified.  Re-entrant on distinct streams.  Results are
  * bitwise deterministic for identical inputs, options and device type.
  *
@@ -73,6 +76,9 @@ typedef struct {
                           before the RQC; 0 = none (default; reading 10) */
   int rqc_max;         /* twisted factorizations of the RQC before the
                           bisection fallback; default 10 (reading 10) */
+  int shift_strategy;  /* 0: child shifts at the cluster ends only (readings
+                          8, 9); 1 (default): an interior shift first for
+                          clusters of >= 2000 members (reading 30) */
 } mrrr_opts_t;
 
 void mrrr_default_opts(mrrr_opts_t *opts);
@@ -168,10 +174,14 @@ int mrrr_stemr_host(int64_t n, const double *d, const double *e, int range,
  * left.  Returns 0 or -i for an invalid argument i. */
 int mrrr_plan_columns(int64_t m, int nranks, const unsigned char *free_cut, int64_t *cuts);
 
-/* Upper bound of the device workspace mrrr_stemr allocates internally for an
- * order-n problem with k wanted eigenpairs (bytes), excluding the
- * representation-tree node pool, which grows with the number of clusters
- * (<= 24 n bytes per cluster node). */
+/* Upper bound (bytes) of the device workspace mrrr_stemr holds for an
+ * order-n problem with k wanted eigenpairs, EXCEPT the child representations
+ * of the tree's cluster nodes: 16 n bytes per cluster node, kept until the
+ * solve ends (the number of nodes depends on the spectrum: 2638 at random
+ * n=20000, 13241 at random n=1e5; mrrr_stats_t.pool_bytes reports it).  The
+ * bound covers the O(n) arrays, the per-eigenvalue slot arrays, the vector
+ * checkpoints (capped at 16 GB) and the cluster-step scratch (capped at
+ * 16 GB; MRRR_SCRATCH_GB lowers both caps). */
 size_t mrrr_workspace_bytes(int64_t n, int64_t k);
 
 /* Workspace is taken from library-owned device chunks per host thread and
@@ -237,6 +247,8 @@ typedef struct {
   double ms_k_final_refine; /* RQC fallback: bracket refinement to 4 eps (0 without fallback) */
   int64_t vec_nudges;       /* vector factorizations redone at a nudged shift (reading 25) */
   int64_t vec_items;        /* warp work items of the vector kernels (lanes: vec_tasks) */
+  int64_t pool_bytes;       /* child representations of the cluster nodes (16 n B per node) */
+  int64_t workspace_bytes;  /* device workspace held by this thread after the call (all of it) */
 } mrrr_stats_t;
 int mrrr_get_stats(mrrr_stats_t *out);
 

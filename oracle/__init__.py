@@ -31,7 +31,8 @@ def build(force: bool = False) -> str:
 class Opts(C.Structure):
     _fields_ = [("tol_relgap", C.c_double), ("rtol_class", C.c_double),
                 ("max_depth", C.c_int), ("perturb_root", C.c_int),
-                ("seed", C.c_uint64), ("rtol_vec", C.c_double), ("rqc_max", C.c_int)]
+                ("seed", C.c_uint64), ("rtol_vec", C.c_double), ("rqc_max", C.c_int),
+                ("shift_strategy", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -40,7 +41,7 @@ class Stats(C.Structure):
                 ("twisted_resweeps", C.c_int64), ("rqc_fallbacks", C.c_int64),
                 ("nodes", C.c_int64), ("max_depth", C.c_int64),
                 ("singletons", C.c_int64), ("root_retries", C.c_int64),
-                ("tier", C.c_int64 * 4), ("rqc_hist", C.c_int64 * 12)]
+                ("tier", C.c_int64 * 4), ("rqc_hist", C.c_int64 * 12), ("interior", C.c_int64)]
 
     def as_dict(self):
         out = {}

@@ -17,6 +17,9 @@
 #include <string.h>
 
 #define EPS DBL_EPSILON /* 2^-52, O "Definitions" */
+#ifndef ORACLE_INTERIOR_PROBES
+#define ORACLE_INTERIOR_PROBES 4 /* reading 30: end members and the two next to the shift */
+#endif
 
 void oracle_default_opts(oracle_opts_t *o) {
   o->tol_relgap = 1e-3;                /* P:L1069-1072 footnote */
@@ -26,6 +29,7 @@ void oracle_default_opts(oracle_opts_t *o) {
   o->seed = 0x1205210700000000ULL;     /* SURVEY §8(b) default seed */
   o->rtol_vec = 0.0;                   /* reading 10 */
   o->rqc_max = 10;                     /* reading 10 */
+  o->shift_strategy = 1;               /* reading 30 */
 }
 
 /* ------------------------------------------------------------------------ */
@@ -494,7 +498,7 @@ static void cluster(ctx_t *c, const rrr_t *R, int64_t s, int64_t t, int depth) {
   if (!DpA) { free(C.D); c->err = 6; return; }
   double *LpA = DpA + (nb + 1), *zL = DpA + 2 * (nb + 1), *zR = DpA + 3 * (nb + 1);
   static const double mult[3] = {1.0, 2.0, 4.0};
-  double cs[6], cg[6];
+  double cs[7], cg[7];
   /* offset unit (reading 8, amended): twice the end bracket's width, but at
    * least 2 rtol_c |lambda| -- the width classification guarantees -- so the
    * shift does not depend on how far below rtol_c a bracket happens to be */
@@ -506,12 +510,59 @@ static void cluster(ctx_t *c, const rrr_t *R, int64_t s, int64_t t, int depth) {
     cs[2 * mi] = c->lo[s] - mult[mi] * dl;
     cs[2 * mi + 1] = c->hi[t] + mult[mi] * dr;
   }
-  for (int k = 0; k < 6; ++k) {
+  /* reading 30 (shift_strategy 1): an interior candidate at the midpoint of
+   * the widest conservative gap between consecutive members in the middle
+   * half of the cluster ("close to one of the eigenvalues in the cluster",
+   * P:L1102-1103), taken when that gap is resolvable (> 1e-10 relative: not
+   * a degenerate group) and its child passes the growth tests (raw growth
+   * <= 8 spdiam, or weighted growth <= 64 spdiam with the end probes and the
+   * probes of the two members next to the shift) -- the cluster then splits
+   * on both sides of the shift, and the tree's depth grows like log(m)
+   * instead of m / (members peeled per level) */
+  int64_t m = t - s + 1;
+  if (c->o->shift_strategy == 1 && m >= 2000 && c->hi[t] - c->lo[s] > 1e-6 * spd) {
+    int64_t a = s + m / 4, b = t - m / 4, jb = -1;
+    double gb = -INFINITY;
+    for (int64_t j = a; j < b; ++j) {
+      double g = c->lo[j + 1] - c->hi[j];
+      if (g > gb) { gb = g; jb = j; }
+    }
+    if (jb >= 0) {
+      double la = 0.5 * (c->lo[jb] + c->hi[jb]), lb = 0.5 * (c->lo[jb + 1] + c->hi[jb + 1]);
+      if (gb > 1e-10 * fmax(fabs(la), fabs(lb))) {
+        double sg = 0.5 * (c->hi[jb] + c->lo[jb + 1]), g6;
+        oracle_child_rrr(nb, R->D, R->L, R->LD, sg, DpA, LpA, &g6);
+        c->st->child_sweeps++;
+        int take = isfinite(g6) && g6 <= 8.0 * spd;
+        if (!take && isfinite(g6) && g6 <= 1e8 * spd) {
+          int64_t r, nc;
+          double gg, lam;
+          int rs = 0;
+          double wg = 0;
+          double lams[4] = {0.5 * (c->lo[s] + c->hi[s]), 0.5 * (c->lo[t] + c->hi[t]), la, lb};
+          for (int q = 0; q < ORACLE_INTERIOR_PROBES; ++q) {
+            lam = lams[q];
+            twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lam, R->pivmin, &c->ws, zL, &r, &gg, &nc, &rs);
+            wg = fmax(wg, weighted_growth(nb, zL, DpA));
+          }
+          take = wg <= 64.0 * spd;
+        }
+        if (take) {
+          best = 6;
+          cs[6] = sg; cg[6] = g6;
+          c->st->interior++;
+        }
+      }
+    }
+  }
+  for (int k = 0; k < 6 && best != 6; ++k) {
     oracle_child_rrr(nb, R->D, R->L, R->LD, cs[k], DpA, LpA, &cg[k]);
     c->st->child_sweeps++;
     if (cg[k] <= 8.0 * spd && (best < 0 || cg[k] < cg[best])) best = k;
   }
-  if (best >= 0) c->st->tier[0]++;
+  if (best == 6) {
+    /* interior shift taken */
+  } else if (best >= 0) c->st->tier[0]++;
   else {
     int64_t r, nc;
     double g;

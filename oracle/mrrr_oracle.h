@@ -31,6 +31,8 @@ typedef struct {
   uint64_t seed;      /* perturbation seed */
   double rtol_vec;    /* singleton bracket refinement before the RQC; 0 = none (reading 10) */
   int rqc_max;        /* RQC factorizations before the bisection fallback; 10 (reading 10) */
+  int shift_strategy; /* 0: shifts at the cluster ends only (readings 8, 9); 1 (default):
+                         an interior candidate first for large clusters (reading 30) */
 } oracle_opts_t;
 
 typedef struct {
@@ -46,6 +48,7 @@ typedef struct {
   int64_t root_retries;        /* O5 delta doublings */
   int64_t tier[4];             /* O9 acceptance tier counts (i)..(iv) */
   int64_t rqc_hist[12];        /* factorizations per vector (index = count, 11 = >10) */
+  int64_t interior;            /* clusters whose child took the interior shift (reading 30) */
 } oracle_stats_t;
 
 void oracle_default_opts(oracle_opts_t *o);

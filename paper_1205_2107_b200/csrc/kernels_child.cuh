@@ -35,7 +35,8 @@ namespace mrrr {
 constexpr int kCT = 16;     // rows per tile
 constexpr int kCRing = 6;   // tiles in flight per warp
 constexpr int kCSWarps = 5; // 4 probe chains + the candidate warp
-constexpr int kCSRows = 17; // scratch rows per cluster: t of 6 candidates, 4 per probe, |z| of 2, q every 8 rows
+constexpr int kNC = 7;      // candidates: 6 at the cluster ends (readings 8, 9) + the interior one (reading 30)
+constexpr int kCSRows = kNC + 11; // scratch rows per cluster: t of the candidates, 4 per probe, |z| of 2, q every 8 rows
 
 struct ChainRing {
   double2 rDL[kCRing][kCT];  // (D, LLD)
@@ -45,9 +46,10 @@ struct ChainRing {
 struct ChildSmem {
   ChainRing ring[kCSWarps];
   double tq[2][kCT][8];      // candidate tile: t_i, q_i per row and candidate (conflict-free writes)
-  double red[kCSWarps][20];  // per-warp partials of the growth reductions
+  double red[kCSWarps][3 * kNC + 2];  // per-warp partials of the growth reductions
   unsigned okw[kCSWarps];    // per-warp finiteness masks of the candidates
-  double sig[6];             // the candidates' shifts
+  double sig[kNC];           // the candidates' shifts
+  int has_int;               // the interior candidate exists (reading 30)
   double am_v[4];            // per-warp argmin (probes)
   int am_i[4];
   int best, tier, bad;
@@ -69,6 +71,8 @@ struct ChildArgs {
   int *tier_out;
   int *fail;
   unsigned long long *ctr;     // [0] probes (twisted factorizations)
+  int shift_strategy;          // 1: interior candidate first (reading 30)
+  double int_wg;               // the interior candidate's weighted-growth bound (x spdiam)
 };
 
 // Issue the rows of tile `tile` into ring slot `slot` (lanes 0-15: (D, LLD),
@@ -110,11 +114,14 @@ __device__ __forceinline__ void cs_probe_fwd(ChainRing &R, const double2 *DL, co
     };
     if (lane < kCT) kld = R.rLD[slot][lane].x;
     if (rows == kCT && r0 + kCT < nb) {  // every row of the tile is below nb - 1
-      double2 v[kCT];  // the tile's rows in registers before the dependent steps
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) v[k] = R.rDL[slot][k];
+      for (int h = 0; h < kCT; h += 8) {  // rows in registers, 8 at a time, before the dependent steps
+        double2 v[8];
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) row(v[k], k, false);
+        for (int k = 0; k < 8; ++k) v[k] = R.rDL[slot][h + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) row(v[k], h + k, false);
+      }
     } else {
       for (int k = 0; k < rows; ++k) row(R.rDL[slot][k], k, true);
     }
@@ -156,11 +163,14 @@ __device__ __forceinline__ void cs_probe_bwd(ChainRing &R, const double2 *DL, co
     };
     if (lane < kCT) kld = R.rLD[slot][lane].x;
     if (top - r0 + 1 == kCT) {
-      double2 v[kCT];  // the tile's rows in registers before the dependent steps
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) v[k] = R.rDL[slot][k];
+      for (int h = kCT - 8; h >= 0; h -= 8) {  // rows in registers, 8 at a time, before the dependent steps
+        double2 v[8];
 #pragma unroll
-      for (int k = kCT - 1; k >= 0; --k) row(v[k], k);
+        for (int k = 0; k < 8; ++k) v[k] = R.rDL[slot][h + k];
+#pragma unroll
+        for (int k = 7; k >= 0; --k) row(v[k], h + k);
+      }
     } else {
       for (int k = top - r0; k >= 0; --k) row(R.rDL[slot][k], k);
     }
@@ -176,7 +186,7 @@ __device__ __forceinline__ void cs_probe_bwd(ChainRing &R, const double2 *DL, co
   __pipeline_wait_prior(0);
 }
 
-// The six candidate chains (lane k < 6 runs shift sig[k]; the other lanes
+// The candidate chains (lane k < kNC runs shift sig[k]; the other lanes
 // repeat lane 0's): TP[k * zstride + i] = t_i (= D+_i q_i) and, every 8 rows,
 // QK[k * (zstride / 8) + i / 8] = q_i.  The chain does no division: D+_i =
 // t_i / q_i with q_i = t_{i-1} (or QK where the chain rescaled, i % 8 == 0)
@@ -189,7 +199,7 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
 #pragma unroll
   for (int k = 0; k < kCRing - 1; ++k) cs_issue(R, DL, nullptr, nb, k < ntile ? k : -1, k, lane, false);
   double p = -sigma, q = 1.0;
-  const int cand = lane < 6 ? lane : 0;
+  const int cand = lane < kNC ? lane : 0;
   double *tp = TP + cand * zstride, *qk = QK + cand * (zstride / 8);
   for (int c = 0; c < ntile; ++c) {
     __pipeline_wait_prior(kCRing - 2);
@@ -197,9 +207,9 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
     const int slot = c % kCRing, r0 = c * kCT, rows = min(kCT, nb - r0);
     auto row = [&](const double2 v, int k, bool last_check) {
       const int i = r0 + k;
-      if ((k & 7) == 0 && lane < 6) qk[i >> 3] = q;
+      if ((k & 7) == 0 && lane < kNC) qk[i >> 3] = q;
       const double tt = fma(v.x, q, p);
-      if (lane < 6) S.tq[0][k][lane] = tt;
+      if (lane < kNC) S.tq[0][k][lane] = tt;
       if (!last_check || i < nb - 1) { p = fma(-sigma, tt, v.y * p); q = tt; }
       if ((k & 7) == 7) {
         const double f = pow2_scale(min(max(max_exp(p, q), 1), 2045));
@@ -207,18 +217,21 @@ __device__ __forceinline__ void cs_candidates(ChainRing &R, ChildSmem &S, const 
       }
     };
     if (rows == kCT && r0 + kCT < nb) {  // every row of the tile is below nb - 1
-      double2 v[kCT];
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) v[k] = R.rDL[slot][k];
+      for (int h = 0; h < kCT; h += 8) {  // rows in registers, 8 at a time, before the dependent steps
+        double2 v[8];
 #pragma unroll
-      for (int k = 0; k < kCT; ++k) row(v[k], k, false);
+        for (int k = 0; k < 8; ++k) v[k] = R.rDL[slot][h + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) row(v[k], h + k, false);
+      }
     } else {
       for (int k = 0; k < rows; ++k) row(R.rDL[slot][k], k, true);
     }
     __syncwarp();
-    // the tile's t values, coalesced: 96 stores spread over the warp
+    // the tile's t values, coalesced: kNC * 16 stores spread over the warp
 #pragma unroll
-    for (int e = lane; e < 6 * kCT; e += 32) {
+    for (int e = lane; e < kNC * kCT; e += 32) {
       const int cc = e >> 4, k = e & (kCT - 1);
       if (k < rows) TP[cc * zstride + r0 + k] = S.tq[0][k][cc];
     }
@@ -248,10 +261,10 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
   const double2 *DL = P.DL, *LD = A.LDv + P.row0;
   const int64_t zs = A.zstride;
   double *base = A.scratch + (int64_t)blockIdx.x * kCSRows * zs;
-  double *TP = base;                 // 6 candidates' t
-  double *pr[2] = {base + 6 * zs, base + 10 * zs};  // per probe: s, P, rho, sig
-  double *zl = base + 14 * zs, *zr = base + 15 * zs;
-  double *QK = base + 16 * zs;       // 6 candidates' q every 8 rows (zs / 8 each)
+  double *TP = base;                 // the candidates' t
+  double *pr[2] = {base + kNC * zs, base + (kNC + 4) * zs};  // per probe: s, P, rho, sig
+  double *zl = base + (kNC + 8) * zs, *zr = base + (kNC + 9) * zs;
+  double *QK = base + (kNC + 10) * zs;  // the candidates' q every 8 rows (zs / 8 each)
 
   // ---- phase 1: the five chains
   const long long clk_p0 = clock64();
@@ -263,10 +276,41 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
     if ((wid & 1) == 0) cs_probe_fwd(S.ring[wid], DL, LD, nb, lam, lane, q, q + 2 * zs);
     else cs_probe_bwd(S.ring[wid], DL, LD, nb, lam, lane, q + zs, q + 3 * zs);
   } else {
+    // reading 30 (shift_strategy 1): the interior candidate -- the midpoint of
+    // the widest conservative gap between consecutive members in the middle
+    // half of a cluster of >= 2000 members whose width exceeds 1e-6 spdiam,
+    // if that gap exceeds 1e-10 of the members' magnitudes (not a degenerate
+    // group); warp reduction, ties to the lowest member (the oracle's order)
+    const int mm = s1 - s0 + 1;
+    double sig_int = 0.0;
+    bool has_int = false;
+    if (A.shift_strategy == 1 && mm >= 2000 && A.hi[s1] - A.lo[s0] > 1e-6 * P.spdiam) {
+      const int ja = s0 + mm / 4, jb = s1 - mm / 4;  // members j in [ja, jb) and j + 1
+      double gb = -CUDART_INF;
+      int jbest = -1;
+      for (int j = ja + lane; j < jb; j += 32) {
+        const double gj = A.lo[j + 1] - A.hi[j];
+        if (gj > gb) { gb = gj; jbest = j; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double og = __shfl_xor_sync(0xffffffffu, gb, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, jbest, o);
+        if (og > gb || (og == gb && oj >= 0 && (jbest < 0 || oj < jbest))) { gb = og; jbest = oj; }
+      }
+      if (jbest >= 0) {
+        const double la = 0.5 * (A.lo[jbest] + A.hi[jbest]), lb = 0.5 * (A.lo[jbest + 1] + A.hi[jbest + 1]);
+        if (gb > 1e-10 * fmax(fabs(la), fabs(lb))) {
+          has_int = true;
+          sig_int = 0.5 * (A.hi[jbest] + A.lo[jbest + 1]);
+        }
+      }
+    }
     const int which = lane < 6 ? lane : 0;
     const double mult = (double)(1 << (which >> 1));
     double sigma;
-    if ((which & 1) == 0) {
+    if (lane == 6 && has_int) {
+      sigma = sig_int;
+    } else if ((which & 1) == 0) {
       const double l = A.lo[s0], h = A.hi[s0];
       const double dl = fmax(fmax(2.0 * (h - l), 2.0 * A.rtol * fabs(l)), 4.0 * kEps * fabs(l));
       sigma = l - mult * dl;
@@ -276,7 +320,8 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
       sigma = h + mult * dr;
     }
     cs_candidates(S.ring[4], S, DL, nb, sigma, lane, TP, QK, zs);
-    if (lane < 6) S.sig[lane] = sigma;
+    if (lane < kNC) S.sig[lane] = sigma;
+    if (lane == 0) S.has_int = has_int;
   }
   if (lane == 0) atomicMax(&A.ctr[1 + (wid == 4 ? 1 : (wid & 1) ? 2 : 3)], (unsigned long long)(clock64() - clk_p0));
   __syncthreads();
@@ -371,17 +416,17 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
   if (tid == 0) atomicMax(&A.ctr[5], (unsigned long long)(clock64() - clk_p1));
   const long long clk_p2 = clock64();
   // ---- phase 3: growth of the candidates, raw and weighted (all threads)
-  double g[6], nl[6], nr[6], dnl = 0.0, dnr = 0.0;
-  unsigned okm = 0x3f;
+  double g[kNC], nl[kNC], nr[kNC], dnl = 0.0, dnr = 0.0;
+  unsigned okm = (1u << kNC) - 1u;
 #pragma unroll
-  for (int k = 0; k < 6; ++k) { g[k] = 0.0; nl[k] = 0.0; nr[k] = 0.0; }
-#pragma unroll 4
+  for (int k = 0; k < kNC; ++k) { g[k] = 0.0; nl[k] = 0.0; nr[k] = 0.0; }
+#pragma unroll 2
   for (int i = tid; i < nb; i += 32 * kCSWarps) {
     const double a = zl[i], b = zr[i];
     const double a2 = a * a, b2 = b * b;
     dnl += a2; dnr += b2;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
+    for (int k = 0; k < kNC; ++k) {
       const double d = cs_dplus(TP, QK, zs, k, i);
       const double ad = fabs(d);
       if (!(isfinite(d) && d != 0.0)) okm &= ~(1u << k);
@@ -392,7 +437,7 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
   }
   for (int o = 16; o; o >>= 1) {
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
+    for (int k = 0; k < kNC; ++k) {
       g[k] = fmax(g[k], __shfl_xor_sync(0xffffffffu, g[k], o));
       nl[k] += __shfl_xor_sync(0xffffffffu, nl[k], o);
       nr[k] += __shfl_xor_sync(0xffffffffu, nr[k], o);
@@ -403,28 +448,39 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
   }
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < 6; ++k) { S.red[wid][k] = g[k]; S.red[wid][6 + k] = nl[k]; S.red[wid][12 + k] = nr[k]; }
-    S.red[wid][18] = dnl; S.red[wid][19] = dnr; S.okw[wid] = okm;
+    for (int k = 0; k < kNC; ++k) {
+      S.red[wid][k] = g[k]; S.red[wid][kNC + k] = nl[k]; S.red[wid][2 * kNC + k] = nr[k];
+    }
+    S.red[wid][3 * kNC] = dnl; S.red[wid][3 * kNC + 1] = dnr; S.okw[wid] = okm;
   }
   __syncthreads();
 
   // ---- phase 4: the tiered choice (reading 9) by thread 0
   if (tid == 0) {
     atomicMax(&A.ctr[6], (unsigned long long)(clock64() - clk_p2));
-    double G[6], NL[6], NR[6], DNL = 0.0, DNR = 0.0;
-    unsigned ok = 0x3f;
-    for (int k = 0; k < 6; ++k) { G[k] = 0.0; NL[k] = 0.0; NR[k] = 0.0; }
+    double G[kNC], NL[kNC], NR[kNC], DNL = 0.0, DNR = 0.0;
+    unsigned ok = (1u << kNC) - 1u;
+    for (int k = 0; k < kNC; ++k) { G[k] = 0.0; NL[k] = 0.0; NR[k] = 0.0; }
     for (int w = 0; w < kCSWarps; ++w) {
-      for (int k = 0; k < 6; ++k) {
+      for (int k = 0; k < kNC; ++k) {
         G[k] = fmax(G[k], S.red[w][k]);
-        NL[k] += S.red[w][6 + k];
-        NR[k] += S.red[w][12 + k];
+        NL[k] += S.red[w][kNC + k];
+        NR[k] += S.red[w][2 * kNC + k];
       }
-      DNL += S.red[w][18]; DNR += S.red[w][19];
+      DNL += S.red[w][3 * kNC]; DNR += S.red[w][3 * kNC + 1];
       ok &= S.okw[w];
     }
     const double spd = P.spdiam;
     int b1 = -1, b2 = -1, b3 = -1;
+    // reading 30: the interior candidate first -- taken if its child is finite
+    // and its raw growth <= 8 spdiam, or <= 1e8 spdiam with the weighted
+    // growth (end probes) <= 64 spdiam
+    int b_int = -1;
+    if (S.has_int && ((ok >> 6) & 1u)) {
+      const double g6 = G[6];
+      const double w6 = (DNL > 0 && DNR > 0) ? fmax(NL[6] / DNL, NR[6] / DNR) : CUDART_INF;
+      if (g6 <= 8.0 * spd || (g6 <= 1e8 * spd && w6 <= A.int_wg * spd)) b_int = 6;
+    }
     double r1 = 0, r2 = 0, r3 = 0;
     for (int k = 0; k < 6; ++k) {
       const bool fin = (ok >> k) & 1u;
@@ -437,6 +493,7 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
     int tier = 0, best = b1;
     if (best < 0) { tier = 1; best = b2; }
     if (best < 0) { tier = 3; best = b3; if (!(r3 <= 1e8 * spd)) best = -1; }
+    if (b_int >= 0) { tier = 5; best = b_int; }
     S.best = best;
     S.tier = best < 0 ? 4 : tier;
     S.sg = best < 0 ? 0.0 : S.sig[best];

@@ -157,8 +157,11 @@ struct Trace {
 struct BumpWs {
   std::vector<std::pair<char *, size_t>> chunks;
   size_t chunk = 0, off = 0;
+  size_t used = 0, used_peak = 0;  // bytes handed out since the last reset, and their peak over resets
   void *get(size_t bytes) {
     bytes = (std::max<size_t>(bytes, 1) + 255) & ~size_t(255);
+    used += bytes;
+    used_peak = std::max(used_peak, used);
     for (;;) {
       if (chunk < chunks.size() && off + bytes <= chunks[chunk].second) {
         void *p = chunks[chunk].first + off;
@@ -183,7 +186,7 @@ struct BumpWs {
       off = 0;
     }
   }
-  void reset() { chunk = 0; off = 0; }
+  void reset() { chunk = 0; off = 0; used = 0; }
   void release() {
     for (auto &c : chunks) cudaFree(c.first);
     chunks.clear();
@@ -837,6 +840,8 @@ int solve(Problem &P, int64_t *m_out) {
   }
   const int64_t n = P.n;
   DevArena ar(device_ws(g_ws_call));
+  device_ws(g_ws_level).used_peak = 0;
+  size_t cs_scratch_used = 0;
   Trace tr;
   g_staging.reset();
   Timer tm(s), tall(s);
@@ -1141,6 +1146,9 @@ int solve(Problem &P, int64_t *m_out) {
     return 8;
   };
   const int rw_m_tree = rw_m_env > 0 ? rw_m_env : 1;
+  // reading 30: weighted-growth bound of the interior candidate (x spdiam);
+  // MRRR_INT_WG overrides (diagnostic)
+  const double int_wg = getenv("MRRR_INT_WG") ? atof(getenv("MRRR_INT_WG")) : 64.0;
   {
     std::vector<Work> wv;
     kt_root.start(s);
@@ -1636,9 +1644,11 @@ int solve(Problem &P, int64_t *m_out) {
     if (env_int("MRRR_CS_GROUP", 0) > 0) cgrp = std::min(cgrp, env_int("MRRR_CS_GROUP", 0));  // test hook
     const int64_t zs_cs = (nbmax + 7) / 8 * 8;  // scratch row stride (q every 8 rows needs ceil(nb / 8) per candidate)
     double *scratch = nown ? (double *)grow_buffer(child_scratch(), (size_t)kCSRows * cgrp * zs_cs * sizeof(double)) : nullptr;
+    if (nown) cs_scratch_used = std::max(cs_scratch_used, (size_t)kCSRows * cgrp * zs_cs * sizeof(double));
     double *dsig_own = lv.alloc<double>(nown + 1), *dsig = lv.alloc<double>(ncl);
     int *dtier = lv.alloc<int>(nown + 1);
     double2 *pool = ar.alloc<double2>((size_t)std::max(nown, 1) * nbmax);  // child RRRs live until the vectors
+    g_stats.pool_bytes += (int64_t)std::max(nown, 1) * nbmax * (int64_t)sizeof(double2);
     tr.fine(s, "  alloc+upload");
     int h_fail[4] = {0, 0, 0, 0};
     {
@@ -1650,6 +1660,8 @@ int solve(Problem &P, int64_t *m_out) {
         C.scratch = scratch; C.zstride = zs_cs;
         C.pool = pool; C.stride = nbmax; C.sigma_out = dsig_own; C.tier_out = dtier; C.fail = dfail + 1;
         C.ctr = ctr + 16;
+        C.shift_strategy = P.o.shift_strategy;
+        C.int_wg = int_wg;
         k_child_step<<<C.ncl - c0, 32 * kCSWarps, 0, s>>>(C);
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
@@ -1890,6 +1902,11 @@ int solve(Problem &P, int64_t *m_out) {
     g_stats.ms_k_vectors = ms;
   }
   g_stats.ms_k_final_refine = kt_fin.ms();
+  // bytes this call used: the call arena, the largest level arena, the
+  // cluster-step scratch it asked for (the chunks held may be larger: they
+  // grow geometrically and are kept for the next call)
+  g_stats.workspace_bytes = (int64_t)device_ws(g_ws_call).used + (int64_t)device_ws(g_ws_level).used_peak +
+                            (int64_t)cs_scratch_used;
   return 0;
 }
 
@@ -1929,6 +1946,7 @@ void mrrr_default_opts(mrrr_opts_t *o) {
   o->grid_factor = 4;
   o->rtol_vec = 0.0;
   o->rqc_max = 10;
+  o->shift_strategy = 1;  // DESIGN.md reading 30
 }
 
 // mrrr_negcount: the bisection kernels' Sturm count (projective sweep with
@@ -2154,9 +2172,19 @@ int mrrr_trim_workspace(void) {
 }
 
 size_t mrrr_workspace_bytes(int64_t n, int64_t k) {
-  size_t nn = (size_t)n, kk = (size_t)k;
-  size_t seg = (nn + MRRR_SEG - 1) / MRRR_SEG;
-  return nn * (8 * 3 + 4 * 3 + 16 * 2 + 8) + kk * (8 * 4 + 4 * 6) + seg * kk * (32 + 16) + (1 << 20);
+  const double nn = (double)n, kk = (double)std::min(k + 2, n), cap = 16e9;
+  const double seg = std::ceil(nn / MRRR_SEG);
+  // O(n): scaled d, e, e^2, split flags, root (D, LLD), (LD, LD^2), chain buffers, row->block
+  const double fixed = nn * (3 * 8 + 4 + 2 * 16 + 8 + 4 + 4);
+  // per slot: j, node, out, active, run end, lo/hi (+ exchange), wl/wu, lambda, fail list,
+  // task (24 B), share of a warp item, split-phase state (RqcState + sort keys)
+  const double slots = kk * (5 * 4 + 4 * 8 + 8 + 4 + 24 + 1 + 88 + 5 * 4);
+  // vector checkpoints: 4 side streams x (piece + 32) columns x 64 B per 16-row segment
+  const double ck = std::min(cap, 4.0 * (std::ceil(kk / 4) + 32) * seg * 64.0) + 4.0 * 32 * seg * 64.0;
+  // cluster-step scratch: kCSRows rows of n doubles per cluster of a level (<= k / 2 clusters)
+  const double cs = std::min(cap, std::floor(kk / 2) * kCSRows * 8.0 * (std::ceil(nn / 8) * 8)) +
+                    kCSRows * 8.0 * (std::ceil(nn / 8) * 8);
+  return (size_t)(fixed + slots + ck + cs) + ((size_t)64 << 20);  // + per-level lists, headroom
 }
 
 const char *mrrr_strerror(int code) {

@@ -21,7 +21,8 @@ RANGE_ALL, RANGE_INDEX, RANGE_VALUE = 0, 1, 2
 class Opts(C.Structure):
     _fields_ = [("tol_relgap", C.c_double), ("rtol_class", C.c_double), ("max_depth", C.c_int),
                 ("perturb_root", C.c_int), ("seed", C.c_uint64), ("multisection", C.c_int),
-                ("grid_factor", C.c_int), ("rtol_vec", C.c_double), ("rqc_max", C.c_int)]
+                ("grid_factor", C.c_int), ("rtol_vec", C.c_double), ("rqc_max", C.c_int),
+                ("shift_strategy", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -34,7 +35,7 @@ class Stats(C.Structure):
                 ("ms_k_root_bisect", C.c_double), ("ms_k_vectors", C.c_double),
                 ("vec_tasks", C.c_int64), ("vec_elems", C.c_int64),
                 ("ms_k_final_refine", C.c_double), ("vec_nudges", C.c_int64),
-                ("vec_items", C.c_int64)]
+                ("vec_items", C.c_int64), ("pool_bytes", C.c_int64), ("workspace_bytes", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -248,3 +248,24 @@ def test_value_endpoints_on_eigenvalues(torch_cuda, P, oracle_mod, vl, vu):
     assert np.max(np.abs(w - lam[k0:k0 + len(w)])) <= 4 * n * EPS * tnorm1(d, e)
     # the set is contiguous and lies in [vl, vu] up to the counting tie
     assert lam[k0] >= vl - 1e-9 and lam[k0 + len(w) - 1] <= vu + 1e-9
+
+
+@pytest.mark.parametrize("case", ["random_3000", "glued_40", "clement_2000_idx"])
+def test_workspace_bound(torch_cuda, P, case):
+    """mrrr_workspace_bytes(n, k) bounds the workspace a call uses, apart from
+    the cluster nodes' child representations (16 n B per node, reported as
+    pool_bytes); include/mrrr.h."""
+    kw = {}
+    if case == "random_3000":
+        d, e = W.random_uniform(3000, 2)
+    elif case == "glued_40":
+        d, e = W.glued_wilkinson(40)
+    else:
+        d, e = W.clement(2000)
+        kw = {"il": 1, "iu": 500}
+    gpu_solve(P, torch_cuda, d, e, **kw)
+    st = P.last_stats()
+    n, k = len(d), (kw["iu"] - kw["il"] + 1 if kw else len(d))
+    bound = P.mrrr.lib().mrrr_workspace_bytes(n, k)
+    assert st["pool_bytes"] >= 16 * n * st["nodes"]
+    assert 0 < st["workspace_bytes"] - st["pool_bytes"] <= bound, (st["workspace_bytes"], st["pool_bytes"], bound)

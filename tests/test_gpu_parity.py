@@ -420,3 +420,33 @@ def test_config5_random_100000(torch_cuda, P, oracle_mod):
         ok = dk_comparable(wo, residuals(d, e, w[il - 1:iu], Zs), residuals(d, e, wo, Zo))
         if ok.any():
             assert np.max(vec_diff_signfree(Zs[:, ok], Zo[:, ok])) <= 1e-9
+
+
+# ---------------------------------------------------------------------------
+# Reading 30: the interior child shift (mrrr_opts_t.shift_strategy = 1)
+@pytest.mark.parametrize("name", ["clement_4000", "random_3000", "random_6000_s1"])
+def test_interior_strategy_parity(torch_cuda, P, oracle_mod, name):
+    """GPU and oracle both with shift_strategy 1: eigenpairs agree (values,
+    Davis-Kahan-comparable vectors) and the accuracy contract holds."""
+    d, e = {"clement_4000": lambda: W.clement(4000), "random_3000": lambda: W.random_uniform(3000, 0),
+            "random_6000_s1": lambda: W.random_uniform(6000, 1)}[name]()
+    o = P.default_opts(shift_strategy=1)
+    w, Z = gpu_solve(P, torch_cuda, d, e, opts=o)
+    wo, Zo = oracle_mod.stemr(d, e, opts=oracle_mod.default_opts(shift_strategy=1))
+    compare(d, e, w, Z, wo, Zo)
+
+
+def test_interior_strategy_clement_full(torch_cuda, P):
+    """Clement n=50000, all pairs, shift_strategy 1: the 50-level chain of the
+    end shifts becomes a tree of <= 10 levels; closed-form eigenvalues and the
+    accuracy contract (GPU-side residual and orthogonality)."""
+    torch = torch_cuda
+    n = 50000
+    d, e = W.clement(n)
+    o = P.default_opts(shift_strategy=1)
+    wt, Zt = P.stemr(torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda"), opts=o)
+    assert P.last_stats()["levels"] <= 10
+    lam = 2.0 * np.arange(1, n + 1) - n - 1
+    assert np.max(np.abs(wt.cpu().numpy() - lam)) <= 4 * n * EPS * tnorm1(d, e)
+    res, orth = gpu_metrics(torch, d, e, wt, Zt)
+    assert res <= 1 and orth <= 1, (res, orth)

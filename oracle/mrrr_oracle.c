@@ -29,7 +29,7 @@ void oracle_default_opts(oracle_opts_t *o) {
   o->seed = 0x1205210700000000ULL;     /* SURVEY §8(b) default seed */
   o->rtol_vec = 0.0;                   /* reading 10 */
   o->rqc_max = 10;                     /* reading 10 */
-  o->shift_strategy = 1;               /* reading 30 */
+  o->shift_strategy = 0;               /* reading 30 (option 1) */
 }
 
 /* ------------------------------------------------------------------------ */

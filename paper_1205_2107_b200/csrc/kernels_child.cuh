@@ -43,15 +43,20 @@ struct ChainRing {
   double2 rLD[kCRing][kCT];  // (LD, LD^2)
 };
 
+constexpr int kCSWarpsAdj = kCSWarps + 4;  // + the probes of the two members next to the interior shift
+constexpr int kCSRowsAdj = kCSRows + 10;   // + their 8 probe rows and 2 |z| rows
+
 struct ChildSmem {
-  ChainRing ring[kCSWarps];
+  ChainRing ring[kCSWarpsAdj];
   double tq[2][kCT][8];      // candidate tile: t_i, q_i per row and candidate (conflict-free writes)
-  double red[kCSWarps][3 * kNC + 2];  // per-warp partials of the growth reductions
-  unsigned okw[kCSWarps];    // per-warp finiteness masks of the candidates
+  double red[kCSWarpsAdj][3 * kNC + 4];  // per-warp partials of the growth reductions
+  unsigned okw[kCSWarpsAdj];             // per-warp finiteness masks of the candidates
   double sig[kNC];           // the candidates' shifts
   int has_int;               // the interior candidate exists (reading 30)
-  double am_v[4];            // per-warp argmin (probes)
-  int am_i[4];
+  int jint;                  // its gap lies between members jint and jint + 1
+  double sig_int;
+  double am_v[kCSWarpsAdj];  // per-warp argmin (probes)
+  int am_i[kCSWarpsAdj];
   int best, tier, bad;
   double sg;
 };
@@ -73,6 +78,7 @@ struct ChildArgs {
   unsigned long long *ctr;     // [0] probes (twisted factorizations)
   int shift_strategy;          // 1: interior candidate first (reading 30)
   double int_wg;               // the interior candidate's weighted-growth bound (x spdiam)
+  const int *cl_list;          // optional: the launch's clusters are cl_list[c0 .. ncl-1]
 };
 
 // Issue the rows of tile `tile` into ring slot `slot` (lanes 0-15: (D, LLD),
@@ -250,61 +256,91 @@ __device__ __forceinline__ double cs_dplus(const double *TP, const double *QK, i
   return div_nr(tp[i], q);
 }
 
-__global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
+// ADJ = 0: the step of a cluster with the end candidates only (five warps).
+// ADJ = 1 (reading 30, clusters of >= 2000 members): also the interior
+// candidate, and two more probes (four more warps) at the members next to its
+// shift, whose weighted growth the interior child must also pass.
+template <int ADJ>
+__global__ void __launch_bounds__(32 * (kCSWarps + 4 * ADJ), ADJ ? 1 : 3) k_child_step(ChildArgs A) {
+  constexpr int NW = kCSWarps + 4 * ADJ, NP = 2 + 2 * ADJ, ROWS = ADJ ? kCSRowsAdj : kCSRows;
   __shared__ ChildSmem S;
-  const int c = A.c0 + blockIdx.x;
-  if (c >= A.ncl) return;
+  if (A.c0 + (int)blockIdx.x >= A.ncl) return;
+  const int c = A.cl_list ? A.cl_list[A.c0 + blockIdx.x] : A.c0 + (int)blockIdx.x;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const Node P = A.nodes[A.cl_parent[c]];
   const int nb = P.nb;
   const int s0 = A.cl_s0[c], s1 = A.cl_s1[c] - 1;
   const double2 *DL = P.DL, *LD = A.LDv + P.row0;
   const int64_t zs = A.zstride;
-  double *base = A.scratch + (int64_t)blockIdx.x * kCSRows * zs;
+  double *base = A.scratch + (int64_t)blockIdx.x * ROWS * zs;
   double *TP = base;                 // the candidates' t
-  double *pr[2] = {base + kNC * zs, base + (kNC + 4) * zs};  // per probe: s, P, rho, sig
-  double *zl = base + (kNC + 8) * zs, *zr = base + (kNC + 9) * zs;
   double *QK = base + (kNC + 10) * zs;  // the candidates' q every 8 rows (zs / 8 each)
+  // per probe side: s, P, rho, sig (4 rows) and |z| (1 row); sides 0, 1 the
+  // cluster's end members, 2, 3 (ADJ) the members next to the interior shift
+  double *pr[4] = {base + kNC * zs, base + (kNC + 4) * zs, base + kCSRows * zs, base + (kCSRows + 4) * zs};
+  double *zz[4] = {base + (kNC + 8) * zs, base + (kNC + 9) * zs, base + (kCSRows + 8) * zs, base + (kCSRows + 9) * zs};
+  double *zl = zz[0], *zr = zz[1];
 
-  // ---- phase 1: the five chains
-  const long long clk_p0 = clock64();
-  if (wid < 4) {
-    const int side = wid >> 1;
-    const int slot = side == 0 ? s0 : s1;
-    const double lam = 0.5 * (A.lo[slot] + A.hi[slot]);
-    double *q = pr[side];
-    if ((wid & 1) == 0) cs_probe_fwd(S.ring[wid], DL, LD, nb, lam, lane, q, q + 2 * zs);
-    else cs_probe_bwd(S.ring[wid], DL, LD, nb, lam, lane, q + zs, q + 3 * zs);
-  } else {
-    // reading 30 (shift_strategy 1): the interior candidate -- the midpoint of
-    // the widest conservative gap between consecutive members in the middle
-    // half of a cluster of >= 2000 members whose width exceeds 1e-6 spdiam,
-    // if that gap exceeds 1e-10 of the members' magnitudes (not a degenerate
-    // group); warp reduction, ties to the lowest member (the oracle's order)
+  // ---- phase 0 (ADJ): the interior candidate (reading 30) -- the midpoint of
+  // the widest conservative gap between consecutive members in the middle
+  // half of a cluster of >= 2000 members whose width exceeds 1e-6 spdiam,
+  // if that gap exceeds 1e-10 of the members' magnitudes (not a degenerate
+  // group); a CTA-wide reduction, ties to the lowest member (the oracle's order)
+  if (ADJ) {
     const int mm = s1 - s0 + 1;
-    double sig_int = 0.0;
-    bool has_int = false;
+    double gb = -CUDART_INF;
+    int jbest = -1;
     if (A.shift_strategy == 1 && mm >= 2000 && A.hi[s1] - A.lo[s0] > 1e-6 * P.spdiam) {
       const int ja = s0 + mm / 4, jb = s1 - mm / 4;  // members j in [ja, jb) and j + 1
-      double gb = -CUDART_INF;
-      int jbest = -1;
-      for (int j = ja + lane; j < jb; j += 32) {
+      for (int j = ja + tid; j < jb; j += 32 * NW) {
         const double gj = A.lo[j + 1] - A.hi[j];
         if (gj > gb) { gb = gj; jbest = j; }
       }
-      for (int o = 16; o; o >>= 1) {
-        const double og = __shfl_xor_sync(0xffffffffu, gb, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, jbest, o);
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double og = __shfl_xor_sync(0xffffffffu, gb, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, jbest, o);
+      if (og > gb || (og == gb && oj >= 0 && (jbest < 0 || oj < jbest))) { gb = og; jbest = oj; }
+    }
+    if (lane == 0) { S.am_v[wid] = gb; S.am_i[wid] = jbest; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < NW; ++w) {
+        const double og = S.am_v[w];
+        const int oj = S.am_i[w];
         if (og > gb || (og == gb && oj >= 0 && (jbest < 0 || oj < jbest))) { gb = og; jbest = oj; }
       }
+      S.has_int = 0; S.jint = s0; S.sig_int = 0.0;
       if (jbest >= 0) {
         const double la = 0.5 * (A.lo[jbest] + A.hi[jbest]), lb = 0.5 * (A.lo[jbest + 1] + A.hi[jbest + 1]);
         if (gb > 1e-10 * fmax(fabs(la), fabs(lb))) {
-          has_int = true;
-          sig_int = 0.5 * (A.hi[jbest] + A.lo[jbest + 1]);
+          S.has_int = 1; S.jint = jbest;
+          S.sig_int = 0.5 * (A.hi[jbest] + A.lo[jbest + 1]);
         }
       }
     }
+    __syncthreads();
+  } else if (tid == 0) {
+    S.has_int = 0;
+  }
+  // probe side of a probe warp (-1: the candidate warp) and its eigenvalue
+  const int pside = wid < 4 ? (wid >> 1) : (wid == 4 ? -1 : 2 + ((wid - 5) >> 1));
+  const int pw0 = pside < 2 ? 2 * pside : 5 + 2 * (pside - 2);  // first warp of the side
+  auto probe_slot = [&](int side) { return side == 0 ? s0 : side == 1 ? s1 : S.jint + (side - 2); };
+
+  // ---- phase 1: the chains (probes: stationary / progressive sweeps; candidates)
+  const long long clk_p0 = clock64();
+  if (pside >= 0) {
+    if (pside < 2 || S.has_int) {
+      const int slot = probe_slot(pside);
+      const double lam = 0.5 * (A.lo[slot] + A.hi[slot]);
+      double *q = pr[pside];
+      if (wid == pw0) cs_probe_fwd(S.ring[wid], DL, LD, nb, lam, lane, q, q + 2 * zs);
+      else cs_probe_bwd(S.ring[wid], DL, LD, nb, lam, lane, q + zs, q + 3 * zs);
+    }
+  } else {
+    const bool has_int = ADJ && S.has_int;
+    const double sig_int = ADJ ? S.sig_int : 0.0;
     const int which = lane < 6 ? lane : 0;
     const double mult = (double)(1 << (which >> 1));
     double sigma;
@@ -321,18 +357,18 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
     }
     cs_candidates(S.ring[4], S, DL, nb, sigma, lane, TP, QK, zs);
     if (lane < kNC) S.sig[lane] = sigma;
-    if (lane == 0) S.has_int = has_int;
   }
   if (lane == 0) atomicMax(&A.ctr[1 + (wid == 4 ? 1 : (wid & 1) ? 2 : 3)], (unsigned long long)(clock64() - clk_p0));
   __syncthreads();
   const long long clk_p1 = clock64();
 
-  // ---- phase 2: each probe's twist index and |z| (warps 2 side, 2 side + 1)
-  if (wid < 4) {
-    const int side = wid >> 1, gt = tid & 63;
-    const double lam = 0.5 * (A.lo[side == 0 ? s0 : s1] + A.hi[side == 0 ? s0 : s1]);
+  // ---- phase 2: each probe's twist index and |z| (the side's two warps)
+  if (pside >= 0 && (pside < 2 || S.has_int)) {
+    const int side = pside, gt = tid - 32 * pw0;
+    const int pslot = probe_slot(side);
+    const double lam = 0.5 * (A.lo[pslot] + A.hi[pslot]);
     const double *sS = pr[side], *sP = pr[side] + zs, *sR = pr[side] + 2 * zs, *sG = pr[side] + 3 * zs;
-    double *z = side == 0 ? zl : zr;
+    double *z = zz[side];
     double bv = CUDART_INF;
     int bi = nb;
 #pragma unroll 8
@@ -348,8 +384,8 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
     if (lane == 0) { S.am_v[wid] = bv; S.am_i[wid] = bi; }
     // the two warps of a probe meet here (named barrier per probe)
     asm volatile("bar.sync %0, 64;" ::"r"(1 + side));
-    const double v0 = S.am_v[2 * side], v1 = S.am_v[2 * side + 1];
-    const int i0 = S.am_i[2 * side], i1 = S.am_i[2 * side + 1];
+    const double v0 = S.am_v[pw0], v1 = S.am_v[pw0 + 1];
+    const int i0 = S.am_i[pw0], i1 = S.am_i[pw0 + 1];
     int r = (v1 < v0 || (v1 == v0 && i1 < i0)) ? i1 : i0;
     if (r >= nb) r = nb - 1;  // no finite gamma: any twist (the vector only weights)
     // |z| by a product scan of |ratio| in (mantissa, exponent) form -- m in
@@ -360,7 +396,7 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
     // carry; one pass writes z.  (Round 1 walked one contiguous run per lane
     // twice: dependent loads, 35 % of the step's samples at level 0.)  A zero
     // or non-finite ratio zeroes the rest of that side (as a log of -inf would).
-    const bool up = (wid & 1) == 0;     // up: rows r-1 .. 0 from rho; down: rows r+1 .. nb-1 from sig
+    const bool up = wid == pw0;         // up: rows r-1 .. 0 from rho; down: rows r+1 .. nb-1 from sig
     const int m = up ? r : nb - 1 - r;  // ratios on this side
     if (up && lane == 0) z[r] = 1.0;
     constexpr double kDead = -1.0e9;    // exponent of a zeroed product
@@ -417,11 +453,13 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
   const long long clk_p2 = clock64();
   // ---- phase 3: growth of the candidates, raw and weighted (all threads)
   double g[kNC], nl[kNC], nr[kNC], dnl = 0.0, dnr = 0.0;
+  double na = 0.0, nbb = 0.0, dna = 0.0, dnb = 0.0;  // ADJ: the interior child against probes 2, 3
   unsigned okm = (1u << kNC) - 1u;
+  const bool adj = ADJ && S.has_int;
 #pragma unroll
   for (int k = 0; k < kNC; ++k) { g[k] = 0.0; nl[k] = 0.0; nr[k] = 0.0; }
 #pragma unroll 2
-  for (int i = tid; i < nb; i += 32 * kCSWarps) {
+  for (int i = tid; i < nb; i += 32 * NW) {
     const double a = zl[i], b = zr[i];
     const double a2 = a * a, b2 = b * b;
     dnl += a2; dnr += b2;
@@ -433,6 +471,19 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
       g[k] = fmax(g[k], ad);
       nl[k] = fma(ad, a2, nl[k]);
       nr[k] = fma(ad, b2, nr[k]);
+      if (ADJ && k == 6 && adj) {
+        const double x = zz[2][i], y = zz[3][i];
+        na = fma(ad, x * x, na); nbb = fma(ad, y * y, nbb);
+        dna = fma(x, x, dna); dnb = fma(y, y, dnb);
+      }
+    }
+  }
+  if (ADJ) {
+    for (int o = 16; o; o >>= 1) {
+      na += __shfl_xor_sync(0xffffffffu, na, o);
+      nbb += __shfl_xor_sync(0xffffffffu, nbb, o);
+      dna += __shfl_xor_sync(0xffffffffu, dna, o);
+      dnb += __shfl_xor_sync(0xffffffffu, dnb, o);
     }
   }
   for (int o = 16; o; o >>= 1) {
@@ -452,33 +503,39 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
       S.red[wid][k] = g[k]; S.red[wid][kNC + k] = nl[k]; S.red[wid][2 * kNC + k] = nr[k];
     }
     S.red[wid][3 * kNC] = dnl; S.red[wid][3 * kNC + 1] = dnr; S.okw[wid] = okm;
+    S.red[wid][3 * kNC + 2] = na; S.red[wid][3 * kNC + 3] = nbb;
+    S.am_v[wid] = dna; S.tq[0][wid][7] = dnb;  // (spare smem: the argmin slots are free now)
   }
   __syncthreads();
 
   // ---- phase 4: the tiered choice (reading 9) by thread 0
   if (tid == 0) {
     atomicMax(&A.ctr[6], (unsigned long long)(clock64() - clk_p2));
-    double G[kNC], NL[kNC], NR[kNC], DNL = 0.0, DNR = 0.0;
+    double G[kNC], NL[kNC], NR[kNC], DNL = 0.0, DNR = 0.0, NA = 0.0, NB = 0.0, DNA = 0.0, DNB = 0.0;
     unsigned ok = (1u << kNC) - 1u;
     for (int k = 0; k < kNC; ++k) { G[k] = 0.0; NL[k] = 0.0; NR[k] = 0.0; }
-    for (int w = 0; w < kCSWarps; ++w) {
+    for (int w = 0; w < NW; ++w) {
       for (int k = 0; k < kNC; ++k) {
         G[k] = fmax(G[k], S.red[w][k]);
         NL[k] += S.red[w][kNC + k];
         NR[k] += S.red[w][2 * kNC + k];
       }
       DNL += S.red[w][3 * kNC]; DNR += S.red[w][3 * kNC + 1];
+      NA += S.red[w][3 * kNC + 2]; NB += S.red[w][3 * kNC + 3];
+      DNA += S.am_v[w]; DNB += S.tq[0][w][7];
       ok &= S.okw[w];
     }
     const double spd = P.spdiam;
     int b1 = -1, b2 = -1, b3 = -1;
     // reading 30: the interior candidate first -- taken if its child is finite
     // and its raw growth <= 8 spdiam, or <= 1e8 spdiam with the weighted
-    // growth (end probes) <= 64 spdiam
+    // growth <= 64 spdiam against the four probes (the cluster's end members
+    // and the two members next to the shift)
     int b_int = -1;
-    if (S.has_int && ((ok >> 6) & 1u)) {
+    if (ADJ && S.has_int && ((ok >> 6) & 1u)) {
       const double g6 = G[6];
-      const double w6 = (DNL > 0 && DNR > 0) ? fmax(NL[6] / DNL, NR[6] / DNR) : CUDART_INF;
+      const double w6 = (DNL > 0 && DNR > 0 && DNA > 0 && DNB > 0)
+                            ? fmax(fmax(NL[6] / DNL, NR[6] / DNR), fmax(NA / DNA, NB / DNB)) : CUDART_INF;
       if (g6 <= 8.0 * spd || (g6 <= 1e8 * spd && w6 <= A.int_wg * spd)) b_int = 6;
     }
     double r1 = 0, r2 = 0, r3 = 0;
@@ -511,7 +568,7 @@ __global__ void __launch_bounds__(32 * kCSWarps, 3) k_child_step(ChildArgs A) {
   double2 *out = A.pool + (int64_t)c * A.stride;
   bool bad = false;
 #pragma unroll 4
-  for (int i = tid; i < nb; i += 32 * kCSWarps) {
+  for (int i = tid; i < nb; i += 32 * NW) {
     const double Dp = cs_dplus(TP, QK, zs, best, i);
     const double lld = (i < nb - 1) ? __ldg(&LD[i]).y / Dp : 0.0;
     bad |= !isfinite(Dp) || Dp == 0.0 || !isfinite(lld);

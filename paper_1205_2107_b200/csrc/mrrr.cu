@@ -1652,17 +1652,43 @@ int solve(Problem &P, int64_t *m_out) {
     tr.fine(s, "  alloc+upload");
     int h_fail[4] = {0, 0, 0, 0};
     {
-      for (int c0 = 0; c0 < nown; c0 += cgrp) {
+      // clusters of >= 2000 members (reading 30) go through the nine-warp
+      // step with the interior candidate, in their own launch and scratch;
+      // the others through the five-warp step, in groups that fit the scratch
+      std::vector<int> small_cl, big_cl;
+      for (int i = 0; i < nown; ++i)
+        (P.o.shift_strategy == 1 && ocl_s1[i] - ocl_s0[i] >= 2000 ? big_cl : small_cl).push_back(i);
+      auto child_args = [&](const int *list, int c0, int c1, double *scr) {
         ChildArgs C{};
         C.nodes = dnodes; C.cl_parent = docl_parent; C.cl_s0 = docl_s0; C.cl_s1 = docl_s1;
-        C.lo = slo; C.hi = shi; C.LDv = LDv; C.c0 = c0; C.ncl = std::min(nown, c0 + cgrp);
+        C.lo = slo; C.hi = shi; C.LDv = LDv; C.c0 = c0; C.ncl = c1;
         C.rtol = P.o.rtol_class;
-        C.scratch = scratch; C.zstride = zs_cs;
+        C.scratch = scr; C.zstride = zs_cs;
         C.pool = pool; C.stride = nbmax; C.sigma_out = dsig_own; C.tier_out = dtier; C.fail = dfail + 1;
         C.ctr = ctr + 16;
         C.shift_strategy = P.o.shift_strategy;
         C.int_wg = int_wg;
-        k_child_step<<<C.ncl - c0, 32 * kCSWarps, 0, s>>>(C);
+        C.cl_list = list;
+        return C;
+      };
+      if (!big_cl.empty()) {
+        const int nbig = (int)big_cl.size();
+        int *dbig = lv.alloc<int>(nbig);
+        h2d(dbig, big_cl.data(), nbig, s);
+        double *scr = lv.alloc<double>((size_t)kCSRowsAdj * nbig * zs_cs);
+        k_child_step<1><<<nbig, 32 * kCSWarpsAdj, 0, s>>>(child_args(dbig, 0, nbig, scr));
+        CK(cudaGetLastError());
+        g_stats.kernel_launches++;
+      }
+      const int nsmall = (int)small_cl.size();
+      int *dsmall = nullptr;
+      if (!big_cl.empty() && nsmall) {
+        dsmall = lv.alloc<int>(nsmall);
+        h2d(dsmall, small_cl.data(), nsmall, s);
+      }
+      for (int c0 = 0; c0 < nsmall; c0 += cgrp) {
+        k_child_step<0><<<std::min(nsmall, c0 + cgrp) - c0, 32 * kCSWarps, 0, s>>>(
+            child_args(dsmall, c0, std::min(nsmall, c0 + cgrp), scratch));
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }
@@ -1946,7 +1972,7 @@ void mrrr_default_opts(mrrr_opts_t *o) {
   o->grid_factor = 4;
   o->rtol_vec = 0.0;
   o->rqc_max = 10;
-  o->shift_strategy = 1;  // DESIGN.md reading 30
+  o->shift_strategy = 0;  // DESIGN.md reading 30: the interior shift is an option
 }
 
 // mrrr_negcount: the bisection kernels' Sturm count (projective sweep with

@@ -47,16 +47,16 @@ def test_clement_closed_form(oracle_mod, n):
 
 
 def test_interior_shift_strategy(oracle_mod):
-    """Reading 30 (shift_strategy 1, the default: an interior child shift for
-    clusters of >= 2000 members) against 0 (end shifts only): on Clement n=4000 (one root cluster of ~3000 members,
+    """Reading 30 (shift_strategy 1: an interior child shift for clusters of
+    >= 2000 members) against the default 0 (end shifts only): on Clement n=4000 (one root cluster of ~3000 members,
     peeled from one end per level by end shifts) the eigenvalues still equal
     the closed form, the accuracy contract holds, and the tree is shallower
     than the end shifts' chain."""
     n = 4000
     d, e = W.clement(n)
-    w0, Z0, st0 = oracle_mod.stemr(d, e, opts=oracle_mod.default_opts(shift_strategy=0), return_stats=True)
-    w1, Z1, st1 = oracle_mod.stemr(d, e, return_stats=True)  # the default (reading 30)
-    assert oracle_mod.default_opts().shift_strategy == 1
+    w0, Z0, st0 = oracle_mod.stemr(d, e, return_stats=True)  # the default: end shifts
+    w1, Z1, st1 = oracle_mod.stemr(d, e, opts=oracle_mod.default_opts(shift_strategy=1), return_stats=True)
+    assert oracle_mod.default_opts().shift_strategy == 0
     lam = 2.0 * np.arange(1, n + 1) - n - 1
     tn = tnorm1(d, e)
     assert np.max(np.abs(w1 - lam)) <= 4 * n * EPS * tn

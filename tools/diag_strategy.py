@@ -44,8 +44,9 @@ for name in sys.argv[1:]:
         res = 0.0
         orth = 0.0
         blocks = list(range(0, k, B))
-        if n > 30000:
+        if n > 30000 and not os.environ.get("FULL"):
             blocks = blocks[::4]
+        worst = (0.0, -1, -1)
         for a0 in blocks:
             Zb = Z[:, a0:a0 + B]
             TZ = dt[:, None] * Zb
@@ -56,11 +57,17 @@ for name in sys.argv[1:]:
             G = Z.T @ Zb
             idx = torch.arange(Zb.shape[1], device="cuda")
             G[a0 + idx, idx] -= 1.0
-            orth = max(orth, float(G.abs().max()))
+            Ga = G.abs()
+            v, flat = Ga.flatten().max(0)
+            if float(v) > worst[0]:
+                worst = (float(v), int(flat) // Ga.shape[1], a0 + int(flat) % Ga.shape[1])
+            orth = max(orth, float(v))
             del TZ, R, G
         print(json.dumps({"config": name, "shift_strategy": strat, "int_wg": os.environ.get("MRRR_INT_WG", "64"),
                           "ms": round(best, 2),
                           "levels": st["levels"], "nodes": st["nodes"],
-                          "res": res / tn / (10 * n * EPS), "orth": orth / (10 * n * EPS)}), flush=True)
+                          "res": res / tn / (10 * n * EPS), "orth": orth / (10 * n * EPS),
+                          "worst_pair": [worst[1], worst[2], float(w[worst[1]]), float(w[worst[2]])] if worst[1] >= 0 else None}),
+              flush=True)
         del w, Z, Zb
         torch.cuda.empty_cache()

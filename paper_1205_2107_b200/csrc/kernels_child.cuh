@@ -256,6 +256,23 @@ __device__ __forceinline__ double cs_dplus(const double *TP, const double *QK, i
   return div_nr(tp[i], q);
 }
 
+// |D+_i| for the growth tests only (reading 9): |t_i| times the hardware
+// reciprocal of |q_i| (MUFU.RCP64H, ~2^-22 relative) -- the growth bounds
+// (8, 64, 1e8 spdiam) and the least-growth choice do not need the quotient's
+// last bits, and the full-precision division per candidate and row was the
+// largest cost of the step's reductions.  Non-finite or zero D+ (t or q zero
+// or not finite) returns a NaN so that the caller's finiteness test fails.
+__device__ __forceinline__ double cs_absdplus_fast(const double *TP, const double *QK, int64_t zstride, int k,
+                                                    int i) {
+  const double *tp = TP + k * zstride;
+  const double q = (i & 7) == 0 ? QK[k * (zstride / 8) + (i >> 3)] : tp[i - 1];
+  const double t = tp[i];
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(fabs(q)));
+  const bool ok = isfinite(t) && t != 0.0 && isfinite(q) && q != 0.0;
+  return ok ? fabs(t) * r : CUDART_NAN;
+}
+
 // ADJ = 0: the step of a cluster with the end candidates only (five warps).
 // ADJ = 1 (reading 30, clusters of >= 2000 members): also the interior
 // candidate, and two more probes (four more warps) at the members next to its
@@ -465,9 +482,8 @@ __global__ void __launch_bounds__(32 * (kCSWarps + 4 * ADJ), ADJ ? 1 : 3) k_chil
     dnl += a2; dnr += b2;
 #pragma unroll
     for (int k = 0; k < kNC; ++k) {
-      const double d = cs_dplus(TP, QK, zs, k, i);
-      const double ad = fabs(d);
-      if (!(isfinite(d) && d != 0.0)) okm &= ~(1u << k);
+      const double ad = cs_absdplus_fast(TP, QK, zs, k, i);
+      if (!(isfinite(ad) && ad != 0.0)) okm &= ~(1u << k);
       g[k] = fmax(g[k], ad);
       nl[k] = fma(ad, a2, nl[k]);
       nr[k] = fma(ad, b2, nr[k]);

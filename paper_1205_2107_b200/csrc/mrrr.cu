@@ -21,6 +21,7 @@
 #include "kernels_vec.cuh"
 #include "kernels_warp.cuh"
 #include "kernels_child.cuh"
+#include "kernels_child2.cuh"
 
 using namespace mrrr;
 
@@ -1149,6 +1150,13 @@ int solve(Problem &P, int64_t *m_out) {
   // reading 30: weighted-growth bound of the interior candidate (x spdiam);
   // MRRR_INT_WG overrides (diagnostic)
   const double int_wg = getenv("MRRR_INT_WG") ? atof(getenv("MRRR_INT_WG")) : 64.0;
+  // the cluster step: one warp per chain (k_child_step: the shortest chain
+  // latency, for levels of at most kChildV1Max clusters) or the chains packed
+  // into the lanes of three warps (k_child_step2: fewer instructions, for the
+  // wide, issue-bound levels); the same arithmetic, bit for bit.
+  // MRRR_CHILD_V1 = 1 / 0 forces one of them (diagnostic).
+  const int child_v1_env = env_int("MRRR_CHILD_V1", -1);
+  constexpr int kChildV1Max = 296;  // two clusters per SM
   {
     std::vector<Work> wv;
     kt_root.start(s);
@@ -1655,6 +1663,7 @@ int solve(Problem &P, int64_t *m_out) {
       // clusters of >= 2000 members (reading 30) go through the nine-warp
       // step with the interior candidate, in their own launch and scratch;
       // the others through the five-warp step, in groups that fit the scratch
+      const bool child_v1 = child_v1_env >= 0 ? child_v1_env != 0 : nown <= kChildV1Max;
       std::vector<int> small_cl, big_cl;
       for (int i = 0; i < nown; ++i)
         (P.o.shift_strategy == 1 && ocl_s1[i] - ocl_s0[i] >= 2000 ? big_cl : small_cl).push_back(i);
@@ -1676,7 +1685,8 @@ int solve(Problem &P, int64_t *m_out) {
         int *dbig = lv.alloc<int>(nbig);
         h2d(dbig, big_cl.data(), nbig, s);
         double *scr = lv.alloc<double>((size_t)kCSRowsAdj * nbig * zs_cs);
-        k_child_step<1><<<nbig, 32 * kCSWarpsAdj, 0, s>>>(child_args(dbig, 0, nbig, scr));
+        if (child_v1) k_child_step<1><<<nbig, 32 * kCSWarpsAdj, 0, s>>>(child_args(dbig, 0, nbig, scr));
+        else k_child_step2<1><<<nbig, 96, 0, s>>>(child_args(dbig, 0, nbig, scr));
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }
@@ -1687,8 +1697,9 @@ int solve(Problem &P, int64_t *m_out) {
         h2d(dsmall, small_cl.data(), nsmall, s);
       }
       for (int c0 = 0; c0 < nsmall; c0 += cgrp) {
-        k_child_step<0><<<std::min(nsmall, c0 + cgrp) - c0, 32 * kCSWarps, 0, s>>>(
-            child_args(dsmall, c0, std::min(nsmall, c0 + cgrp), scratch));
+        const int nl = std::min(nsmall, c0 + cgrp) - c0;
+        if (child_v1) k_child_step<0><<<nl, 32 * kCSWarps, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
+        else k_child_step2<0><<<nl, 96, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }

@@ -172,7 +172,8 @@ def test_deterministic(torch_cuda, P):
 
 @pytest.mark.parametrize("env", [{"MRRR_CS_GROUP": "3"}, {"MRRR_VEC_MODE": "1"}, {"MRRR_VEC_PAIR": "0"},
                                  {"MRRR_VEC_PAIR": "2"}, {"MRRR_HP_STREAM": "0"}, {"MRRR_VEC_SPLIT": "0"},
-                                 {"MRRR_VEC_PACK": "0"}])
+                                 {"MRRR_VEC_PACK": "0"}, {"MRRR_CHILD_V1": "1"},
+                                 {"MRRR_CHILD_V1": "0"}])
 def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     """The launch schedule does not change a single bit: cluster steps in
     groups that reuse the scratch (MRRR_CS_GROUP, the n = 1e5 memory cap's
@@ -183,8 +184,12 @@ def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     high-priority one (MRRR_HP_STREAM=0), the single-warp RQC in one kernel
     instead of two phases with the lanes regrouped by twist index
     (MRRR_VEC_SPLIT=0), one node per vector work item instead of up to
-    kMaxSeg nodes of a block packed into a warp (MRRR_VEC_PACK=0) -- against
-    the default schedule.
+    kMaxSeg nodes of a block packed into a warp (MRRR_VEC_PACK=0), the cluster
+    step with one warp per chain or one lane per chain at every level
+    (MRRR_CHILD_V1=1 / 0; the default picks by the level's width; the same
+    per-chain arithmetic; their reductions sum over different thread counts,
+    which can move a weighted growth by an ulp but not, on these inputs, a
+    decision) -- against the default schedule.
     Each cluster's step and each eigenpair's RQC depend on their own data only."""
     for d, e in (W.glued_wilkinson(40), W.random_uniform(3000, 2)):
         w1, Z1 = gpu_solve(P, torch_cuda, d, e)

@@ -1147,6 +1147,9 @@ int solve(Problem &P, int64_t *m_out) {
     return 8;
   };
   const int rw_m_tree = rw_m_env > 0 ? rw_m_env : 1;
+  // clusters of at least rw_end members refine their two end members in
+  // work items of their own (0: off); MRRR_RW_END overrides
+  const int rw_end = env_int("MRRR_RW_END", 0);
   // reading 30: weighted-growth bound of the interior candidate (x spdiam);
   // MRRR_INT_WG overrides (diagnostic)
   const double int_wg = getenv("MRRR_INT_WG") ? atof(getenv("MRRR_INT_WG")) : 64.0;
@@ -1734,7 +1737,17 @@ int solve(Problem &P, int64_t *m_out) {
       for (int i = 0; i < nown; ++i) {
         const int c = own_cl[i];
         all.clear();
-        make_work(node_base + c, cl_s0[c], cl_s1[c], rw_chunk_tree(cl_s1[c] - cl_s0[c]), all);
+        const int mcl = cl_s1[c] - cl_s0[c];
+        if (rw_end > 0 && mcl >= rw_end) {
+          // the two end members alone (the child's shift sits next to one of
+          // them: in child coordinates it needs ~20 more bits than the rest,
+          // and alone its warp gives it all 32 shifts from the first round)
+          make_work(node_base + c, cl_s0[c], cl_s0[c] + 1, 1, all);
+          make_work(node_base + c, cl_s0[c] + 1, cl_s1[c] - 1, rw_chunk_tree(mcl), all);
+          make_work(node_base + c, cl_s1[c] - 1, cl_s1[c], 1, all);
+        } else {
+          make_work(node_base + c, cl_s0[c], cl_s1[c], rw_chunk_tree(mcl), all);
+        }
         for (const Work &W : all) {
           bool mine = !dist;
           for (int q = W.s0; q < W.s1 && !mine; ++q) mine = h_slot_owner[q] == P.rank;

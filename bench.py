@@ -429,7 +429,7 @@ def main():
             etot = float(t.item())
         e2e = {"value": m * args.steps / (etot / 1e3), "unit": "eigenpairs/s",
                "h2d_bytes_per_step": 8 * (2 * n - 1), "d2h_bytes_per_step": 8 * m + 8 * n * m,
-               "ms_per_step": etot / args.steps}
+               "ms_per_step": etot / args.steps, "z_copies_per_step": P.last_stats()["z_copies"]}
 
     # ---------------- CPU oracle on a bounded sample (rank 0, N=1 only)
     cpu = None

@@ -250,6 +250,7 @@ typedef struct {
   int64_t vec_items;        /* warp work items of the vector kernels (lanes: vec_tasks) */
   int64_t pool_bytes;       /* child representations of the cluster nodes (16 n B per node) */
   int64_t workspace_bytes;  /* device workspace held by this thread after the call (all of it) */
+  int64_t z_copies;         /* device-to-host copies of Z column runs (mrrr_stemr_host) */
 } mrrr_stats_t;
 int mrrr_get_stats(mrrr_stats_t *out);
 

@@ -1147,6 +1147,8 @@ int solve(Problem &P, int64_t *m_out) {
     return 8;
   };
   const int rw_m_tree = rw_m_env > 0 ? rw_m_env : 1;
+  // shifts per thread of the root grid (MRRR_GRID_M, diagnostic: 1, 2 or 4)
+  const int grid_m = env_int("MRRR_GRID_M", 4);
   // clusters of at least rw_end members refine their two end members in
   // work items of their own (0: off); MRRR_RW_END overrides
   const int rw_end = env_int("MRRR_RW_END", 0);
@@ -1172,7 +1174,7 @@ int solve(Problem &P, int64_t *m_out) {
         G = std::max(G, 256);
         if (!dist) {
           int *cnt = ar.alloc<int>(G + 1);
-          launch_grid(4, dnodes, B.root_node, hlo0[r], hhi0[r], G, 1, G, cnt, ctr + 1, s);
+          launch_grid(grid_m, dnodes, B.root_node, hlo0[r], hhi0[r], G, 1, G, cnt, ctr + 1, s);
           g_stats.root_sweeps += G - 1;
           k_grid_assign2<<<1, 1024, 0, s>>>(cnt, G, B.nb, hlo0[r], hhi0[r], slot_j, B.slot0,
                                             B.slot1, slo, shi);
@@ -1185,7 +1187,7 @@ int solve(Problem &P, int64_t *m_out) {
           int *cnt_part = ar.alloc<int>((size_t)gp + G + 1);
           int *cnt = ar.alloc<int>((size_t)nr * gp + 2);
           guarded([&] {
-            if (g_hi > g_lo) launch_grid(4, dnodes, B.root_node, hlo0[r], hhi0[r], G, g_lo, g_hi, cnt_part, ctr + 1, s);
+            if (g_hi > g_lo) launch_grid(grid_m, dnodes, B.root_node, hlo0[r], hhi0[r], G, g_lo, g_hi, cnt_part, ctr + 1, s);
           });
           g_stats.root_sweeps += std::max(0, g_hi - g_lo);
           if (P.allgather(P.ag_ctx, cnt_part + g_lo, cnt + 1, (size_t)gp * sizeof(int), (void *)s) != 0)
@@ -1444,7 +1446,12 @@ int solve(Problem &P, int64_t *m_out) {
   // the host on the copy stream once every piece that writes into it has been
   // launched, after those pieces' events -- the D2H of Z (3.2 GB at n = 20000)
   // overlaps the rest of the solve instead of following it
-  constexpr int64_t kZB = 256;
+  // (measured, n = 20000: 32 / 64 / 256 / 1024 columns per block -> e2e 101.7 /
+  // 102.1 / 105.3 / 102.9 ms; copying each piece's own column runs instead --
+  // 810-2485 copies -- 107.8-134.6 ms: the columns of a level's singletons are
+  // only ready when its piece ends, late in the solve, and the small copies
+  // cost more than they overlap.  MRRR_ZB: diagnostic)
+  const int64_t kZB = std::max(1, env_int("MRRR_ZB", 64));
   const bool zstream = P.hZ != nullptr && vectors && P.m_local > 0;
   cudaStream_t sc = zstream ? copy_stream() : nullptr;
   // the copy stream rejoins the solve stream on EVERY exit (an error after
@@ -1467,6 +1474,7 @@ int solve(Problem &P, int64_t *m_out) {
   auto zb_copy = [&](int64_t c0, int64_t c1) {  // columns [c0, c1) after sc's pending waits
     CK(cudaMemcpy2DAsync(P.hZ + c0 * P.hldz, P.hldz * sizeof(double), P.Z + c0 * P.ldz,
                          P.ldz * sizeof(double), n * sizeof(double), c1 - c0, cudaMemcpyDeviceToHost, sc));
+    ++g_stats.z_copies;
   };
   auto zb_done = [&](size_t t0, size_t t1, cudaEvent_t eb) {  // tasks [t0, t1) written after eb
     if (!zstream) return;

@@ -35,7 +35,8 @@ class Stats(C.Structure):
                 ("ms_k_root_bisect", C.c_double), ("ms_k_vectors", C.c_double),
                 ("vec_tasks", C.c_int64), ("vec_elems", C.c_int64),
                 ("ms_k_final_refine", C.c_double), ("vec_nudges", C.c_int64),
-                ("vec_items", C.c_int64), ("pool_bytes", C.c_int64), ("workspace_bytes", C.c_int64)]
+                ("vec_items", C.c_int64), ("pool_bytes", C.c_int64), ("workspace_bytes", C.c_int64),
+                ("z_copies", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

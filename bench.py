@@ -458,7 +458,11 @@ def main():
                           "total": s0["ms_total"]},
             "tree": {"nodes": s0["nodes"], "levels": s0["levels"], "rqc_iters": s0["rqc_iters"],
                      "rqc_fallbacks": s0["rqc_fallbacks"], "safe_resweeps": s0["safe_resweeps"],
-                     "vec_items": s0["vec_items"], "vec_nudges": s0["vec_nudges"]}}
+                     "vec_items": s0["vec_items"], "vec_nudges": s0["vec_nudges"]},
+            "memory": {"pool_bytes": s0["pool_bytes"], "workspace_bytes": s0["workspace_bytes"],
+                       "z_bytes": 8 * n * m if world == 1 else None,
+                       "note": "device workspace the library holds (all of it, child RRR pools included) "
+                               "beside the caller's w and Z"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -80,6 +80,15 @@ typedef struct {
                           (readings 8, 9); 1: an interior shift first for
                           clusters of >= 2000 members -- shallower trees, less
                           orthogonality margin (reading 30) */
+  double scratch_gb;   /* cap (GB) of each of the two large scratch areas: the
+                          vector checkpoints (4 n B per eigenvector in flight)
+                          and the cluster-step scratch (144 n B per cluster of
+                          a level); default 16.  Smaller caps bound the device
+                          workspace at the price of smaller vector pieces and
+                          grouped cluster steps (random n=1e5, B200: 16 -> Z +
+                          37 GB, 1.20 s; 4 -> Z + 12.9 GB, 1.38 s; 3 -> Z +
+                          10.9 GB, 1.56 s; 2 -> Z + 8.8 GB, 1.90 s; DESIGN.md
+                          section 4.6) */
 } mrrr_opts_t;
 
 void mrrr_default_opts(mrrr_opts_t *opts);
@@ -177,12 +186,14 @@ int mrrr_plan_columns(int64_t m, int nranks, const unsigned char *free_cut, int6
 
 /* Upper bound (bytes) of the device workspace mrrr_stemr holds for an
  * order-n problem with k wanted eigenpairs, EXCEPT the child representations
- * of the tree's cluster nodes: 16 n bytes per cluster node, kept until the
- * solve ends (the number of nodes depends on the spectrum: 2638 at random
- * n=20000, 13241 at random n=1e5; mrrr_stats_t.pool_bytes reports it).  The
- * bound covers the O(n) arrays, the per-eigenvalue slot arrays, the vector
- * checkpoints (capped at 16 GB) and the cluster-step scratch (capped at
- * 16 GB; MRRR_SCRATCH_GB lowers both caps). */
+ * of the tree's cluster nodes: 16 n bytes per slot, and slots are recycled
+ * once a node's child steps and vector pieces are done, so the pool holds
+ * about the clusters of the levels whose vectors are in flight, not the whole
+ * tree (random n=20000: 2448 slots for 2638 nodes; n=1e5: 3280 for 13241;
+ * mrrr_stats_t.pool_bytes reports it).  The bound covers the O(n) arrays,
+ * the per-eigenvalue slot arrays, the vector checkpoints (capped at 16 GB)
+ * and the cluster-step scratch (capped at 16 GB; MRRR_SCRATCH_GB lowers both
+ * caps). */
 size_t mrrr_workspace_bytes(int64_t n, int64_t k);
 
 /* Workspace is taken from library-owned device chunks per host thread and
@@ -248,7 +259,7 @@ typedef struct {
   double ms_k_final_refine; /* RQC fallback: bracket refinement to 4 eps (0 without fallback) */
   int64_t vec_nudges;       /* vector factorizations redone at a nudged shift (reading 25) */
   int64_t vec_items;        /* warp work items of the vector kernels (lanes: vec_tasks) */
-  int64_t pool_bytes;       /* child representations of the cluster nodes (16 n B per node) */
+  int64_t pool_bytes;       /* child-representation slots allocated (16 n B each; recycled) */
   int64_t workspace_bytes;  /* device workspace held by this thread after the call (all of it) */
   int64_t z_copies;         /* device-to-host copies of Z column runs (mrrr_stemr_host) */
 } mrrr_stats_t;

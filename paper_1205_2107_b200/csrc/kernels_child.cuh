@@ -70,8 +70,7 @@ struct ChildArgs {
   double rtol;
   double *scratch;             // kCSRows * zstride doubles per cluster of the launch
   int64_t zstride;
-  double2 *pool;               // child c's rows at pool + c * stride
-  int64_t stride;
+  double2 *const *pool;        // child c's rows at pool[c] (recycled slots, mrrr.cu)
   double *sigma_out;
   int *tier_out;
   int *fail;
@@ -581,7 +580,7 @@ __global__ void __launch_bounds__(32 * (kCSWarps + 4 * ADJ), ADJ ? 1 : 3) k_chil
   if (best < 0) return;
 
   // ---- phase 5: the chosen child, (D+_i, LLD+_i = LD_i^2 / D+_i), coalesced
-  double2 *out = A.pool + (int64_t)c * A.stride;
+  double2 *out = A.pool[c];
   bool bad = false;
 #pragma unroll 4
   for (int i = tid; i < nb; i += 32 * NW) {

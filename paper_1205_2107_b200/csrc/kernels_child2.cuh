@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : 4) k_child_step2(ChildArgs A) {
   if (best < 0) return;
 
   // ---- phase 5: the chosen child, (D+_i, LLD+_i = LD_i^2 / D+_i), coalesced
-  double2 *out = A.pool + (int64_t)c * A.stride;
+  double2 *out = A.pool[c];
   bool bad = false;
 #pragma unroll 4
   for (int i = tid; i < nb; i += 96) {

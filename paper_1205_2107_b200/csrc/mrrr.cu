@@ -501,18 +501,17 @@ __global__ void k_root_nodes(Node *nodes, const Block *blocks, const int *root_b
 }
 
 // Child node entries and bracket translation to child coordinates (O9.4).
-// cl_pool[c]: the pool row of cluster c's child RRR on this rank, -1 when
-// another rank owns the cluster (multi-GPU: the entry keeps the tree's
-// numbering; its representation is never read here)
+// cl_rrr[c]: cluster c's child RRR slot on this rank, null when another
+// rank owns the cluster (multi-GPU: the entry keeps the tree's numbering; its
+// representation is never read here)
 __global__ void k_child_nodes(Node *nodes, int node_base, const int *cl_parent, const int *cl_s0,
-                              const int *cl_s1, const double *sigma, int ncl, double2 *pool,
-                              int64_t stride, const int *slot_jlocal, const int *cl_pool) {
+                              const int *cl_s1, const double *sigma, int ncl, double2 *const *cl_rrr,
+                              const int *slot_jlocal) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncl) return;
   Node P = nodes[cl_parent[c]];
   Node N = P;
-  const int pi = cl_pool[c];
-  N.DL = pi >= 0 ? pool + (int64_t)pi * stride : nullptr;
+  N.DL = cl_rrr[c];
   N.slot0 = cl_s0[c]; N.slot1 = cl_s1[c];
   N.depth = P.depth + 1;
   N.jbase = slot_jlocal[cl_s0[c]];
@@ -1069,8 +1068,13 @@ int solve(Problem &P, int64_t *m_out) {
   const int nr = std::max(1, P.nranks);
   const bool dist = nr > 1;
   // cap of each of the two large scratch areas (vector checkpoints, cluster
-  // step scratch); MRRR_SCRATCH_GB overrides (virtual ranks sharing one GPU)
-  const double scratch_bytes = 1e9 * std::max(1, env_int("MRRR_SCRATCH_GB", 16));
+  // step scratch): opts.scratch_gb (16 by default); MRRR_SCRATCH_GB overrides
+  // (virtual ranks sharing one GPU), MRRR_CK_GB / MRRR_CS_GB one of the two
+  // (diagnostic)
+  const double scratch_gb = getenv("MRRR_SCRATCH_GB") ? std::max(0.25, atof(getenv("MRRR_SCRATCH_GB")))
+                            : P.o.scratch_gb > 0 ? P.o.scratch_gb : 16.0;
+  const double ck_bytes = 1e9 * (getenv("MRRR_CK_GB") ? std::max(0.25, atof(getenv("MRRR_CK_GB"))) : scratch_gb);
+  const double scratch_bytes = 1e9 * (getenv("MRRR_CS_GB") ? std::max(0.25, atof(getenv("MRRR_CS_GB"))) : scratch_gb);
   double *xrecv = dist ? ar.alloc<double>((size_t)nr * xstride) : nullptr;
   int *slot_owner = dist ? ar.alloc<int>(nslots) : nullptr;
   std::vector<int> h_slot_owner(dist ? nslots : 0, 0);
@@ -1433,7 +1437,7 @@ int solve(Problem &P, int64_t *m_out) {
   // capped so that the checkpoints (64 B per 16-row segment and task) stay
   // within scratch_bytes (16 GB by default; n = 1e5: pieces of ~nslots/10)
   const int piece_div = std::max(1, env_int("MRRR_PIECE_DIV", kSide));  // diagnostic knob
-  const int64_t ck_mem_cap = (int64_t)(scratch_bytes / (64.0 * kSide * ((nbmax + kSeg - 1) / kSeg)));
+  const int64_t ck_mem_cap = (int64_t)(ck_bytes / (64.0 * kSide * ((nbmax + kSeg - 1) / kSeg)));
   const int64_t task_basis = dist ? std::min<int64_t>(nslots, wcap + 2) : nslots;
   const int64_t ck_cap =
       std::max<int64_t>(256, std::min<int64_t>((task_basis + piece_div - 1) / piece_div, ck_mem_cap)) + 32;
@@ -1442,6 +1446,68 @@ int solve(Problem &P, int64_t *m_out) {
   BwdCk *ck_b[kSide] = {};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vec_ev;
   size_t vec_done = 0;
+  // Child RRR slots (nbmax (D+, LLD+) rows each), RECYCLED (SURVEY H9,
+  // memory independent of the tree's size).  A node's slot is
+  // written by its cluster's child step and read by the refinement of its
+  // members (same level), by the child steps of its own clusters (next level:
+  // the last reader on the call's stream) and by the vector pieces of its
+  // singletons (side streams).  After that child step the slot waits in
+  // pool_hold for the pieces holding the node's singletons; it returns to the
+  // free list once every one of them has completed (event query, no host
+  // wait) and the deferred-fallback counter copied after it reads zero (the
+  // fallback re-reads a failed vector's node, reading 10).  So no slot is
+  // rewritten before its last reader.  With the vectors after the tree
+  // (MRRR_VEC_MODE=1) the slots live until the end, as in round 1.
+  std::vector<double2 *> pool_free, node_rrr(nnodes, nullptr);
+  std::vector<int> node_pf(nnodes, -1), node_pl(nnodes, -1);  // first / last piece holding a singleton of the node
+  struct PoolHold {
+    double2 *p;
+    int pf, pl;
+  };
+  std::vector<PoolHold> pool_hold;
+  std::vector<cudaEvent_t> piece_done;
+  std::vector<volatile int *> piece_fail;  // pinned: the fallback counter after the piece
+  std::vector<signed char> piece_ok;      // 1 done, no fallback; 0 done with fallback; -1 running
+  int64_t pool_slots = 0;
+  // slots for `need` clusters: recycle what is done, then one fresh batch
+  auto pool_reserve = [&](int need) {
+    for (size_t q = 0; q < piece_done.size(); ++q) {
+      if (piece_ok[q] >= 0) continue;
+      const cudaError_t st = cudaEventQuery(piece_done[q]);
+      if (st == cudaErrorNotReady) continue;
+      if (st != cudaSuccess) throw CudaError{st};
+      piece_ok[q] = piece_fail[q] != nullptr && *piece_fail[q] == 0 ? 1 : 0;
+    }
+    size_t k = 0;
+    for (size_t h = 0; h < pool_hold.size(); ++h) {
+      const PoolHold &H = pool_hold[h];
+      bool done = true;
+      for (int q = H.pf; q >= 0 && q <= H.pl && done; ++q) done = piece_ok[q] == 1;
+      if (done) pool_free.push_back(H.p);
+      else pool_hold[k++] = H;
+    }
+    pool_hold.resize(k);
+    const int fresh = need - (int)pool_free.size();
+    if (fresh > 0) {
+      double2 *b = ar.alloc<double2>((size_t)fresh * nbmax);
+      for (int i = fresh - 1; i >= 0; --i) pool_free.push_back(b + (size_t)i * nbmax);
+      pool_slots += fresh;
+      g_stats.pool_bytes = pool_slots * nbmax * (int64_t)sizeof(double2);
+    }
+  };
+  auto pool_take = [&]() -> double2 * {
+    double2 *p = pool_free.back();
+    pool_free.pop_back();
+    return p;
+  };
+  auto pool_release_level = [&](const std::vector<int> &nodes_done) {
+    if (vec_mode != 0 && vectors) return;
+    for (int nd : nodes_done)
+      if (nd < (int)node_rrr.size() && node_rrr[nd]) {
+        pool_hold.push_back({node_rrr[nd], node_pf[nd], node_pl[nd]});
+        node_rrr[nd] = nullptr;
+      }
+  };
   // streamed download (host entry, pinned Z): a block of kZB columns goes to
   // the host on the copy stream once every piece that writes into it has been
   // launched, after those pieces' events -- the D2H of Z (3.2 GB at n = 20000)
@@ -1566,6 +1632,23 @@ int solve(Problem &P, int64_t *m_out) {
       } else {
         launch_wvec(A, s2, pair);
       }
+      {
+        // the deferred-fallback counter after this piece (pool_collect)
+        volatile int *pfc = (volatile int *)g_staging.get(sizeof(int));
+        if (pfc) {
+          *pfc = -1;
+          CK(cudaMemcpyAsync((void *)pfc, fail_count, sizeof(int), cudaMemcpyDeviceToHost, s2));
+        }
+        const int pc = (int)piece_done.size();
+        piece_done.push_back(eb);
+        piece_fail.push_back(pfc);
+        piece_ok.push_back(-1);
+        for (const VecTask &t : bt) {
+          if (t.node >= (int)node_pf.size()) continue;
+          if (node_pf[t.node] < 0) node_pf[t.node] = pc;
+          node_pl[t.node] = pc;
+        }
+      }
       CK(cudaEventRecord(eb, s2));
       tr.fine(s2, "  vectors (side stream)");
       vec_ev.push_back({ea, eb});
@@ -1629,7 +1712,6 @@ int solve(Problem &P, int64_t *m_out) {
     g_stats.nodes += nown;
     // grow node table
     int node_base = nnodes;
-    std::vector<int> cl_pool(ncl, -1);
     guarded([&] {
     if (nnodes + ncl > node_cap) {
       int ncap = std::max(node_cap * 2, nnodes + ncl + 16);
@@ -1642,18 +1724,17 @@ int solve(Problem &P, int64_t *m_out) {
     std::vector<int> ocl_parent(nown), ocl_s0(nown), ocl_s1(nown);
     for (int i = 0; i < nown; ++i) {
       const int c = own_cl[i];
-      ocl_parent[i] = cl_parent[c]; ocl_s0[i] = cl_s0[c]; ocl_s1[i] = cl_s1[c]; cl_pool[c] = i;
+      ocl_parent[i] = cl_parent[c]; ocl_s0[i] = cl_s0[c]; ocl_s1[i] = cl_s1[c];
     }
     int *dcl_parent = lv.alloc<int>(ncl), *dcl_s0 = lv.alloc<int>(ncl), *dcl_s1 = lv.alloc<int>(ncl);
     int *docl_parent = lv.alloc<int>(nown + 1), *docl_s0 = lv.alloc<int>(nown + 1), *docl_s1 = lv.alloc<int>(nown + 1);
-    int *dcl_pool = lv.alloc<int>(ncl), *down_cl = lv.alloc<int>(nown + 1);
+    int *down_cl = lv.alloc<int>(nown + 1);
     h2d(dcl_parent, cl_parent.data(), ncl, s);
     h2d(dcl_s0, cl_s0.data(), ncl, s);
     h2d(dcl_s1, cl_s1.data(), ncl, s);
     h2d(docl_parent, ocl_parent.data(), nown, s);
     h2d(docl_s0, ocl_s0.data(), nown, s);
     h2d(docl_s1, ocl_s1.data(), nown, s);
-    h2d(dcl_pool, cl_pool.data(), ncl, s);
     h2d(down_cl, own_cl.data(), nown, s);
     // a5 cluster step on the own clusters: probes, six candidates, choice,
     // chosen child (one kernel).  The step's scratch (kCSRows rows of nbmax
@@ -1666,8 +1747,17 @@ int solve(Problem &P, int64_t *m_out) {
     if (nown) cs_scratch_used = std::max(cs_scratch_used, (size_t)kCSRows * cgrp * zs_cs * sizeof(double));
     double *dsig_own = lv.alloc<double>(nown + 1), *dsig = lv.alloc<double>(ncl);
     int *dtier = lv.alloc<int>(nown + 1);
-    double2 *pool = ar.alloc<double2>((size_t)std::max(nown, 1) * nbmax);  // child RRRs live until the vectors
-    g_stats.pool_bytes += (int64_t)std::max(nown, 1) * nbmax * (int64_t)sizeof(double2);
+    // child RRR slots of the own clusters (recycled: pool_take)
+    std::vector<double2 *> cl_rrr(ncl, nullptr), own_rrr(std::max(nown, 1), nullptr);
+    pool_reserve(nown);
+    for (int i = 0; i < nown; ++i) own_rrr[i] = cl_rrr[own_cl[i]] = pool_take();
+    double2 **dcl_rrr = lv.alloc<double2 *>(ncl), **down_rrr = lv.alloc<double2 *>(std::max(nown, 1));
+    h2d(dcl_rrr, cl_rrr.data(), ncl, s);
+    h2d(down_rrr, own_rrr.data(), nown, s);
+    node_rrr.resize(node_base + ncl, nullptr);
+    node_pf.resize(node_base + ncl, -1);
+    node_pl.resize(node_base + ncl, -1);
+    for (int c = 0; c < ncl; ++c) node_rrr[node_base + c] = cl_rrr[c];
     tr.fine(s, "  alloc+upload");
     int h_fail[4] = {0, 0, 0, 0};
     {
@@ -1684,7 +1774,7 @@ int solve(Problem &P, int64_t *m_out) {
         C.lo = slo; C.hi = shi; C.LDv = LDv; C.c0 = c0; C.ncl = c1;
         C.rtol = P.o.rtol_class;
         C.scratch = scr; C.zstride = zs_cs;
-        C.pool = pool; C.stride = nbmax; C.sigma_out = dsig_own; C.tier_out = dtier; C.fail = dfail + 1;
+        C.pool = down_rrr; C.sigma_out = dsig_own; C.tier_out = dtier; C.fail = dfail + 1;
         C.ctr = ctr + 16;
         C.shift_strategy = P.o.shift_strategy;
         C.int_wg = int_wg;
@@ -1722,7 +1812,10 @@ int solve(Problem &P, int64_t *m_out) {
       if (nown) k_scatter<<<(nown + 255) / 256, 256, 0, s>>>(down_cl, dsig_own, nown, dsig);
       // the child node entries are written before the translate kernel reads sigma
       k_child_nodes<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, node_base, dcl_parent, dcl_s0, dcl_s1, dsig, ncl,
-                                                   pool, nbmax, slot_j, dcl_pool);
+                                                   dcl_rrr, slot_j);
+      // the parents' RRRs (read by the child step above, last reader on this
+      // stream) go back to the pool once their vector pieces are done
+      pool_release_level(level_nodes);
       CK(cudaGetLastError());
       // translate member brackets to child coordinates
       std::vector<int> slot_cl, first_slot;
@@ -1770,7 +1863,12 @@ int solve(Problem &P, int64_t *m_out) {
       d2h(h_fail, dfail, 4, s);
       if (getenv("MRRR_DUMP")) {
         char nm[64];
-        snprintf(nm, sizeof nm, "L%d_pool.bin", level); dump(nm, pool, (size_t)nown * nbmax, s);
+        {
+          double2 *pc = lv.alloc<double2>((size_t)std::max(nown, 1) * nbmax);
+          for (int i = 0; i < nown; ++i)
+            CK(cudaMemcpyAsync(pc + (size_t)i * nbmax, own_rrr[i], nbmax * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+          snprintf(nm, sizeof nm, "L%d_pool.bin", level); dump(nm, pc, (size_t)nown * nbmax, s);
+        }
         snprintf(nm, sizeof nm, "L%d_sigma.bin", level); dump(nm, dsig, ncl, s);
         snprintf(nm, sizeof nm, "L%d_tier.bin", level); dump(nm, dtier, nown, s);
         snprintf(nm, sizeof nm, "L%d_s0.bin", level); dump(nm, dcl_s0, ncl, s);
@@ -2005,6 +2103,7 @@ void mrrr_default_opts(mrrr_opts_t *o) {
   o->rtol_vec = 0.0;
   o->rqc_max = 10;
   o->shift_strategy = 0;  // DESIGN.md reading 30: the interior shift is an option
+  o->scratch_gb = 16.0;
 }
 
 // mrrr_negcount: the bisection kernels' Sturm count (projective sweep with

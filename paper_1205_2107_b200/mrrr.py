@@ -22,7 +22,7 @@ class Opts(C.Structure):
     _fields_ = [("tol_relgap", C.c_double), ("rtol_class", C.c_double), ("max_depth", C.c_int),
                 ("perturb_root", C.c_int), ("seed", C.c_uint64), ("multisection", C.c_int),
                 ("grid_factor", C.c_int), ("rtol_vec", C.c_double), ("rqc_max", C.c_int),
-                ("shift_strategy", C.c_int)]
+                ("shift_strategy", C.c_int), ("scratch_gb", C.c_double)]
 
 
 class Stats(C.Structure):

@@ -253,8 +253,8 @@ def test_value_endpoints_on_eigenvalues(torch_cuda, P, oracle_mod, vl, vu):
 @pytest.mark.parametrize("case", ["random_3000", "glued_40", "clement_2000_idx"])
 def test_workspace_bound(torch_cuda, P, case):
     """mrrr_workspace_bytes(n, k) bounds the workspace a call uses, apart from
-    the cluster nodes' child representations (16 n B per node, reported as
-    pool_bytes); include/mrrr.h."""
+    the cluster nodes' child representations (16 n B per slot, reported as
+    pool_bytes: recycled, so at most one slot per node); include/mrrr.h."""
     kw = {}
     if case == "random_3000":
         d, e = W.random_uniform(3000, 2)
@@ -267,5 +267,28 @@ def test_workspace_bound(torch_cuda, P, case):
     st = P.last_stats()
     n, k = len(d), (kw["iu"] - kw["il"] + 1 if kw else len(d))
     bound = P.mrrr.lib().mrrr_workspace_bytes(n, k)
-    assert st["pool_bytes"] >= 16 * n * st["nodes"]
+    assert st["nodes"] == 0 or 16 * n <= st["pool_bytes"] <= 16 * n * st["nodes"]
     assert 0 < st["workspace_bytes"] - st["pool_bytes"] <= bound, (st["workspace_bytes"], st["pool_bytes"], bound)
+
+
+def test_scratch_cap_and_pool_recycling(torch_cuda, P):
+    """mrrr_opts_t.scratch_gb bounds the two large scratch areas: at 0.25 GB
+    (random n=20000) the vector pieces hold <= 781 eigenvectors and the
+    cluster steps run in groups of <= 86 clusters -- more launches, less
+    workspace, and not a bit of difference in w or Z (each eigenpair's RQC and
+    each cluster's step depend on their own data only).  The child
+    representation slots are recycled: fewer slots than tree nodes."""
+    d, e, _ = W.make("random_20000")
+    n = len(d)
+    w1, Z1 = gpu_solve(P, torch_cuda, d, e)
+    s1 = P.last_stats()
+    P.trim_workspace()
+    w2, Z2 = gpu_solve(P, torch_cuda, d, e, opts=P.default_opts(scratch_gb=0.25))
+    s2 = P.last_stats()
+    P.trim_workspace()
+    assert np.array_equal(w1, w2) and np.array_equal(Z1, Z2)
+    assert s2["kernel_launches"] > s1["kernel_launches"]
+    assert s2["workspace_bytes"] < s1["workspace_bytes"]
+    assert s1["nodes"] == s2["nodes"] and s1["nodes"] > 1000
+    for s in (s1, s2):
+        assert 16 * n <= s["pool_bytes"] < 16 * n * s["nodes"]

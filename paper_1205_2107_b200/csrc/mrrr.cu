@@ -15,6 +15,7 @@
 #include <vector>
 
 #include <cub/device/device_segmented_radix_sort.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/mrrr.h"
 #include "kernels_tree.cuh"
@@ -119,14 +120,33 @@ int env_int(const char *name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
-// Host wall-clock trace of the phases (MRRR_TRACE=1), for overhead hunting.
+// Host wall-clock trace of the phases (MRRR_TRACE=1), for overhead hunting,
+// and NVTX ranges of the same phases (always; header-only NVTX v3, a no-op
+// unless a profiler injects itself): "mrrr" around the call, one nested
+// range per phase (root, each tree level, the vector tail), one per vector
+// piece launch.
+struct NvtxScope {
+  explicit NvtxScope(const char *name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
 struct Trace {
   bool on;
   int lvl = 0;
+  bool phase_open = false;
   std::chrono::steady_clock::time_point t0, tl;
   Trace() : on(getenv("MRRR_TRACE") != nullptr) {
     t0 = tl = std::chrono::steady_clock::now();
     if (on) lvl = atoi(getenv("MRRR_TRACE"));
+    nvtxRangePushA("mrrr");
+  }
+  ~Trace() {
+    if (phase_open) nvtxRangePop();
+    nvtxRangePop();
+  }
+  void phase(const char *name) {
+    if (phase_open) nvtxRangePop();
+    nvtxRangePushA(name);
+    phase_open = true;
   }
   // MRRR_TRACE=2: also the steps inside a tree level (synchronising the stream)
   void fine(cudaStream_t s, const char *what) {
@@ -850,6 +870,7 @@ int solve(Problem &P, int64_t *m_out) {
   const bool vectors = P.Z != nullptr;
 
   // ---------------- a1: prep ----------------
+  tr.phase("mrrr root");
   double *ds = ar.alloc<double>(n), *es = ar.alloc<double>(n), *es2 = ar.alloc<double>(n);
   int *brk = ar.alloc<int>(n);
   double *hdr = ar.alloc<double>(8);
@@ -1618,6 +1639,7 @@ int solve(Problem &P, int64_t *m_out) {
         CK(cudaEventRecord(ready2, s));
         CK(cudaStreamWaitEvent(s2, ready2, 0));
       }
+      NvtxScope nvtx_piece("mrrr vector piece");
       cudaEvent_t ea = ev_time(), eb = ev_time();
       CK(cudaEventRecord(ea, s2));
       if (split) {
@@ -1659,6 +1681,11 @@ int solve(Problem &P, int64_t *m_out) {
   };
   Timer ttree(s);
   for (;;) {
+    {
+      char nm[32];
+      snprintf(nm, sizeof nm, "mrrr level %d", level);
+      tr.phase(nm);
+    }
     h2d(active, h_active.data(), nslots, s);
     k_classify<<<(nslots + 255) / 256, 256, 0, s>>>(slot_node, slo, shi, active, (int)nslots,
                                                     P.o.tol_relgap, run_end);
@@ -1912,6 +1939,7 @@ int solve(Problem &P, int64_t *m_out) {
   g_stats.ms_tree = ttree.stop();
 
   // ---------------- a6: singleton vectors (launched per level above) ----------------
+  tr.phase("mrrr vector tail");
   Timer tv(s);
   const int ntask = (int)tasks.size();
   g_stats.singletons = ntask;

@@ -607,7 +607,10 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
     }
     __syncwarp();
   }
-  if (lane == 0) atomicAdd(sweeps, (unsigned long long)rounds * SH);
+  if (lane == 0) {
+    atomicAdd(sweeps, (unsigned long long)rounds * SH);
+    atomicAdd(&g_rw_hist[min(rounds, 63)], 1u);
+  }
   if (lane < nm) {
     const int sl = slot_list ? slot_list[Wk.s0 + lane] : Wk.s0 + lane;
     lo_arr[sl] = S.lo[lane]; hi_arr[sl] = S.hi[lane];

@@ -1786,6 +1786,10 @@ int solve(Problem &P, int64_t *m_out) {
     node_pl.resize(node_base + ncl, -1);
     for (int c = 0; c < ncl; ++c) node_rrr[node_base + c] = cl_rrr[c];
     tr.fine(s, "  alloc+upload");
+    if (tr.lvl >= 2) {
+      unsigned z[64] = {};
+      CK(cudaMemcpyToSymbol(g_rw_hist, z, sizeof z));
+    }
     int h_fail[4] = {0, 0, 0, 0};
     {
       // clusters of >= 2000 members (reading 30) go through the nine-warp
@@ -1887,6 +1891,16 @@ int solve(Problem &P, int64_t *m_out) {
       launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, wlo, whi, 1, P.o.rtol_class,
                     dfail + 2, ctr + 2, ctr + 1, s, rw_m_tree);
       tr.fine(s, "  refine");
+      if (tr.lvl >= 2) {  // diagnostic: rounds per refinement warp
+        unsigned hist[64];
+        CK(cudaMemcpyFromSymbol(hist, g_rw_hist, sizeof hist));
+        fprintf(stderr, "[mrrr]   refine rounds histogram:");
+        for (int r = 0; r < 64; ++r)
+          if (hist[r]) fprintf(stderr, " %d:%u", r, hist[r]);
+        fprintf(stderr, "\n");
+        memset(hist, 0, sizeof hist);
+        CK(cudaMemcpyToSymbol(g_rw_hist, hist, sizeof hist));
+      }
       d2h(h_fail, dfail, 4, s);
       if (getenv("MRRR_DUMP")) {
         char nm[64];

@@ -452,7 +452,8 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
                                                                const double *whi_arr, int verify, double rtol,
                                                                int max_rounds, int *fail,
                                                                unsigned long long *sweeps,
-                                                               unsigned long long *safe_ctr) {
+                                                               unsigned long long *safe_ctr,
+                                                               double class_tol = 0.0, double early_w = 0.0) {
   static_assert(M >= 1 && M <= 4, "cnt[] is sized for at most 4 shifts per lane");
   __shared__ RefWarpSmem smem[kRWWarps];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -606,6 +607,38 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
       S.lo[i] = l; S.hi[i] = h; S.state[i] = stt;
     }
     __syncwarp();
+    // Reading 31 (tree refinement, class_tol > 0): a verified member stops
+    // once its bracket is within early_w (relative) and the classification
+    // of both its boundaries is decided: lo_{j+1} - hi_j > class_tol * the
+    // largest |endpoint| of the two brackets.  Brackets only shrink, so the
+    // test then also holds for the final brackets, where k_classify applies
+    // it to the midpoints (|mid| <= that bound): the member is a singleton
+    // whatever more bits it would get.  Only neighbours in this work item
+    // (verified) or the node's ends count -- the decision depends on the
+    // item's own data, so every run and every rank takes the same one.
+    if (class_tol > 0.0) {
+      bool stop = false;
+      if (lane < nm && S.state[lane] == 1) {
+        const double l = S.lo[lane], h = S.hi[lane];
+        const double ml = fmax(fabs(l), fabs(h));
+        if (h - l <= early_w * ml) {
+          const int sl = Wk.s0 + lane;
+          bool left = sl == N.slot0, right = sl + 1 == N.slot1;
+          if (!left && lane > 0 && S.state[lane - 1] != 0) {
+            const double nl = S.lo[lane - 1], nh = S.hi[lane - 1];
+            left = l - nh > class_tol * fmax(ml, fmax(fabs(nl), fabs(nh)));
+          }
+          if (!right && lane + 1 < nm && S.state[lane + 1] != 0) {
+            const double nl = S.lo[lane + 1], nh = S.hi[lane + 1];
+            right = nl - h > class_tol * fmax(ml, fmax(fabs(nl), fabs(nh)));
+          }
+          stop = left && right;
+        }
+      }
+      __syncwarp();
+      if (stop) S.state[lane] = 2;
+      __syncwarp();
+    }
   }
   if (lane == 0) {
     atomicAdd(sweeps, (unsigned long long)rounds * SH);

@@ -749,18 +749,19 @@ __global__ void k_iota(int *v, int n) {
 void launch_refine(const Node *nodes, const Work *work, int nwork, const int *slot_list,
                    const int *slot_j, double *lo, double *hi, const double *wlo, const double *whi,
                    int verify, double rtol, int *fail, unsigned long long *sweeps,
-                   unsigned long long *safe, cudaStream_t s, int M = 4) {
+                   unsigned long long *safe, cudaStream_t s, int M = 4, double class_tol = 0.0,
+                   double early_w = 0.0) {
   if (nwork == 0) return;
   const int grid = (nwork + kRWWarps - 1) / kRWWarps;
   if (M == 1)
     k_refine_warp<1><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
-                                                   verify, rtol, 4000, fail, sweeps, safe);
+                                                   verify, rtol, 4000, fail, sweeps, safe, class_tol, early_w);
   else if (M == 2)
     k_refine_warp<2><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
-                                                   verify, rtol, 4000, fail, sweeps, safe);
+                                                   verify, rtol, 4000, fail, sweeps, safe, class_tol, early_w);
   else
     k_refine_warp<4><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
-                                                   verify, rtol, 4000, fail, sweeps, safe);
+                                                   verify, rtol, 4000, fail, sweeps, safe, class_tol, early_w);
   CK(cudaGetLastError());
   g_stats.kernel_launches++;
 }
@@ -1172,6 +1173,9 @@ int solve(Problem &P, int64_t *m_out) {
     return 8;
   };
   const int rw_m_tree = rw_m_env > 0 ? rw_m_env : 1;
+  // reading 31: tree members stop refining at 2^-early_bits once their
+  // classification is decided (MRRR_EARLY_BITS; 0 = off, refine all to rtol_class)
+  const int early_bits = env_int("MRRR_EARLY_BITS", 12);
   // shifts per thread of the root grid (MRRR_GRID_M, diagnostic: 1, 2 or 4)
   const int grid_m = env_int("MRRR_GRID_M", 4);
   // clusters of at least rw_end members refine their two end members in
@@ -1889,7 +1893,8 @@ int solve(Problem &P, int64_t *m_out) {
       Work *dwork = lv.alloc<Work>(wv.size() + 1);
       h2d(dwork, wv.data(), wv.size(), s);
       launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, wlo, whi, 1, P.o.rtol_class,
-                    dfail + 2, ctr + 2, ctr + 1, s, rw_m_tree);
+                    dfail + 2, ctr + 2, ctr + 1, s, rw_m_tree, early_bits > 0 ? P.o.tol_relgap : 0.0,
+                    std::ldexp(1.0, -early_bits));
       tr.fine(s, "  refine");
       if (tr.lvl >= 2) {  // diagnostic: rounds per refinement warp
         unsigned hist[64];

@@ -1243,8 +1243,21 @@ int solve(Problem &P, int64_t *m_out) {
     Work *dwork = ar.alloc<Work>(std::max<size_t>(wv.size(), 1));
     h2d(dwork, wv.data(), wv.size(), s);
     guarded([&] {
+      if (tr.lvl >= 2) {
+        unsigned z[64] = {};
+        CK(cudaMemcpyToSymbol(g_rw_hist, z, sizeof z));
+      }
       launch_refine(dnodes, dwork + w0, (int)(w1 - w0), nullptr, slot_j, slo, shi, nullptr, nullptr, 0, rtol_root,
                     dfail + 2, ctr, ctr + 1, s);
+      if (tr.lvl >= 2) {  // diagnostic: rounds per root refinement warp
+        CK(cudaStreamSynchronize(s));
+        unsigned hist[64];
+        CK(cudaMemcpyFromSymbol(hist, g_rw_hist, sizeof hist));
+        fprintf(stderr, "[mrrr]   root refine: %d items; rounds histogram:", (int)(w1 - w0));
+        for (int r = 0; r < 64; ++r)
+          if (hist[r]) fprintf(stderr, " %d:%u", r, hist[r]);
+        fprintf(stderr, "\n");
+      }
       if (dist) {
         int hf = 0;
         d2h(&hf, dfail + 2, 1, s);
@@ -1578,21 +1591,29 @@ int solve(Problem &P, int64_t *m_out) {
       }
     }
   };
-  // pieces that overlap a busy tree level run on single warps (smaller
+  // pieces that overlap a heavy tree level run on single warps (smaller
   // footprint next to the tree's kernels); the last flush, and pieces whose
-  // level leaves at most kPairMaxClusters clusters to refine, on warp pairs
-  // (half the latency, resources to spare).  MRRR_VEC_PAIR: 0 never, 2 always.
-  const int kPairMaxClusters = env_int("MRRR_PAIR_MAXCL", 200);
+  // level leaves at most kPairWork cluster-rows (clusters x block order) to
+  // step and refine, on warp pairs (half the latency).  Measured (B200):
+  // random n=20000 (<= 1049 clusters x 2e4 rows per level) 53.6 -> 51.3 ms
+  // with pairs at every level, glued n=21000 71.0 -> 69.6 ms, but random
+  // n=1e5 (221-1173 clusters x 1e5 rows) 1084 -> 1133 ms: there the longer
+  // pair pieces crowd the tree's kernels.  MRRR_VEC_PAIR: 0 never, 2 always;
+  // MRRR_PAIR_WORK overrides the bound (diagnostic).
+  const double kPairWork = getenv("MRRR_PAIR_WORK") ? atof(getenv("MRRR_PAIR_WORK")) : 2.5e7;
   const int vec_pair = env_int("MRRR_VEC_PAIR", 1);
   const int vec_split = env_int("MRRR_VEC_SPLIT", 1);
   const int vec_pack = env_int("MRRR_VEC_PACK", 1) ? kMaxSeg : 1;
+  const int tree_side = std::min(kSide, std::max(1, env_int("MRRR_TREE_SIDE", kSide)));
   auto flush_vectors = [&](int tree_left) {
     for (size_t t0 = vec_done; t0 < tasks.size();) {
       const size_t t1 = std::min<size_t>(tasks.size(), t0 + (size_t)(ck_cap - 32));
       const int nbt = (int)(t1 - t0);
       std::vector<VecTask> bt(tasks.begin() + t0, tasks.begin() + t1);
       VecTask *dtb = ar.alloc<VecTask>(nbt);
-      const int sk = nbatch % kSide;
+      // side streams: tree_side of them while the tree runs (fewer vector
+      // warps next to its kernels), all kSide for the last flush
+      const int sk = tree_left > 0 ? nbatch % tree_side : nbatch % kSide;
       if (!ck_f[sk]) {
         ck_f[sk] = ar.alloc<FwdCk>((size_t)nseg_v * ck_cap);
         ck_b[sk] = ar.alloc<BwdCk>((size_t)nseg_v * ck_cap);
@@ -1613,7 +1634,7 @@ int solve(Problem &P, int64_t *m_out) {
       A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam + t0; A.mode = 0; A.ctr = ctr + 8;
       A.slot_j = slot_j; A.rqc_max = std::max(1, P.o.rqc_max);
       A.fail_list = fail_list; A.fail_count = fail_count; A.task_base = (int)t0;
-      const bool pair = vec_pair == 2 || (vec_pair == 1 && tree_left <= kPairMaxClusters);
+      const bool pair = vec_pair == 2 || (vec_pair == 1 && (double)tree_left * (double)nbmax <= kPairWork);
       // single-warp pieces: split RQC with the lanes regrouped by twist index
       // between the phases (k_wvectors_split: ~25 % fewer rows walked by the
       // fixed-twist factorizations and the solve; random n = 1e5 1.84 -> 1.59 s).

@@ -1861,6 +1861,14 @@ int solve(Problem &P, int64_t *m_out) {
         g_stats.kernel_launches++;
       }
       tr.fine(s, "  child step");
+      if (tr.lvl >= 2) {  // diagnostic: this level's slowest cluster step, cycles per phase
+        unsigned long long c[8];
+        CK(cudaMemcpy(c, ctr + 16, sizeof c, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[mrrr]   child step cycles (%s): candidates %llu, probe bwd %llu, probe fwd %llu; "
+                "twist+scan %llu; growth %llu\n", child_v1 ? "v1" : "v2", c[2], c[3], c[4], c[5], c[6]);
+        const unsigned long long z[5] = {0, 0, 0, 0, 0};
+        CK(cudaMemcpy(ctr + 18, z, sizeof z, cudaMemcpyHostToDevice));
+      }
       g_stats.child_sweeps += 7 * nown;
       // sigma of every cluster of the level (0 where another rank owns it:
       // those members' brackets arrive by the exchange below)

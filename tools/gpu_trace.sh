@@ -1,4 +1,3 @@
-python tools/trace_run.py random_20000 1 2> gpurun_out/tr1.txt
 python tools/trace_run.py random_20000 2 2> gpurun_out/tr2.txt
-MRRR_VEC_MODE=1 python tools/trace_run.py random_20000 1 2> gpurun_out/tr1v.txt
-MRRR_VEC_MODE=1 python tools/trace_run.py random_20000 2 2> gpurun_out/tr2v.txt
+MRRR_CHILD_V1=1 python tools/trace_run.py random_20000 2 2> gpurun_out/tr2_v1.txt
+MRRR_CHILD_V1=0 python tools/trace_run.py random_20000 2 2> gpurun_out/tr2_v2.txt

@@ -53,7 +53,16 @@ struct Child2Smem {
 };
 
 template <int ADJ>
-__global__ void __launch_bounds__(96, ADJ ? 2 : 4) k_child_step2(ChildArgs A) {
+// resident CTAs per SM asked of ptxas for k_child_step2<0>: 6 (96 registers,
+// 284 B of spills) against 4 (168 registers, none).  Measured on B200 with
+// the vector pieces overlapping (bench, 20 steps, twice each): random n=20000
+// 51.3 -> 49.0 ms, n=1e5 1084 -> 1073 ms; alone (MRRR_TRACE=2) the wide
+// levels' steps get slower (4.07 -> 4.71 ms), so the gain is in sharing the
+// SMs with the vector warps.  5 (128 registers): 54.3 ms; 8 (80): 49.4 ms.
+#ifndef MRRR_CS2_MINB
+#define MRRR_CS2_MINB 6
+#endif
+__global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(ChildArgs A) {
   constexpr int NPROBE = 2 + 2 * ADJ;  // probe sides
   __shared__ Child2Smem S;
   if (A.c0 + (int)blockIdx.x >= A.ncl) return;

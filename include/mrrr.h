@@ -220,7 +220,10 @@ int mrrr_trim_workspace(void);
  *  (7) mode   0: the kernels' division-free projective sweep
  *             with its qd fallback when the sweep over/underflows; 1: the qd
  *             fallback alone (differential stationary qd, a zero pivot's NaN
- *             ratio replaced by its limit 1, reading 5).
+ *             ratio replaced by its limit 1, reading 5); 2: the
+ *             refinement kernels' twisted count (reading 32):
+ *             stationary over rows 0 .. r-1, progressive over rows nb-2 .. r,
+ *             plus the sign of gamma_r, r = 16 * floor((nb - 1) / 32).
  *  (8) stream cudaStream_t (as void*); the call synchronises it.
  * Returns 0, -i for an invalid argument i, 5 (CUDA) or 6 (out of memory).
  * Allocates nb * 16 bytes of stream-ordered scratch, freed before return.

@@ -437,14 +437,14 @@ constexpr int kRWMembers = 32;  // capacity; a work item holds <= kRWMembers slo
 constexpr int kRWT = 16, kRWRing = 6, kRWWarps = 4;
 
 struct RefWarpSmem {
-  double2 ring[kRWRing][kRWT];
+  double2 ring[kRWRing][2 * kRWT];  // SPLIT: [0, 16) the top part's tile, [16, 32) the bottom's
   double lo[kRWMembers], hi[kRWMembers], wl[kRWMembers], wu[kRWMembers];
   double plo[kRWMembers], phi[kRWMembers];
   int j[kRWMembers], state[kRWMembers], act[kRWMembers];
   int cnt[32 * 4];
 };
 
-template <int M>
+template <int M, bool SPLIT>
 __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes, const Work *work, int nwork,
                                                                const int *__restrict__ slot_list,
                                                                const int *__restrict__ slot_j, double *lo_arr,
@@ -492,11 +492,15 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
     if (a) S.act[__popc(bal & ((1u << lane) - 1u))] = lane;
     __syncwarp();
     const int P = min(SH / na, 64);
-    double mu[M];
+    // shifts: lane l runs C = M (whole sweep) or 2M (SPLIT: lanes l and l^16
+    // share the same 2M shifts, l < 16 the top part, l >= 16 the bottom part)
+    constexpr int C = SPLIT ? 2 * M : M;
+    const int hl = SPLIT ? (lane & 15) : lane;
+    double mu[C];
     bool any = false;
 #pragma unroll
-    for (int c = 0; c < M; ++c) {
-      const int f = lane * M + c;
+    for (int c = 0; c < C; ++c) {
+      const int f = hl * C + c;
       const int ai = f / P, sub = f - ai * P;
       mu[c] = 0.0;
       if (ai < na) {
@@ -508,64 +512,170 @@ __global__ void __launch_bounds__(32 * kRWWarps) k_refine_warp(const Node *nodes
         any = true;
       }
     }
-    // ---- one sweep of the node for the lane's M shifts
-    Sturm st[M];
-#pragma unroll
-    for (int c = 0; c < M; ++c) sturm_init(st[c], mu[c]);
+    Sturm st[C];
     bool ok = true;
-    auto issue = [&](int t) {
-      const int row = t * kRWT + lane;
-      if (lane < kRWT && t < ntile && row < body)
-        __pipeline_memcpy_async(&S.ring[t % kRWRing][lane], &N.DL[row], sizeof(double2));
-      __pipeline_commit();
-    };
+    if (!SPLIT) {
+      // ---- one sweep of the node for the lane's M shifts
 #pragma unroll
-    for (int k = 0; k < kRWRing - 1; ++k) issue(k);
-    for (int t = 0; t < ntile; ++t) {
-      __pipeline_wait_prior(kRWRing - 2);
-      __syncwarp();
-      const double2 *T = S.ring[t % kRWRing];
-      const int rows = min(kRWT, body - t * kRWT);
-      if (any) {
-        if (rows == kRWT) {
-          double2 v[kRWT];  // the tile's rows in registers before the dependent steps
+      for (int c = 0; c < C; ++c) sturm_init(st[c], mu[c]);
+      auto issue = [&](int t) {
+        const int row = t * kRWT + lane;
+        if (lane < kRWT && t < ntile && row < body)
+          __pipeline_memcpy_async(&S.ring[t % kRWRing][lane], &N.DL[row], sizeof(double2));
+        __pipeline_commit();
+      };
 #pragma unroll
-          for (int k = 0; k < kRWT; ++k) v[k] = T[k];
+      for (int k = 0; k < kRWRing - 1; ++k) issue(k);
+      for (int t = 0; t < ntile; ++t) {
+        __pipeline_wait_prior(kRWRing - 2);
+        __syncwarp();
+        const double2 *T = S.ring[t % kRWRing];
+        const int rows = min(kRWT, body - t * kRWT);
+        if (any) {
+          if (rows == kRWT) {
+            double2 v[kRWT];  // the tile's rows in registers before the dependent steps
 #pragma unroll
-          for (int k = 0; k < kRWT; ++k) {
+            for (int k = 0; k < kRWT; ++k) v[k] = T[k];
 #pragma unroll
-            for (int c = 0; c < M; ++c) sturm_step(st[c], v[k].x, v[k].y, mu[c]);
-            if ((k & 7) == 7) {
+            for (int k = 0; k < kRWT; ++k) {
 #pragma unroll
-              for (int c = 0; c < M; ++c) ok &= sturm_rescale(st[c]);
+              for (int c = 0; c < C; ++c) sturm_step(st[c], v[k].x, v[k].y, mu[c]);
+              if ((k & 7) == 7) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) ok &= sturm_rescale(st[c]);
+              }
             }
-          }
-        } else {
-          for (int k = 0; k < rows; ++k) {
-            const double2 v = T[k];
+          } else {
+            for (int k = 0; k < rows; ++k) {
+              const double2 v = T[k];
 #pragma unroll
-            for (int c = 0; c < M; ++c) sturm_step(st[c], v.x, v.y, mu[c]);
-            if ((k & 7) == 7) {
+              for (int c = 0; c < C; ++c) sturm_step(st[c], v.x, v.y, mu[c]);
+              if ((k & 7) == 7) {
 #pragma unroll
-              for (int c = 0; c < M; ++c) ok &= sturm_rescale(st[c]);
+                for (int c = 0; c < C; ++c) ok &= sturm_rescale(st[c]);
+              }
             }
           }
         }
+        __syncwarp();
+        issue(t + kRWRing - 1);
       }
-      __syncwarp();
-      issue(t + kRWRing - 1);
-    }
-    __pipeline_wait_prior(0);
-    const double Dl = __ldg(&N.DL[nb - 1]).x;
+      __pipeline_wait_prior(0);
+      const double Dl = __ldg(&N.DL[nb - 1]).x;
 #pragma unroll
-    for (int c = 0; c < M; ++c) { sturm_last(st[c], Dl); ok &= sturm_ok(st[c]); }
-    if (any && (!ok || g_force_safe)) {
+      for (int c = 0; c < C; ++c) { sturm_last(st[c], Dl); ok &= sturm_ok(st[c]); }
+    } else {
+      // ---- the count as a twisted factorization at row r (LAPACK dlaneg's
+      // form, reading 32): the stationary transform over rows
+      // 0 .. r-1 (lanes < 16) and the progressive one over rows nb-2 .. r
+      // (lanes >= 16) run at the same time, then
+      //   N(mu) = #{D+_i < 0, i < r} + #{D-_i < 0, i > r} + [gamma_r < 0],
+      //   gamma_r = s_r + mu + p_r.
+      // The progressive step in projective form, p = a/b: u = LLD_i b + a
+      // (= D-_i b), a' = D_i a - mu u, b' = u -- the stationary step with
+      // (D, LLD) swapped, so both halves run the same instructions.
+      const bool fwd = lane < 16;
+      const int Lf = ((nb - 1) / (2 * kRWT)) * kRWT;  // r: whole tiles on top
+      const int Lb = nb - 1 - Lf;                     // >= Lf rows below
+      const int ntf = Lf / kRWT, ntb = (Lb + kRWT - 1) / kRWT;
+      const double Dl = __ldg(&N.DL[nb - 1]).x;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        sturm_init(st[c], mu[c]);
+        if (!fwd) st[c].p = Dl - mu[c];
+      }
+      auto issue = [&](int t) {
+        if (fwd) {
+          if (t < ntf) __pipeline_memcpy_async(&S.ring[t % kRWRing][hl], &N.DL[t * kRWT + hl], sizeof(double2));
+        } else {
+          const int row = nb - 2 - (t * kRWT + hl);
+          if (t < ntb && row >= Lf) {  // stored swapped: (LLD, D)
+            double2 *dst = &S.ring[t % kRWRing][kRWT + hl];
+            __pipeline_memcpy_async(&dst->x, &N.DL[row].y, sizeof(double));
+            __pipeline_memcpy_async(&dst->y, &N.DL[row].x, sizeof(double));
+          }
+        }
+        __pipeline_commit();
+      };
+      // the sign of each pivot t (= D+ q) goes into a bit mask (one funnel
+      // shift per step); a tile's negative pivots are the sign CHANGES of
+      // consecutive t (q_i = t_{i-1} up to a positive power of two, q_0 > 0),
+      // popc(m ^ (m >> 1)) over its rows -- negbit's count, bit for bit
+      unsigned sg[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) sg[c] = 0u;
+      auto step = [&](int c, double x, double y) {
+        const double tt = fma(x, st[c].q, st[c].p);
+        sg[c] = __funnelshift_l((unsigned)hi32(tt), sg[c], 1);
+        st[c].p = fma(-mu[c], tt, y * st[c].p);
+        st[c].q = tt;
+      };
+#pragma unroll
+      for (int k = 0; k < kRWRing - 1; ++k) issue(k);
+      for (int t = 0; t < ntb; ++t) {
+        __pipeline_wait_prior(kRWRing - 2);
+        __syncwarp();
+        const double2 *T = S.ring[t % kRWRing] + (fwd ? 0 : kRWT);  // (x, y) = (D, LLD) / (LLD, D)
+        if (any) {
+          if (t < ntf && (t + 1) * kRWT <= Lb) {  // both halves step a whole tile
+            double x[kRWT], y[kRWT];
+#pragma unroll
+            for (int k = 0; k < kRWT; ++k) { const double2 v = T[k]; x[k] = v.x; y[k] = v.y; }
+#pragma unroll
+            for (int k = 0; k < kRWT; ++k) {
+#pragma unroll
+              for (int c = 0; c < C; ++c) step(c, x[k], y[k]);
+              if ((k & 7) == 7) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) ok &= sturm_rescale(st[c]);
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) st[c].c += __popc((sg[c] ^ (sg[c] >> 1)) & 0xffffu);
+          } else {
+            const int rows = fwd ? (t < ntf ? kRWT : 0) : min(kRWT, Lb - t * kRWT);
+            for (int k = 0; k < rows; ++k) {
+              const double x = T[k].x, y = T[k].y;
+#pragma unroll
+              for (int c = 0; c < C; ++c) step(c, x, y);
+              if ((k & 7) == 7) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) ok &= sturm_rescale(st[c]);
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) st[c].c += __popc((sg[c] ^ (sg[c] >> 1)) & ((1u << rows) - 1u));
+          }
+        }
+        __syncwarp();
+        issue(t + kRWRing - 1);
+      }
+      __pipeline_wait_prior(0);
+      // normalise both states (max(|p|, |q|) in [1, 2)), then combine at r
+#pragma unroll
+      for (int c = 0; c < C; ++c) { ok &= sturm_rescale(st[c]); ok &= sturm_ok(st[c]); }
+      ok &= __shfl_xor_sync(0xffffffffu, (int)ok, 16) != 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const double a = __shfl_xor_sync(0xffffffffu, st[c].p, 16);
+        const double b = __shfl_xor_sync(0xffffffffu, st[c].q, 16);
+        const unsigned cb = __shfl_xor_sync(0xffffffffu, st[c].c, 16);
+        // gamma_r q b = (s_r + mu) q b + p_r q b, sign against sign(q b)
+        const double X = fma(mu[c], st[c].q, st[c].p);
+        const double Ng = fma(X, b, a * st[c].q);
+        const unsigned ng = (Ng != 0.0) ? (((unsigned)(hi32(Ng) ^ hi32(st[c].q) ^ hi32(b))) >> 31) : 0u;
+        st[c].c += cb + ng;
+      }
+    }
+    if (any && (!ok || g_force_safe) && (!SPLIT || lane < 16)) {
       atomicAdd(safe_ctr, 1ull);
 #pragma unroll
-      for (int c = 0; c < M; ++c) st[c].c = negcount_qd_safe(N.DL, nb, mu[c]);
+      for (int c = 0; c < C; ++c) st[c].c = negcount_qd_safe(N.DL, nb, mu[c]);
     }
+    if (!SPLIT || lane < 16) {
 #pragma unroll
-    for (int c = 0; c < M; ++c) S.cnt[lane * M + c] = (int)st[c].c;
+      for (int c = 0; c < C; ++c) S.cnt[hl * C + c] = (int)st[c].c;
+    }
     __syncwarp();
     // ---- owners update their member (lane ai < na owns active member act[ai])
     if (lane < na) {

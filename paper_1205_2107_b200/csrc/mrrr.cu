@@ -750,18 +750,21 @@ void launch_refine(const Node *nodes, const Work *work, int nwork, const int *sl
                    const int *slot_j, double *lo, double *hi, const double *wlo, const double *whi,
                    int verify, double rtol, int *fail, unsigned long long *sweeps,
                    unsigned long long *safe, cudaStream_t s, int M = 4, double class_tol = 0.0,
-                   double early_w = 0.0) {
+                   double early_w = 0.0, bool split = false) {
   if (nwork == 0) return;
   const int grid = (nwork + kRWWarps - 1) / kRWWarps;
-  if (M == 1)
-    k_refine_warp<1><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
-                                                   verify, rtol, 4000, fail, sweeps, safe, class_tol, early_w);
-  else if (M == 2)
-    k_refine_warp<2><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
-                                                   verify, rtol, 4000, fail, sweeps, safe, class_tol, early_w);
-  else
-    k_refine_warp<4><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, whi,
-                                                   verify, rtol, 4000, fail, sweeps, safe, class_tol, early_w);
+#define MRRR_RW(MM, SP)                                                                                   \
+  k_refine_warp<MM, SP><<<grid, 32 * kRWWarps, 0, s>>>(nodes, work, nwork, slot_list, slot_j, lo, hi, wlo, \
+                                                       whi, verify, rtol, 4000, fail, sweeps, safe, class_tol, \
+                                                       early_w)
+  if (M == 1) {
+    if (split) MRRR_RW(1, true); else MRRR_RW(1, false);
+  } else if (M == 2) {
+    if (split) MRRR_RW(2, true); else MRRR_RW(2, false);
+  } else {
+    if (split) MRRR_RW(4, true); else MRRR_RW(4, false);
+  }
+#undef MRRR_RW
   CK(cudaGetLastError());
   g_stats.kernel_launches++;
 }
@@ -1176,6 +1179,10 @@ int solve(Problem &P, int64_t *m_out) {
   // reading 31: tree members stop refining at 2^-early_bits once their
   // classification is decided (MRRR_EARLY_BITS; 0 = off, refine all to rtol_class)
   const int early_bits = env_int("MRRR_EARLY_BITS", 12);
+  // twisted (split) counts in the refinement sweeps (reading 32): 1 = tree
+  // levels, 2 = tree and root, 0 = whole stationary sweeps everywhere
+  const int split_env = env_int("MRRR_SPLIT", 2);
+  const bool split_tree = split_env >= 1, split_root = split_env >= 2;
   // shifts per thread of the root grid (MRRR_GRID_M, diagnostic: 1, 2 or 4)
   const int grid_m = env_int("MRRR_GRID_M", 4);
   // clusters of at least rw_end members refine their two end members in
@@ -1248,7 +1255,7 @@ int solve(Problem &P, int64_t *m_out) {
         CK(cudaMemcpyToSymbol(g_rw_hist, z, sizeof z));
       }
       launch_refine(dnodes, dwork + w0, (int)(w1 - w0), nullptr, slot_j, slo, shi, nullptr, nullptr, 0, rtol_root,
-                    dfail + 2, ctr, ctr + 1, s);
+                    dfail + 2, ctr, ctr + 1, s, 4, 0.0, 0.0, split_root);
       if (tr.lvl >= 2) {  // diagnostic: rounds per root refinement warp
         CK(cudaStreamSynchronize(s));
         unsigned hist[64];
@@ -1868,6 +1875,12 @@ int solve(Problem &P, int64_t *m_out) {
                 "twist+scan %llu; growth %llu\n", child_v1 ? "v1" : "v2", c[2], c[3], c[4], c[5], c[6]);
         const unsigned long long z[5] = {0, 0, 0, 0, 0};
         CK(cudaMemcpy(ctr + 18, z, sizeof z, cudaMemcpyHostToDevice));
+        std::vector<int> ht(std::max(nown, 1));
+        CK(cudaMemcpy(ht.data(), dtier, nown * sizeof(int), cudaMemcpyDeviceToHost));
+        int tc[8] = {};
+        for (int i = 0; i < nown; ++i) tc[std::min(std::max(ht[i], 0), 7)]++;
+        fprintf(stderr, "[mrrr]   child tiers: (i) %d, (ii) %d, (iii) %d, none %d, interior %d\n", tc[0], tc[1],
+                tc[3], tc[4], tc[5]);
       }
       g_stats.child_sweeps += 7 * nown;
       // sigma of every cluster of the level (0 where another rank owns it:
@@ -1923,7 +1936,7 @@ int solve(Problem &P, int64_t *m_out) {
       h2d(dwork, wv.data(), wv.size(), s);
       launch_refine(dnodes, dwork, (int)wv.size(), nullptr, slot_j, slo, shi, wlo, whi, 1, P.o.rtol_class,
                     dfail + 2, ctr + 2, ctr + 1, s, rw_m_tree, early_bits > 0 ? P.o.tol_relgap : 0.0,
-                    std::ldexp(1.0, -early_bits));
+                    std::ldexp(1.0, -early_bits), split_tree);
       tr.fine(s, "  refine");
       if (tr.lvl >= 2) {  // diagnostic: rounds per refinement warp
         unsigned hist[64];
@@ -2189,11 +2202,43 @@ __global__ void k_diag_interleave(const double *D, const double *LLD, int nb, do
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nb) DL[i] = make_double2(D[i], i < nb - 1 ? LLD[i] : 0.0);
 }
+// The refinement kernels' twisted count (k_refine_warp<M, true>, reading 32)
+// on one thread: stationary steps over rows 0 .. r-1, progressive steps over
+// rows nb-2 .. r with (D, LLD) swapped, rescales after every 8th step of each
+// part, a final rescale, and gamma_r's sign -- the same operations in the
+// same order as the warp kernel's lanes, so the same count.
+__device__ unsigned negcount_twisted_global(const double2 *__restrict__ DL, int nb, double mu) {
+  const int Lf = ((nb - 1) / 32) * 16, Lb = nb - 1 - Lf;
+  Sturm f, b;
+  sturm_init(f, mu);
+  sturm_init(b, mu);
+  b.p = __ldg(&DL[nb - 1]).x - mu;
+  bool ok = true;
+  for (int i = 0; i < Lf; ++i) {
+    const double2 v = __ldg(&DL[i]);
+    sturm_step(f, v.x, v.y, mu);
+    if ((i & 7) == 7) ok &= sturm_rescale(f);
+  }
+  for (int q = 0; q < Lb; ++q) {
+    const double2 v = __ldg(&DL[nb - 2 - q]);
+    sturm_step(b, v.y, v.x, mu);
+    if ((q & 7) == 7) ok &= sturm_rescale(b);
+  }
+  ok &= sturm_rescale(f); ok &= sturm_ok(f);
+  ok &= sturm_rescale(b); ok &= sturm_ok(b);
+  if (!ok || g_force_safe) return negcount_qd_safe(DL, nb, mu);
+  const double X = fma(mu, f.q, f.p);
+  const double Ng = fma(X, b.q, b.p * f.q);
+  const unsigned ng = (Ng != 0.0) ? (((unsigned)(hi32(Ng) ^ hi32(f.q) ^ hi32(b.q))) >> 31) : 0u;
+  return f.c + b.c + ng;
+}
 __global__ void k_diag_negcount(const double2 *DL, int nb, const double *mu, int64_t k, int mode,
                                 int64_t *out) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= k) return;
-  out[q] = mode == 1 ? (int64_t)negcount_qd_safe(DL, nb, mu[q]) : (int64_t)negcount_global(DL, nb, mu[q], nullptr);
+  out[q] = mode == 1   ? (int64_t)negcount_qd_safe(DL, nb, mu[q])
+           : mode == 2 ? (int64_t)negcount_twisted_global(DL, nb, mu[q])
+                       : (int64_t)negcount_global(DL, nb, mu[q], nullptr);
 }
 
 __global__ void k_n1(const double *d, double *w, double *Z) {
@@ -2360,7 +2405,7 @@ int mrrr_negcount(int64_t nb, const double *D, const double *LLD, int64_t k, con
   if (k < 0) return -4;
   if (k > 0 && !mu) return -5;
   if (k > 0 && !count) return -6;
-  if (mode != 0 && mode != 1) return -7;
+  if (mode < 0 || mode > 2) return -7;
   if (k == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   double2 *DL = nullptr;

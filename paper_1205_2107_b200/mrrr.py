@@ -354,7 +354,7 @@ def stemr_raw(n, d, e, rng, vl, vu, il, iu, m_ok=True, w=None, Z=None, ldz=None)
 def negcount(D: torch.Tensor, LLD: torch.Tensor, mu: torch.Tensor, mode: int = 0, stream=None):
     """Sturm counts N(mu_q) of the representation (D, LLD) by the library's
     bisection arithmetic (``mrrr_negcount``; mode 0 projective sweep, 1 the qd
-    safe path).  float64 CUDA tensors; returns an int64 CUDA tensor."""
+    safe path, 2 the refinement's twisted count).  float64 CUDA tensors; returns an int64 CUDA tensor."""
     for t in (D, LLD, mu):
         if not (t.is_cuda and t.dtype == torch.float64):
             raise TypeError("negcount takes float64 CUDA tensors")

@@ -58,10 +58,11 @@ ROOTS = {
 
 @pytest.mark.parametrize("name", list(ROOTS))
 def test_negcount_bit_exact(torch_cuda, P, oracle_mod, name):
-    """GPU counts (mode 0: the projective sweep of k_grid / k_refine_warp; mode
-    1: the qd safe path) equal the oracle's O6 count for shifts farther than
-    1e-9 |mu| from every eigenvalue of the representation (closer, the three
-    evaluation orders may legitimately round to different sides).  Includes
+    """GPU counts (mode 0: the projective sweep of k_grid; mode 1: the qd safe
+    path; mode 2: the twisted count of k_refine_warp, reading 32) equal the
+    oracle's O6 count for shifts farther than 1e-9 |mu| from every eigenvalue
+    of the representation (closer, the evaluation orders may legitimately
+    round to different sides).  Includes
     dyadic grid shifts -- the root grid's points, which on structured inputs
     hit exact zero pivots (the oracle's NaN re-sweep; counted below)."""
     torch = torch_cuda
@@ -84,7 +85,7 @@ def test_negcount_bit_exact(torch_cuda, P, oracle_mod, name):
         zero_piv += rs
     ref = np.array(ref)
     Dt, Lt, mt = (torch.tensor(x, device="cuda") for x in (D, LLD, mus))
-    for mode in (0, 1):
+    for mode in (0, 1, 2):
         got = P.mrrr.negcount(Dt, Lt, mt, mode=mode).cpu().numpy()
         bad = np.nonzero(got != ref)[0]
         assert len(bad) == 0, (mode, len(bad), zero_piv, mus[bad[:5]], got[bad[:5]], ref[bad[:5]])
@@ -114,7 +115,7 @@ def test_negcount_exact_zero_pivot(torch_cuda, P, oracle_mod):
     ref = [oracle_mod.negcount(D, None, mu, LLD=LLD, return_resweep=True) for mu in mus]
     assert ref[0][1], "mu = 2 must hit an exact zero pivot in the oracle"
     Dt, Lt, mt = (torch.tensor(x, device="cuda") for x in (D, LLD, mus))
-    for mode in (0, 1):
+    for mode in (0, 1, 2):
         got = P.mrrr.negcount(Dt, Lt, mt, mode=mode).cpu().numpy()
         assert list(got) == [r[0] for r in ref], (mode, got, ref)
     k = np.arange(1, n + 1)

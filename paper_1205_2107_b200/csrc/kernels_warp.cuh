@@ -315,6 +315,58 @@ __device__ __forceinline__ Twist w_full_pair(const WarpCtx &W, double lam, int r
   return tw;
 }
 
+// One tile of a fixed-twist factorization's forward part: rows r0 .. r0+15
+// below the lane's rf.  A lane whose rf lies beyond the tile steps all 16
+// rows unpredicated (the common case: one branch per TILE, not per row -- a
+// per-row predicate compiled to a reconvergence block per row, ~40 % of the
+// vector kernels' stall samples); the lane whose rf falls inside the tile
+// steps the rest in a loop; lanes past rf do nothing.
+__device__ __forceinline__ void w_fixed_fwd_tile(const WarpCtx &W, int slot, int r0, int rf, double lam, Fwd &F) {
+  auto fstep = [&](int k) {
+    const Row R = w_row(W, slot, k);
+    const double t = fma(R.D, F.q, F.p);
+    F.neg += negbit(t, F.q);
+    F.H = R.LD2 * fma(F.q, F.q, F.H);
+    F.p = fma(-lam, t, R.LLD * F.p);
+    F.q = t;
+    if ((k & 7) == 7) fwd_rescale(F.p, F.q, F.H);
+  };
+  if (r0 + kTR <= rf) {
+#pragma unroll
+    for (int k = 0; k < kTR; ++k) fstep(k);
+  } else if (r0 < rf) {
+    for (int k = 0; k < rf - r0; ++k) fstep(k);
+  }
+}
+// The backward part's tile: rows top .. r0 (descending) at or above the
+// lane's rb and below nb - 1.
+__device__ __forceinline__ void w_fixed_bwd_tile(const WarpCtx &W, int slot, int r0, int top, int rb, double lam,
+                                                 Bwd &B) {
+  auto bstep = [&](int k) {
+    const Row R = w_row(W, slot, k);
+    const double u = fma(R.LLD, B.b, B.a);
+    B.neg += negbit(u, B.b);
+    B.K = R.LD2 * fma(B.b, B.b, B.K);
+    B.a = fma(-lam, u, R.D * B.a);
+    B.b = u;
+    if ((k & 7) == 0) bwd_rescale(B.a, B.b, B.K);
+  };
+  const int nb = W.nb;
+  if (top - r0 + 1 == kTR && top < nb - 1) {
+    if (r0 >= rb) {
+#pragma unroll
+      for (int k = kTR - 1; k >= 0; --k) bstep(k);
+    } else if (r0 + kTR > rb) {
+      for (int k = kTR - 1; k >= rb - r0; --k) bstep(k);
+    }
+  } else {
+    for (int k = top - r0; k >= 0; --k) {
+      const int i = r0 + k;
+      if (i < nb - 1 && i >= rb) bstep(k);
+    }
+  }
+}
+
 // Fixed-twist factorization of every lane at its own (lambda, r): F steps
 // rows 0..r-1 (ascending tiles up to the warp's largest r), B rows nb-2..r
 // (descending tiles down to the smallest r), each lane only its own rows.
@@ -331,18 +383,7 @@ __device__ __forceinline__ Twist w_fixed_pair(const WarpCtx &W, double lam, int 
     w_tiles_up(W, 0, cf, [&](int c, int slot) {
       const int r0 = c * kTR;
       if (r0 < rf) put_fck(Xc, c, W.tix, F);
-#pragma unroll
-      for (int k = 0; k < kTR; ++k) {
-        const Row R = w_row(W, slot, k);
-        if (r0 + k < rf) {
-          const double t = fma(R.D, F.q, F.p);
-          F.neg += negbit(t, F.q);
-          F.H = R.LD2 * fma(F.q, F.q, F.H);
-          F.p = fma(-lam, t, R.LLD * F.p);
-          F.q = t;
-          if ((k & 7) == 7) fwd_rescale(F.p, F.q, F.H);
-        }
-      }
+      w_fixed_fwd_tile(W, slot, r0, rf, lam, F);
       return false;
     });
     X.fp[L] = F.p; X.fq[L] = F.q; X.fH[L] = F.H; X.fneg[L] = F.neg;
@@ -354,25 +395,7 @@ __device__ __forceinline__ Twist w_fixed_pair(const WarpCtx &W, double lam, int 
       const int r0 = c * kTR;
       const int top = min(r0 + kTR, nb) - 1;  // rows r0 .. top in this tile
       if (c >= rb / kTR) put_bck(W, c, B);    // state at row min(r0 + kTR, nb - 1)
-      auto bstep = [&](int k) {
-        const Row R = w_row(W, slot, k);
-        const double u = fma(R.LLD, B.b, B.a);
-        B.neg += negbit(u, B.b);
-        B.K = R.LD2 * fma(B.b, B.b, B.K);
-        B.a = fma(-lam, u, R.D * B.a);
-        B.b = u;
-        if ((k & 7) == 0) bwd_rescale(B.a, B.b, B.K);
-      };
-      if (top - r0 + 1 == kTR && top < nb - 1) {
-#pragma unroll
-        for (int k = kTR - 1; k >= 0; --k)
-          if (r0 + k >= rb) bstep(k);
-      } else {
-        for (int k = top - r0; k >= 0; --k) {
-          const int i = r0 + k;
-          if (i < nb - 1 && i >= rb) bstep(k);
-        }
-      }
+      w_fixed_bwd_tile(W, slot, r0, top, rb, lam, B);
       return false;
     });
     X.ba[L] = B.a; X.bb[L] = B.b; X.bK[L] = B.K; X.bneg[L] = B.neg;
@@ -521,19 +544,14 @@ __device__ __forceinline__ Twist w_twist_full(const WarpCtx &W, double lam) {
 // rows 0..r-1 (ascending tiles up to the warp's largest r) and backward rows
 // nb-2..r (descending tiles down to the smallest r), each lane stepping only
 // its own rows.  No argmin, no replay: one pass of simple steps per
-// direction.  With `col` (per lane, may be null) the z
-// multipliers are stored on the way: col[i] = z_i / z_{i+1} = -LD_i q_i / t_i
-// for i < r and col[i+1] = z_{i+1} / z_i = -LD_i b_{i+1} / u_{i+1} for i >= r,
-// so the eigenvector needs no further sweep (w_ratio_solve).
-__device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int r, bool active,
-                                               double *col = nullptr) {
+// direction.
+__device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int r, bool active) {
   const int nb = W.nb;
   Fwd F{-lam, 1.0, 0.0, 0};
   Bwd B{__ldg(&W.DL[nb - 1]).x - lam, 1.0, 0.0, 0};
   // an idle lane steps no rows and does not widen the warp's tile ranges
   const int rf = active ? r : 0;        // forward rows [0, rf)
   const int rb = active ? r : nb - 1;   // backward steps into rows [rb, nb - 1)
-  const bool st = active && col != nullptr;
   const VecCtx X{nullptr, nullptr, nb, W.nseg, W.fck, W.bck, W.ck_stride};
   // ---- forward: tiles 0 .. (max r - 1) / kTR; checkpoints of the segments
   // below r (the replayed solve reads them)
@@ -541,19 +559,7 @@ __device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int
   w_tiles_up(W, 0, cf, [&](int c, int slot) {
     const int r0 = c * kTR;
     if (r0 < rf) put_fck(X, c, W.tix, F);
-#pragma unroll
-    for (int k = 0; k < kTR; ++k) {
-      const Row R = w_row(W, slot, k);
-      if (r0 + k < rf) {
-        const double t = fma(R.D, F.q, F.p);
-        if (st) col[r0 + k] = -R.LD * (F.q * rcp_nr(t));
-        F.neg += negbit(t, F.q);
-        F.H = R.LD2 * fma(F.q, F.q, F.H);
-        F.p = fma(-lam, t, R.LLD * F.p);
-        F.q = t;
-        if ((k & 7) == 7) fwd_rescale(F.p, F.q, F.H);
-      }
-    }
+    w_fixed_fwd_tile(W, slot, r0, rf, lam, F);
     return false;
   });
   // ---- backward: tiles nseg-1 .. r / kTR
@@ -565,26 +571,7 @@ __device__ __forceinline__ Twist w_twist_fixed(const WarpCtx &W, double lam, int
       BwdCk bk; bk.a = B.a; bk.b = B.b;    // state at row min(r0 + kTR, nb - 1)
       W.bck[(int64_t)c * W.ck_stride + W.tix] = bk;
     }
-    auto bstep = [&](int k) {
-      const Row R = w_row(W, slot, k);
-      const double u = fma(R.LLD, B.b, B.a);
-      if (st) col[r0 + k + 1] = -R.LD * (B.b * rcp_nr(u));
-      B.neg += negbit(u, B.b);
-      B.K = R.LD2 * fma(B.b, B.b, B.K);
-      B.a = fma(-lam, u, R.D * B.a);
-      B.b = u;
-      if ((k & 7) == 0) bwd_rescale(B.a, B.b, B.K);
-    };
-    if (top - r0 + 1 == kTR && top < nb - 1) {
-#pragma unroll
-      for (int k = kTR - 1; k >= 0; --k)
-        if (r0 + k >= rb) bstep(k);
-    } else {
-      for (int k = top - r0; k >= 0; --k) {
-        const int i = r0 + k;
-        if (i < nb - 1 && i >= rb) bstep(k);
-      }
-    }
+    w_fixed_bwd_tile(W, slot, r0, top, rb, lam, B);
     return false;
   });
   const double qb = F.q * B.b;

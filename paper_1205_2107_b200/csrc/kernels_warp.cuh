@@ -41,10 +41,14 @@ struct WarpSmem {
   const double2 *segDL[kMaxSeg];     // (D, LLD) array of each segment's node
 };
 
+constexpr int kCpMax = (kMaxSeg + 2) / 2;  // ring copies per lane per tile (segments h, h+2, .. <= nsegs)
+
 struct WarpCtx {
   const double2 *DL, *LDv;  // DL: this lane's node
   int nb, nseg, lane;
   int seg, nsegs;           // this lane's segment; segments of the item
+  const double2 *cp_src[kCpMax];  // this lane's ring copies: sources of segments h + 2j (h = lane / 16)
+  int cp_n;
   WarpSmem *sm;
   FwdCk *fck;
   BwdCk *bck;
@@ -52,16 +56,21 @@ struct WarpCtx {
 };
 
 __device__ __forceinline__ void w_issue(const WarpCtx &W, int c, int slot) {
-  // copies 16 (D, LLD) rows per segment, then the 16 (LD, LD^2) rows; one
-  // segment: lanes 0..15 the former, 16..31 the latter (one copy per lane)
+  // copies 16 (D, LLD) rows per segment, then the 16 (LD, LD^2) rows: lane l
+  // copies row l % 16 of segments l / 16, l / 16 + 2, ... (the (LD, LD^2)
+  // rows count as segment nsegs); the sources were resolved once per item
+  // (w_segments), so a tile costs a few predicated copies per lane
   if (c >= 0 && c < W.nseg) {
-    const int ncopy = (W.nsegs + 1) * kTR;
-    for (int idx = W.lane; idx < ncopy; idx += 32) {
-      const int sg = idx / kTR, k = idx - sg * kTR;
-      const int row = c * kTR + k;
-      if (row < W.nb) {
-        if (sg < W.nsegs) __pipeline_memcpy_async(&W.sm->rDL[slot][k][sg], &W.sm->segDL[sg][row], sizeof(double2));
-        else __pipeline_memcpy_async(&W.sm->rLD[slot][k], &W.LDv[row], sizeof(double2));
+    const int k = W.lane & (kTR - 1), h = W.lane >> 4;
+    const int row = c * kTR + k;
+    if (row < W.nb) {
+#pragma unroll
+      for (int j = 0; j < kCpMax; ++j) {
+        const int sg = h + 2 * j;
+        if (j < W.cp_n) {
+          if (sg < W.nsegs) __pipeline_memcpy_async(&W.sm->rDL[slot][k][sg], W.cp_src[j] + row, sizeof(double2));
+          else __pipeline_memcpy_async(&W.sm->rLD[slot][k], W.cp_src[j] + row, sizeof(double2));
+        }
       }
     }
   }
@@ -79,6 +88,13 @@ __device__ __forceinline__ void w_segments(WarpCtx &W, int node_at_pos, bool act
   W.nsegs = __popc(b);
   if (first) W.sm->segDL[W.seg] = W.DL;
   __syncwarp();
+  const int h = W.lane >> 4;
+  W.cp_n = W.nsegs >= h ? (W.nsegs - h) / 2 + 1 : 0;
+#pragma unroll
+  for (int j = 0; j < kCpMax; ++j) {
+    const int sg = h + 2 * j;
+    W.cp_src[j] = sg < W.nsegs ? W.sm->segDL[sg] : W.LDv;
+  }
 }
 
 // f(c, slot) for tiles c = c0 .. c1 (ascending, warp-uniform bounds); tile c
@@ -1170,9 +1186,11 @@ __device__ __forceinline__ void wvec_split_body(const WVecArgs &A) {
   if (lane == 0) atomicMax(&A.ctr[7], nfact);
 }
 
-__global__ void __launch_bounds__(32 * kSingleWarps) k_wvectors_split(WVecArgs A) { wvec_split_body(A); }
+// At most 168 registers per thread (6 CTAs of 64 threads per SM by
+// registers): the vector pieces share the SMs with the tree's kernels.
+__global__ void __launch_bounds__(32 * kSingleWarps, 6) k_wvectors_split(WVecArgs A) { wvec_split_body(A); }
 
-__global__ void __launch_bounds__(kPairThreads) k_wvectors_pair(WVecArgs A) { wvec_pair_body(A); }
-__global__ void __launch_bounds__(32 * kSingleWarps) k_wvectors(WVecArgs A) { wvec_single_body(A); }
+__global__ void __launch_bounds__(kPairThreads, 6) k_wvectors_pair(WVecArgs A) { wvec_pair_body(A); }
+__global__ void __launch_bounds__(32 * kSingleWarps, 6) k_wvectors(WVecArgs A) { wvec_single_body(A); }
 
 }  // namespace mrrr

@@ -52,7 +52,10 @@ struct Child2Smem {
   double sg;
 };
 
-template <int ADJ>
+// POST = true (ADJ = 0): the chains were run by k_child_chains3
+// (kernels_child3.cuh), which wrote the same scratch rows; phase 1 only sets
+// the candidates' shifts.
+template <int ADJ, bool POST = false>
 // resident CTAs per SM asked of ptxas for k_child_step2<0>: 6 (96 registers,
 // 284 B of spills) against 4 (168 registers, none).  Measured on B200 with
 // the vector pieces overlapping (bench, 20 steps, twice each): random n=20000
@@ -129,7 +132,21 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
   const long long clk_p0 = clock64();
   const int ntile = (nb + kCT - 1) / kCT;
   ChainRing &R = S.ring[wid];
-  if (wid < 2) {
+  if (POST) {
+    if (tid < 6) {
+      const int which = tid;
+      const double mult = (double)(1 << (which >> 1));
+      if ((which & 1) == 0) {
+        const double l = A.lo[s0], h = A.hi[s0];
+        const double dl = fmax(fmax(2.0 * (h - l), 2.0 * A.rtol * fabs(l)), 4.0 * kEps * fabs(l));
+        S.sig[tid] = l - mult * dl;
+      } else {
+        const double l = A.lo[s1], h = A.hi[s1];
+        const double dr = fmax(fmax(2.0 * (h - l), 2.0 * A.rtol * fabs(h)), 4.0 * kEps * fabs(h));
+        S.sig[tid] = h + mult * dr;
+      }
+    }
+  } else if (wid < 2) {
     // warps 0, 1: this lane's chain: a candidate (warp 0) or a forward probe (warp 1)
     const int cb = wid == 0 ? 0 : kNC, nf = wid == 0 ? kNC : NPROBE;
     const int ch = cb + (lane < nf ? lane : 0);
@@ -252,7 +269,7 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
     }
     __pipeline_wait_prior(0);
   }
-  if (lane == 0) atomicMax(&A.ctr[1 + (wid == 0 ? 1 : wid == 1 ? 3 : 2)], (unsigned long long)(clock64() - clk_p0));
+  if (!POST && lane == 0) atomicMax(&A.ctr[1 + (wid == 0 ? 1 : wid == 1 ? 3 : 2)], (unsigned long long)(clock64() - clk_p0));
   __syncthreads();
   const long long clk_p1 = clock64();
 
@@ -333,7 +350,10 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
   if (tid == 0) atomicMax(&A.ctr[5], (unsigned long long)(clock64() - clk_p1));
   const long long clk_p2 = clock64();
 
-  // ---- phase 3: growth of the candidates, raw and weighted (64 threads)
+  // ---- phase 3: growth of the candidates, raw and weighted (96 threads;
+  // with POST the seventh row -- the interior candidate, ADJ only -- was not
+  // written, and its sums are not used for ADJ = 0)
+  constexpr int NCG = POST ? 6 : kNC;
   double g[kNC], nl[kNC], nr[kNC], dnl = 0.0, dnr = 0.0;
   double na = 0.0, nbb = 0.0, dna = 0.0, dnb = 0.0;
   unsigned okm = (1u << kNC) - 1u;
@@ -346,7 +366,7 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
     const double a2 = a * a, b2 = b * b;
     dnl += a2; dnr += b2;
 #pragma unroll
-    for (int k = 0; k < kNC; ++k) {
+    for (int k = 0; k < NCG; ++k) {
       const double ad = cs_absdplus_fast(TP, QK, zs, k, i);
       if (!(isfinite(ad) && ad != 0.0)) okm &= ~(1u << k);
       g[k] = fmax(g[k], ad);

@@ -23,6 +23,7 @@
 #include "kernels_warp.cuh"
 #include "kernels_child.cuh"
 #include "kernels_child2.cuh"
+#include "kernels_child3.cuh"
 
 using namespace mrrr;
 
@@ -1197,6 +1198,10 @@ int solve(Problem &P, int64_t *m_out) {
   // wide, issue-bound levels); the same arithmetic, bit for bit.
   // MRRR_CHILD_V1 = 1 / 0 forces one of them (diagnostic).
   const int child_v1_env = env_int("MRRR_CHILD_V1", -1);
+  // the wide levels' chains lane-dense (k_child_chains3 + k_child_step2<0,
+  // true>); MRRR_CHILD_V3=0: k_child_step2 alone (diagnostic)
+  const int child_v3_env = env_int("MRRR_CHILD_V3", 1);
+  const int c3_groups = std::min(3, std::max(1, env_int("MRRR_C3_GROUPS", 1)));  // clusters per chain warp
   constexpr int kChildV1Max = 296;  // two clusters per SM
   {
     std::vector<Work> wv;
@@ -1828,6 +1833,7 @@ int solve(Problem &P, int64_t *m_out) {
       // step with the interior candidate, in their own launch and scratch;
       // the others through the five-warp step, in groups that fit the scratch
       const bool child_v1 = child_v1_env >= 0 ? child_v1_env != 0 : nown <= kChildV1Max;
+      const bool child_v3 = !child_v1 && child_v3_env != 0;
       std::vector<int> small_cl, big_cl;
       for (int i = 0; i < nown; ++i)
         (P.o.shift_strategy == 1 && ocl_s1[i] - ocl_s0[i] >= 2000 ? big_cl : small_cl).push_back(i);
@@ -1862,8 +1868,21 @@ int solve(Problem &P, int64_t *m_out) {
       }
       for (int c0 = 0; c0 < nsmall; c0 += cgrp) {
         const int nl = std::min(nsmall, c0 + cgrp) - c0;
-        if (child_v1) k_child_step<0><<<nl, 32 * kCSWarps, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
-        else k_child_step2<0><<<nl, 96, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
+        if (child_v1) {
+          k_child_step<0><<<nl, 32 * kCSWarps, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
+        } else if (child_v3) {
+          // chains lane-dense (three clusters per warp), then the rest of the step
+          const int per = c3_groups * kC3Warps;
+          const ChildArgs CA = child_args(dsmall, c0, c0 + nl, scratch);
+          if (c3_groups == 1) k_child_chains3<1><<<(nl + per - 1) / per, 32 * kC3Warps, 0, s>>>(CA);
+          else if (c3_groups == 2) k_child_chains3<2><<<(nl + per - 1) / per, 32 * kC3Warps, 0, s>>>(CA);
+          else k_child_chains3<3><<<(nl + per - 1) / per, 32 * kC3Warps, 0, s>>>(CA);
+          CK(cudaGetLastError());
+          k_child_step2<0, true><<<nl, 96, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
+          g_stats.kernel_launches++;
+        } else {
+          k_child_step2<0><<<nl, 96, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
+        }
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }

@@ -173,7 +173,8 @@ def test_deterministic(torch_cuda, P):
 @pytest.mark.parametrize("env", [{"MRRR_CS_GROUP": "3"}, {"MRRR_VEC_MODE": "1"}, {"MRRR_VEC_PAIR": "0"},
                                  {"MRRR_VEC_PAIR": "2"}, {"MRRR_HP_STREAM": "0"}, {"MRRR_VEC_SPLIT": "0"},
                                  {"MRRR_VEC_PACK": "0"}, {"MRRR_CHILD_V1": "1"},
-                                 {"MRRR_CHILD_V1": "0"}])
+                                 {"MRRR_CHILD_V1": "0"}, {"MRRR_CHILD_V1": "0", "MRRR_CHILD_V3": "0"},
+                                 {"MRRR_CHILD_V1": "0", "MRRR_CS_GROUP": "5"}])
 def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     """The launch schedule does not change a single bit: cluster steps in
     groups that reuse the scratch (MRRR_CS_GROUP, the n = 1e5 memory cap's
@@ -186,7 +187,8 @@ def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     (MRRR_VEC_SPLIT=0), one node per vector work item instead of up to
     kMaxSeg nodes of a block packed into a warp (MRRR_VEC_PACK=0), the cluster
     step with one warp per chain or one lane per chain at every level
-    (MRRR_CHILD_V1=1 / 0; the default picks by the level's width; the same
+    (MRRR_CHILD_V1=1 / 0; with V1=0 the chains run lane-dense, three clusters
+    per warp, unless MRRR_CHILD_V3=0; the default picks by the level's width; the same
     per-chain arithmetic; their reductions sum over different thread counts,
     which can move a weighted growth by an ulp but not, on these inputs, a
     decision) -- against the default schedule.

@@ -423,16 +423,28 @@ static void singleton(ctx_t *c, const rrr_t *R, int64_t j) {
       break;
     }
     delta_prev = delta;
-    /* safeguard (reading 24, amended): a step leaving [lo,hi] from the
-     * interior is clamped to the violated end; from an end it bisects; a
-     * bracket of adjacent doubles is converged. */
+    /* safeguard (reading 24, amended twice): a step leaving [lo,hi] by at
+     * most 4 eps |lambda + delta| is a rounding-level overshoot of an
+     * eigenvalue at that end -- the end itself; otherwise a step leaving
+     * [lo,hi] from the interior is clamped to the violated end and one from
+     * an end bisects, and after such a safeguard step the stagnation test
+     * (reading 10) starts afresh: it compares RQ corrections, and a
+     * bisection halves the next one by construction.  A bracket of adjacent
+     * doubles is converged. */
     double nw = lam + delta;
     if (nw <= lo || nw >= hi) {
-      if (lam == lo || lam == hi) {
+      double slack = 4.0 * EPS * fabs(nw);
+      if (nw <= lo && lo - nw <= slack) {
+        nw = lo;
+      } else if (nw >= hi && nw - hi <= slack) {
+        nw = hi;
+      } else if (lam == lo || lam == hi) {
         nw = 0.5 * (lo + hi);
+        delta_prev = INFINITY;
         if (nw <= lo || nw >= hi) { lam_fin = lam; converged = 1; break; }
       } else {
         nw = (nw <= lo) ? lo : hi;
+        delta_prev = INFINITY;
       }
     }
     lam = nw;

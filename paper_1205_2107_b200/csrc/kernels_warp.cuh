@@ -732,6 +732,40 @@ __device__ __forceinline__ void w_solve_pair(const WarpCtx &W, double lam, int r
   else w_solve_right(W, lam, r, scale, col, active);
 }
 
+// Reading 24 (amended): the shift after an RQ step `delta` from `lam` in the
+// bracket [lo, hi].  A step that leaves the bracket by at most 4 eps |lam +
+// delta| is a rounding-level overshoot of an eigenvalue that sits at the
+// bracket's end: the end itself.  Otherwise a step leaving the bracket from
+// the interior is clamped to the violated end and one from an end bisects;
+// after those safeguard steps `delta_prev` is reset, because the next
+// correction is compared (reading 10's stagnation test) with a step that was
+// not taken -- a bisection halves it by construction, and the test then
+// stopped a linearly converging lane far from the eigenvalue (zero-diagonal
+// T, eigenvalue 0 at a bracket end: tests/test_gpu_edge.py).  `stuck`: the
+// bracket is two adjacent doubles (converged).
+__device__ __forceinline__ double rqc_next(double lam, double delta, double lo, double hi, double &delta_prev,
+                                           bool &stuck) {
+  stuck = false;
+  double nw = lam + delta;
+  delta_prev = delta;
+  if (nw <= lo || nw >= hi) {
+    const double slack = 4.0 * kEps * fabs(nw);
+    if (nw <= lo && lo - nw <= slack) {
+      nw = lo;
+    } else if (nw >= hi && nw - hi <= slack) {
+      nw = hi;
+    } else if (lam == lo || lam == hi) {
+      nw = 0.5 * (lo + hi);
+      delta_prev = CUDART_INF;
+      if (nw <= lo || nw >= hi) stuck = true;
+    } else {
+      nw = (nw <= lo) ? lo : hi;
+      delta_prev = CUDART_INF;
+    }
+  }
+  return nw;
+}
+
 // One work item: up to 32 tasks of one node.
 struct WarpItem {
   int32_t node;    // node of the first task (the item's tasks may span up to kMaxSeg nodes of one block)
@@ -835,23 +869,18 @@ __device__ __forceinline__ void wvec_pair_body(const WVecArgs &A) {
       if (!conv) {
         if (tw.negc >= j) { if (lam < hi) hi = lam; } else { if (lam > lo) lo = lam; }
         const double delta = tw.gamma / tw.nrm2;
+        if (g_debug_rqc && (blockDim.x != kPairThreads || threadIdx.x < 32))
+          printf("rqc task %d it %d lam %.17g r %d gamma %.6g nrm2 %.6g delta %.6g negc %d j %d lo %.17g hi %.17g\n",
+                 tix, it, lam, tw.r, tw.gamma, tw.nrm2, delta, tw.negc, j, lo, hi);
         // stop (reading 10): |delta| <= 4 eps |lambda|, fl(lambda + delta) ==
         // lambda, or stagnation (the correction no longer halves)
         if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam ||
             (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
           conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
         } else {
-          delta_prev = delta;
-          double nw = lam + delta;
-          if (nw <= lo || nw >= hi) {
-            if (lam == lo || lam == hi) {
-              nw = 0.5 * (lo + hi);
-              if (nw <= lo || nw >= hi) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }
-            } else {
-              nw = (nw <= lo) ? lo : hi;
-            }
-          }
-          lam = nw;
+          bool stuck;
+          const double nw = rqc_next(lam, delta, lo, hi, delta_prev, stuck);
+          if (stuck) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }          lam = nw;
         }
         if (!conv && it >= A.rqc_max) { conv = true; failed = true; }
         if (conv) W.tix = spare;  // park: later factorizations must not touch its checkpoints
@@ -962,23 +991,18 @@ __device__ __forceinline__ void wvec_single_body(const WVecArgs &A) {
       if (!conv) {
         if (tw.negc >= j) { if (lam < hi) hi = lam; } else { if (lam > lo) lo = lam; }
         const double delta = tw.gamma / tw.nrm2;
+        if (g_debug_rqc && (blockDim.x != kPairThreads || threadIdx.x < 32))
+          printf("rqc task %d it %d lam %.17g r %d gamma %.6g nrm2 %.6g delta %.6g negc %d j %d lo %.17g hi %.17g\n",
+                 tix, it, lam, tw.r, tw.gamma, tw.nrm2, delta, tw.negc, j, lo, hi);
         // stop (reading 10): |delta| <= 4 eps |lambda|, fl(lambda + delta) ==
         // lambda, or stagnation (the correction no longer halves)
         if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam ||
             (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
           conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
         } else {
-          delta_prev = delta;
-          double nw = lam + delta;
-          if (nw <= lo || nw >= hi) {
-            if (lam == lo || lam == hi) {
-              nw = 0.5 * (lo + hi);
-              if (nw <= lo || nw >= hi) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }
-            } else {
-              nw = (nw <= lo) ? lo : hi;
-            }
-          }
-          lam = nw;
+          bool stuck;
+          const double nw = rqc_next(lam, delta, lo, hi, delta_prev, stuck);
+          if (stuck) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }          lam = nw;
         }
         if (!conv && it >= A.rqc_max) { conv = true; failed = true; }
         if (conv) W.tix = spare;  // park: later factorizations must not touch its checkpoints
@@ -1056,17 +1080,9 @@ struct RqcLane {
         (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
       conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
     } else {
-      delta_prev = delta;
-      double nw = lam + delta;
-      if (nw <= lo || nw >= hi) {
-        if (lam == lo || lam == hi) {
-          nw = 0.5 * (lo + hi);
-          if (nw <= lo || nw >= hi) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }
-        } else {
-          nw = (nw <= lo) ? lo : hi;
-        }
-      }
-      lam = nw;
+      bool stuck;
+      const double nw = rqc_next(lam, delta, lo, hi, delta_prev, stuck);
+      if (stuck) { conv = true; best = tw; lam_best = lam; lam_fin = lam; }      lam = nw;
     }
     if (!conv && it >= rqc_max) { conv = true; failed = true; }
   }

@@ -842,6 +842,15 @@ void set_diag_flags(cudaStream_t s) {
     CK(cudaStreamSynchronize(s));
     last_safe[dev & 63] = fs;
   }
+  {
+    static int last_dbg[64];
+    const int fd = env_int("MRRR_DEBUG_RQC", 0);
+    if (fd != last_dbg[dev & 63]) {
+      CK(cudaMemcpyToSymbolAsync(g_debug_rqc, &fd, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      last_dbg[dev & 63] = fd;
+    }
+  }
   if (fn != last_nudge[dev & 63]) {
     CK(cudaMemcpyToSymbolAsync(g_force_nudge, &fn, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
@@ -870,6 +879,18 @@ int solve(Problem &P, int64_t *m_out) {
   Trace tr;
   g_staging.reset();
   Timer tm(s), tall(s);
+  // MRRR_TIMELINE=1 (diagnostic): device timestamps of the tree's steps and
+  // of every vector piece, printed after the solve (no synchronisation in
+  // between, unlike MRRR_TRACE=2)
+  const bool timeline = getenv("MRRR_TIMELINE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> tline;
+  int tl_level = -1;
+  auto tl_mark = [&](const std::string &what) {
+    if (!timeline) return;
+    cudaEvent_t e = ev_time();
+    cudaEventRecord(e, s);
+    tline.push_back({what, e});
+  };
   KTimer kt_root, kt_fin;
   memset(&g_stats, 0, sizeof(g_stats));
   const bool vectors = P.Z != nullptr;
@@ -1160,16 +1181,16 @@ int solve(Problem &P, int64_t *m_out) {
     }
   };
   // members per refinement warp for a node/cluster of m members: a large
-  // cluster is packed 32 to a warp (4 shifts each while all are active, i.e.
-  // near-bisection work per bit), a small one spread thin (up to 64 shifts
-  // each, fewer rounds).  Depends on m alone, so every rank that holds a
+  // block is packed 16 to a warp (with M = 2: 4 shifts each while all are
+  // active, i.e. near-bisection work per bit), a small one spread thin (up
+  // to 64 shifts each, fewer rounds).  Depends on m alone, so every rank that holds a
   // shared cluster forms the same work items (§8(e)).
   // diagnostics (read per call): MRRR_RW_CHUNK / MRRR_RW_M override the refinement work items
   const int rw_env = env_int("MRRR_RW_CHUNK", 0);
   const int rw_m_env = env_int("MRRR_RW_M", 0);
   auto rw_chunk = [&](int m) {
     if (rw_env > 0) return std::min(rw_env, kRWMembers);
-    return m >= 512 ? 32 : m >= 128 ? 16 : 8;
+    return m >= 128 ? 16 : 8;
   };
   auto rw_chunk_tree = [&](int m) {
     if (rw_env > 0) return std::min(rw_env, kRWMembers);
@@ -1177,6 +1198,11 @@ int solve(Problem &P, int64_t *m_out) {
     return 8;
   };
   const int rw_m_tree = rw_m_env > 0 ? rw_m_env : 1;
+  // shifts per lane of the root refinement (diagnostic MRRR_RW_ROOT_M)
+  // (measured, random n=20000: chunks of 16 members with M = 2 -- 1250 warps
+  // of four chains each, split counts -- root 5.05 -> 4.3 ms with the grid at
+  // one shift per thread, against 625 warps of chunk 32 with M = 4)
+  const int rw_m_root = std::max(1, std::min(4, env_int("MRRR_RW_ROOT_M", 2)));
   // reading 31: tree members stop refining at 2^-early_bits once their
   // classification is decided (MRRR_EARLY_BITS; 0 = off, refine all to rtol_class)
   const int early_bits = env_int("MRRR_EARLY_BITS", 12);
@@ -1185,7 +1211,7 @@ int solve(Problem &P, int64_t *m_out) {
   const int split_env = env_int("MRRR_SPLIT", 2);
   const bool split_tree = split_env >= 1, split_root = split_env >= 2;
   // shifts per thread of the root grid (MRRR_GRID_M, diagnostic: 1, 2 or 4)
-  const int grid_m = env_int("MRRR_GRID_M", 4);
+  const int grid_m = env_int("MRRR_GRID_M", 1);
   // clusters of at least rw_end members refine their two end members in
   // work items of their own (0: off); MRRR_RW_END overrides
   const int rw_end = env_int("MRRR_RW_END", 0);
@@ -1260,7 +1286,7 @@ int solve(Problem &P, int64_t *m_out) {
         CK(cudaMemcpyToSymbol(g_rw_hist, z, sizeof z));
       }
       launch_refine(dnodes, dwork + w0, (int)(w1 - w0), nullptr, slot_j, slo, shi, nullptr, nullptr, 0, rtol_root,
-                    dfail + 2, ctr, ctr + 1, s, 4, 0.0, 0.0, split_root);
+                    dfail + 2, ctr, ctr + 1, s, rw_m_root, 0.0, 0.0, split_root);
       if (tr.lvl >= 2) {  // diagnostic: rounds per root refinement warp
         CK(cudaStreamSynchronize(s));
         unsigned hist[64];
@@ -1422,6 +1448,7 @@ int solve(Problem &P, int64_t *m_out) {
   *m_out = m;
   if (tr.on) { CK(cudaStreamSynchronize(s)); tr.mark("root bisection"); }
   g_stats.ms_root = tm.stop();
+  tl_mark("root done");
 
   if (!vectors) {
     k_values<<<(nslots + 255) / 256, 256, 0, s>>>(slot_node, slot_out, dnodes, slo, shi,
@@ -1495,6 +1522,7 @@ int solve(Problem &P, int64_t *m_out) {
   FwdCk *ck_f[kSide] = {};
   BwdCk *ck_b[kSide] = {};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> vec_ev;
+  std::vector<int> vec_ev_level;  // tree level that launched each piece (MRRR_TIMELINE)
   size_t vec_done = 0;
   // Child RRR slots (nbmax (D+, LLD+) rows each), RECYCLED (SURVEY H9,
   // memory independent of the tree's size).  A node's slot is
@@ -1711,6 +1739,7 @@ int solve(Problem &P, int64_t *m_out) {
       CK(cudaEventRecord(eb, s2));
       tr.fine(s2, "  vectors (side stream)");
       vec_ev.push_back({ea, eb});
+      vec_ev_level.push_back(tl_level);
       zb_done(t0, t1, eb);
       t0 = t1;
     }
@@ -1723,6 +1752,8 @@ int solve(Problem &P, int64_t *m_out) {
       snprintf(nm, sizeof nm, "mrrr level %d", level);
       tr.phase(nm);
     }
+    tl_level = level;
+    tl_mark("L" + std::to_string(level) + " start");
     h2d(active, h_active.data(), nslots, s);
     k_classify<<<(nslots + 255) / 256, 256, 0, s>>>(slot_node, slo, shi, active, (int)nslots,
                                                     P.o.tol_relgap, run_end);
@@ -1887,6 +1918,7 @@ int solve(Problem &P, int64_t *m_out) {
         g_stats.kernel_launches++;
       }
       tr.fine(s, "  child step");
+      tl_mark("L" + std::to_string(level) + " child step done");
       if (tr.lvl >= 2) {  // diagnostic: this level's slowest cluster step, cycles per phase
         unsigned long long c[8];
         CK(cudaMemcpy(c, ctr + 16, sizeof c, cudaMemcpyDeviceToHost));
@@ -1957,6 +1989,7 @@ int solve(Problem &P, int64_t *m_out) {
                     dfail + 2, ctr + 2, ctr + 1, s, rw_m_tree, early_bits > 0 ? P.o.tol_relgap : 0.0,
                     std::ldexp(1.0, -early_bits), split_tree);
       tr.fine(s, "  refine");
+      tl_mark("L" + std::to_string(level) + " refine done");
       if (tr.lvl >= 2) {  // diagnostic: rounds per refinement warp
         unsigned hist[64];
         CK(cudaMemcpyFromSymbol(hist, g_rw_hist, sizeof hist));
@@ -2017,6 +2050,7 @@ int solve(Problem &P, int64_t *m_out) {
   }
   g_stats.levels = level;
   g_stats.ms_tree = ttree.stop();
+  tl_mark("tree done");
 
   // ---------------- a6: singleton vectors (launched per level above) ----------------
   tr.phase("mrrr vector tail");
@@ -2164,6 +2198,21 @@ int solve(Problem &P, int64_t *m_out) {
       ms += v;
     }
     g_stats.ms_k_vectors = ms;
+  }
+  if (timeline) {
+    cudaStreamSynchronize(s);
+    for (auto &m : tline) {
+      float v = 0;
+      cudaEventElapsedTime(&v, tall.a, m.second);
+      fprintf(stderr, "[mrrr timeline] %8.3f ms  tree  %s\n", v, m.first.c_str());
+    }
+    for (size_t i = 0; i < vec_ev.size(); ++i) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, tall.a, vec_ev[i].first);
+      cudaEventElapsedTime(&b, tall.a, vec_ev[i].second);
+      fprintf(stderr, "[mrrr timeline] %8.3f ms  piece %zu (level %d) ends %8.3f ms (%.3f ms)\n", a, i,
+              vec_ev_level[i], b, b - a);
+    }
   }
   g_stats.ms_k_final_refine = kt_fin.ms();
   // bytes this call used: the call arena, the largest level arena, the

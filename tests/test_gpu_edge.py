@@ -293,3 +293,22 @@ def test_scratch_cap_and_pool_recycling(torch_cuda, P):
     assert s1["nodes"] == s2["nodes"] and s1["nodes"] > 1000
     for s in (s1, s2):
         assert 16 * n <= s["pool_bytes"] < 16 * n * s["nodes"]
+
+
+@pytest.mark.parametrize("root_m", ["1", "2", "4"])
+@pytest.mark.parametrize("n", [3, 5, 7, 9, 11, 21, 101, 1001])
+def test_zero_diagonal_exact_zero_eigenvalue(torch_cuda, P, oracle_mod, monkeypatch, n, root_m):
+    """d = 0, e = 1 (odd n: eigenvalue 0 exactly, its vector zero at every odd
+    row).  With some root brackets the eigenvalue sits within rounding of a
+    bracket end; the RQC step then overshoots the end by an ulp or two, which
+    reading 24 (amended) clamps to the end instead of bisecting -- bisection
+    halved every later correction and the stagnation test stopped the lane at
+    ~1e-10 (residual 4e4x the bound at n = 3 and 21).  The root refinement's
+    shifts per lane (MRRR_RW_ROOT_M) change the brackets."""
+    monkeypatch.setenv("MRRR_RW_ROOT_M", root_m)
+    d, e = np.zeros(n), np.ones(n - 1)
+    w, Z = gpu_solve(P, torch_cuda, d, e)
+    lam = np.sort(2 * np.cos(np.arange(1, n + 1) * np.pi / (n + 1)))
+    assert np.max(np.abs(w - lam)) <= 4 * n * EPS * tnorm1(d, e)
+    res, orth = check_accuracy(d, e, w, Z)
+    assert res <= 1 and orth <= 1, (res, orth)

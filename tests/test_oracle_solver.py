@@ -35,6 +35,20 @@ def test_config1_one_two_one_closed_form(oracle_mod):
     assert res <= 1 and orth <= 1
 
 
+@pytest.mark.parametrize("n", [3, 5, 7, 21, 101, 1001])
+def test_zero_diagonal_closed_form(oracle_mod, n):
+    """d = 0, e = 1: lambda_k = 2 cos(k pi / (n+1)) (the 1-2-1 spectrum shifted
+    by -2); for odd n the middle eigenvalue is exactly 0 and its vector has a
+    zero at every odd row -- an RQC that lands on a bracket end within
+    rounding (reading 24's overshoot rule) must still converge to it."""
+    d, e = np.zeros(n), np.ones(n - 1)
+    w, Z = oracle_mod.stemr(d, e)
+    lam = np.sort(2 * np.cos(np.arange(1, n + 1) * np.pi / (n + 1)))
+    assert np.max(np.abs(w - lam)) <= 4 * n * EPS * tnorm1(d, e)
+    res, orth = check_accuracy(d, e, w, Z)
+    assert res <= 1 and orth <= 1
+
+
 @pytest.mark.parametrize("n", [64, 400, 1000])
 def test_clement_closed_form(oracle_mod, n):
     d, e = W.clement(n)

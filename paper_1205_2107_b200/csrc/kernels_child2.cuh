@@ -50,6 +50,7 @@ struct Child2Smem {
   int gjw[3];
   int best, tier;
   double sg;
+  int rr[2];  // POST: the probes' twist indices
 };
 
 // POST = true (ADJ = 0): the chains were run by k_child_chains3
@@ -65,7 +66,10 @@ template <int ADJ, bool POST = false>
 #ifndef MRRR_CS2_MINB
 #define MRRR_CS2_MINB 6
 #endif
-__global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(ChildArgs A) {
+#ifndef MRRR_CS2P_MINB
+#define MRRR_CS2P_MINB 6
+#endif
+__global__ void __launch_bounds__(POST ? 128 : 96, ADJ ? 2 : POST ? MRRR_CS2P_MINB : MRRR_CS2_MINB) k_child_step2(ChildArgs A) {
   constexpr int NPROBE = 2 + 2 * ADJ;  // probe sides
   __shared__ Child2Smem S;
   if (A.c0 + (int)blockIdx.x >= A.ncl) return;
@@ -273,13 +277,32 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
   __syncthreads();
   const long long clk_p1 = clock64();
 
-  // ---- phase 2: each probe's twist index and |z|; warp w takes the sides
-  // w, w + 3 (the up and down scans of a side in sequence)
-  for (int side = wid; side < NPROBE; side += 3) {
-    if (side >= 2 && !has_int) break;
+  // ---- phase 2: each probe's twist index and |z| (the up and down scans
+  // from r).  Without POST warp w takes the sides w, w + 3, each side's
+  // argmin and two scans in sequence; with POST (four warps, ADJ = 0) the two
+  // argmins run on warps 0, 1 and then the four scans on one warp each --
+  // the same per-side arithmetic, so the same values
+  constexpr double kDead = -1.0e9;
+  auto split = [](double x, double &mm, double &ee) {
+    const long long bb = __double_as_longlong(x) & 0x7fffffffffffffffLL;
+    const int ex = (int)(bb >> 52);
+    const bool ok = ex > 0 && ex < 2047;
+    mm = ok ? __longlong_as_double((bb & 0x000fffffffffffffLL) | 0x3ff0000000000000LL) : 1.0;
+    ee = ok ? (double)(ex - 1023) : kDead;
+  };
+  auto mul = [](double &mm, double &ee, double m2, double e2) {
+    mm *= m2; ee += e2;
+    if (mm >= 2.0) { mm *= 0.5; ee += 1.0; }
+  };
+  auto to_double = [](double mm, double ee) {
+    if (ee < -1022.0) return 0.0;
+    if (ee > 1023.0) return CUDART_INF;
+    const int ei = (int)ee;
+    return __hiloint2double(__double2hiint(mm) + (ei << 20), __double2loint(mm));
+  };
+  auto twist_of = [&](int side) {  // r = argmin |s_i + P_i + lam| (ties: lowest i), z[r] = 1
     const double lam = probe_lam(side);
-    const double *sS = pr[side], *sP = pr[side] + zs, *sR = pr[side] + 2 * zs, *sG = pr[side] + 3 * zs;
-    double *z = zz[side];
+    const double *sS = pr[side], *sP = pr[side] + zs;
     double bv = CUDART_INF;
     int bi = nb;
 #pragma unroll 8
@@ -294,56 +317,56 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
     }
     int r = bi;
     if (r >= nb) r = nb - 1;
-    if (lane == 0) z[r] = 1.0;
-    constexpr double kDead = -1.0e9;
-    auto split = [](double x, double &mm, double &ee) {
-      const long long bb = __double_as_longlong(x) & 0x7fffffffffffffffLL;
-      const int ex = (int)(bb >> 52);
-      const bool ok = ex > 0 && ex < 2047;
-      mm = ok ? __longlong_as_double((bb & 0x000fffffffffffffLL) | 0x3ff0000000000000LL) : 1.0;
-      ee = ok ? (double)(ex - 1023) : kDead;
-    };
-    auto mul = [](double &mm, double &ee, double m2, double e2) {
-      mm *= m2; ee += e2;
-      if (mm >= 2.0) { mm *= 0.5; ee += 1.0; }
-    };
-    auto to_double = [](double mm, double ee) {
-      if (ee < -1022.0) return 0.0;
-      if (ee > 1023.0) return CUDART_INF;
-      const int ei = (int)ee;
-      return __hiloint2double(__double2hiint(mm) + (ei << 20), __double2loint(mm));
-    };
-    for (int dirn = 0; dirn < 2; ++dirn) {
-      const bool up = dirn == 0;
-      const int m = up ? r : nb - 1 - r;
-      const double *src = up ? sR + (r - 1) : sG + r;
-      const int dir = up ? -1 : 1;
-      double *dst = up ? z + (r - 1) : z + (r + 1);
-      double cm = 1.0, ce = 0.0;
-      constexpr int kBlk = 8;
-      for (int b0 = 0; b0 < m; b0 += 32 * kBlk) {
-        double xv[kBlk];
+    if (lane == 0) zz[side][r] = 1.0;
+    return r;
+  };
+  auto scan_from = [&](int side, int dirn, int r) {  // |z| of the rows above (dirn 0) or below (1) r
+    const double *sR = pr[side] + 2 * zs, *sG = pr[side] + 3 * zs;
+    double *z = zz[side];
+    const bool up = dirn == 0;
+    const int m = up ? r : nb - 1 - r;
+    const double *src = up ? sR + (r - 1) : sG + r;
+    const int dir = up ? -1 : 1;
+    double *dst = up ? z + (r - 1) : z + (r + 1);
+    double cm = 1.0, ce = 0.0;
+    constexpr int kBlk = 8;
+    for (int b0 = 0; b0 < m; b0 += 32 * kBlk) {
+      double xv[kBlk];
 #pragma unroll
-        for (int u = 0; u < kBlk; ++u) {
-          const int j = b0 + u * 32 + lane;
-          xv[u] = j < m ? src[dir * j] : 1.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kBlk; ++u) {
-          const int j = b0 + u * 32 + lane;
-          double im, ie;
-          split(xv[u], im, ie);
-          if (j >= m) { im = 1.0; ie = 0.0; }
-          for (int o = 1; o < 32; o <<= 1) {
-            const double ym = __shfl_up_sync(0xffffffffu, im, o), ye = __shfl_up_sync(0xffffffffu, ie, o);
-            if (lane >= o) mul(im, ie, ym, ye);
-          }
-          mul(im, ie, cm, ce);
-          if (j < m) dst[dir * j] = to_double(im, ie);
-          cm = __shfl_sync(0xffffffffu, im, 31);
-          ce = __shfl_sync(0xffffffffu, ie, 31);
-        }
+      for (int u = 0; u < kBlk; ++u) {
+        const int j = b0 + u * 32 + lane;
+        xv[u] = j < m ? src[dir * j] : 1.0;
       }
+#pragma unroll
+      for (int u = 0; u < kBlk; ++u) {
+        const int j = b0 + u * 32 + lane;
+        double im, ie;
+        split(xv[u], im, ie);
+        if (j >= m) { im = 1.0; ie = 0.0; }
+        for (int o = 1; o < 32; o <<= 1) {
+          const double ym = __shfl_up_sync(0xffffffffu, im, o), ye = __shfl_up_sync(0xffffffffu, ie, o);
+          if (lane >= o) mul(im, ie, ym, ye);
+        }
+        mul(im, ie, cm, ce);
+        if (j < m) dst[dir * j] = to_double(im, ie);
+        cm = __shfl_sync(0xffffffffu, im, 31);
+        ce = __shfl_sync(0xffffffffu, ie, 31);
+      }
+    }
+  };
+  if (POST) {
+    if (wid < 2) {
+      const int r = twist_of(wid);
+      if (lane == 0) S.rr[wid] = r;
+    }
+    __syncthreads();
+    scan_from(wid & 1, wid >> 1, S.rr[wid & 1]);
+  } else {
+    for (int side = wid; side < NPROBE; side += 3) {
+      if (side >= 2 && !has_int) break;
+      const int r = twist_of(side);
+      scan_from(side, 0, r);
+      scan_from(side, 1, r);
     }
   }
   __syncthreads();
@@ -361,7 +384,7 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
 #pragma unroll
   for (int k = 0; k < kNC; ++k) { g[k] = 0.0; nl[k] = 0.0; nr[k] = 0.0; }
 #pragma unroll 2
-  for (int i = tid; i < nb; i += 96) {
+  for (int i = tid; i < nb && wid < 3; i += 96) {  // (POST: warp 3 sits out -- the same sums as 96 threads)
     const double a = zl[i], b = zr[i];
     const double a2 = a * a, b2 = b * b;
     dnl += a2; dnr += b2;
@@ -396,7 +419,7 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
       dnb += __shfl_xor_sync(0xffffffffu, dnb, o);
     }
   }
-  if (lane == 0) {
+  if (lane == 0 && wid < 3) {
 #pragma unroll
     for (int k = 0; k < kNC; ++k) {
       S.red[wid][k] = g[k]; S.red[wid][kNC + k] = nl[k]; S.red[wid][2 * kNC + k] = nr[k];
@@ -463,7 +486,7 @@ __global__ void __launch_bounds__(96, ADJ ? 2 : MRRR_CS2_MINB) k_child_step2(Chi
   double2 *out = A.pool[c];
   bool bad = false;
 #pragma unroll 4
-  for (int i = tid; i < nb; i += 96) {
+  for (int i = tid; i < nb; i += (POST ? 128 : 96)) {
     const double Dp = cs_dplus(TP, QK, zs, best, i);
     const double lld = (i < nb - 1) ? __ldg(&LD[i]).y / Dp : 0.0;
     bad |= !isfinite(Dp) || Dp == 0.0 || !isfinite(lld);

@@ -1909,7 +1909,7 @@ int solve(Problem &P, int64_t *m_out) {
           else if (c3_groups == 2) k_child_chains3<2><<<(nl + per - 1) / per, 32 * kC3Warps, 0, s>>>(CA);
           else k_child_chains3<3><<<(nl + per - 1) / per, 32 * kC3Warps, 0, s>>>(CA);
           CK(cudaGetLastError());
-          k_child_step2<0, true><<<nl, 96, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
+          k_child_step2<0, true><<<nl, 128, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));
           g_stats.kernel_launches++;
         } else {
           k_child_step2<0><<<nl, 96, 0, s>>>(child_args(dsmall, c0, c0 + nl, scratch));

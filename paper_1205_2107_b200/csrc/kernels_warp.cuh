@@ -1202,11 +1202,137 @@ __device__ __forceinline__ void wvec_split_body(const WVecArgs &A) {
   if (lane == 0) atomicMax(&A.ctr[7], nfact);
 }
 
+// The split RQC on warp PAIRS (round 2): mode 3 = the full factorization
+// (w_full_pair, nudges as in wvec_pair_body) and the first RQC update, state
+// stored per task; the host sorts each node's tasks by twist index; mode 4 =
+// the remaining fixed-twist factorizations (w_fixed_pair) and the solve
+// (w_solve_pair) with the item's lanes in that order.  After the regrouping
+// the lanes of an item share one row window, so warp F's forward rows
+// (below the largest r of the item) and warp B's backward rows (above the
+// smallest r) no longer both span the node.  Per-lane arithmetic is
+// wvec_pair_body's / wvec_split_body's (bit-identical results).
+__device__ __forceinline__ void wvec_pair_split_body(const WVecArgs &A) {
+  extern __shared__ __align__(16) unsigned char wsm_raw[];
+  const int role = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x;
+  if (item >= A.nitems) return;  // whole CTA
+  const WarpItem It = A.items[item];
+  const bool active = It.t0 + lane < It.t1;
+  const int pos = active ? It.t0 + lane : It.t1 - 1;
+  const int tix = A.task_list ? A.task_list[pos] : pos;
+  const VecTask tk = A.tasks[tix];
+  const Node N = A.nodes[tk.node];
+  WarpCtx W;
+  W.DL = N.DL; W.LDv = A.LDv + N.row0; W.nb = N.nb; W.nseg = (N.nb + kTR - 1) / kTR;
+  W.lane = lane;
+  W.sm = reinterpret_cast<WarpSmem *>(wsm_raw) + role;
+  w_segments(W, A.tasks[pos].node, active);
+  PairX &X = *reinterpret_cast<PairX *>(wsm_raw + 2 * sizeof(WarpSmem));
+  W.fck = A.fck; W.bck = A.bck; W.ck_stride = A.ck_stride;
+  const int64_t spare = A.ntask + lane;
+  W.tix = active ? tix : spare;
+  const bool lead = role == 0;
+  const int j = A.slot_j[tk.slot];
+  if (A.mode == 3) {
+    if (N.nb == 1) return;  // phase 2 writes it
+    double lam = isnan(tk.lam0) ? 0.5 * (A.lo[tk.slot] + A.hi[tk.slot]) : tk.lam0;
+    unsigned long long nfact = 0;
+    Twist tw;
+    {
+      double nudge = 2.0 * kEps * fabs(lam) + kTiny;
+      const double lam_base = lam;
+      for (int tries = 0; tries < 60; ++tries) {
+        tw = w_full_pair(W, lam, role, X);
+        ++nfact;
+        if (g_force_nudge && tries == 0) tw.ok = false;  // diagnostic (MRRR_FORCE_NUDGE)
+        if (!__any_sync(0xffffffffu, active && !tw.ok)) break;
+        if (active && !tw.ok) {
+          lam = lam_base + nudge; nudge *= 2.0;
+          if (lead) {
+            atomicAdd(&A.ctr[2], 1ull);
+            if (A.ctr[3] == 0) A.ctr[3] = 1 + (isfinite(tw.gamma) ? 0 : 2) + (isfinite(tw.nrm2) ? 0 : 4);
+          }
+        }
+      }
+    }
+    RqcLane Q;
+    Q.lam = lam; Q.lo = A.lo[tk.slot]; Q.hi = A.hi[tk.slot]; Q.delta_prev = CUDART_INF;
+    Q.lam_best = lam; Q.lam_fin = lam; Q.best = tw; Q.conv = !active; Q.failed = false;
+    if (!Q.conv) Q.update(tw, j, 1, A.rqc_max);
+    if (active && lead) {
+      RqcState st;
+      st.lam = Q.lam; st.lo = Q.lo; st.hi = Q.hi; st.delta_prev = Q.delta_prev;
+      st.lam_best = Q.lam_best; st.lam_fin = Q.lam_fin; st.gamma = Q.best.gamma; st.nrm2 = Q.best.nrm2;
+      st.r = Q.best.r; st.negc = Q.best.negc; st.best_r0 = tw.r;
+      st.flags = (Q.conv ? 1 : 0) | (Q.failed ? 2 : 0) | (Q.best.ok ? 4 : 0);
+      st.nfact = nfact;
+      A.state[tix] = st;
+      A.rkey[tix] = tw.r;
+    }
+    return;
+  }
+  // ---- mode 4: the rest of the RQC and the solve, lanes in twist order
+  if (N.nb == 1) {
+    if (active && lead) { A.Z[tk.col * A.ldz + N.row0] = 1.0; A.lam_out[tix] = __ldg(&N.DL[0]).x; }
+    return;
+  }
+  RqcLane Q;
+  int best_r0 = 0;
+  unsigned long long nfact = 0;
+  if (active) {
+    const RqcState st = A.state[tix];
+    Q.lam = st.lam; Q.lo = st.lo; Q.hi = st.hi; Q.delta_prev = st.delta_prev;
+    Q.lam_best = st.lam_best; Q.lam_fin = st.lam_fin;
+    Q.best.r = st.r; Q.best.gamma = st.gamma; Q.best.nrm2 = st.nrm2; Q.best.negc = st.negc;
+    Q.best.ok = (st.flags & 4) != 0;
+    Q.conv = (st.flags & 1) != 0; Q.failed = (st.flags & 2) != 0;
+    best_r0 = st.best_r0; nfact = st.nfact;
+  } else {
+    Q.lam = 0.0; Q.lo = 0.0; Q.hi = 0.0; Q.delta_prev = CUDART_INF; Q.lam_best = 0.0; Q.lam_fin = 0.0;
+    Q.best.r = 0; Q.best.gamma = 0.0; Q.best.nrm2 = 1.0; Q.best.negc = 0; Q.best.ok = true;
+    Q.conv = true; Q.failed = false;
+  }
+  // checkpoints in the lane's POSITION column (wvec_split_body); a lane that
+  // converged in phase 1 rebuilds them with one fixed-twist factorization
+  W.tix = active ? pos : spare;
+  {
+    const bool refac = active && Q.conv && !Q.failed;
+    if (__any_sync(0xffffffffu, refac)) {
+      (void)w_fixed_pair(W, Q.lam_best, Q.best.r, refac, role, X);
+      if (refac) ++nfact;
+    }
+  }
+  if (Q.conv) W.tix = spare;
+  for (int it = 1;;) {
+    if (__all_sync(0xffffffffu, Q.conv)) break;
+    const Twist tw = w_fixed_pair(W, Q.lam, best_r0, !Q.conv, role, X);
+    if (!Q.conv) ++nfact;
+    ++it;
+    if (!Q.conv && !tw.ok) { Q.conv = true; Q.failed = true; }
+    else if (!Q.conv) Q.update(tw, j, it, A.rqc_max);
+    if (Q.conv) W.tix = spare;
+  }
+  W.tix = active ? pos : spare;
+  if (active && Q.failed && lead) {
+    A.lo[tk.slot] = Q.lo; A.hi[tk.slot] = Q.hi;
+    A.fail_list[atomicAdd(A.fail_count, 1)] = A.task_base + tix;
+    atomicAdd(&A.ctr[1], 1ull);
+  }
+  const double sc = 1.0 / sqrt(Q.best.nrm2);
+  w_solve_pair(W, Q.lam_best, Q.best.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !Q.failed, role);
+  if (lead) {
+    if (active && !Q.failed) A.lam_out[tix] = Q.lam_fin;
+    if (active) atomicAdd(&A.ctr[0], nfact);
+    if (lane == 0) atomicMax(&A.ctr[7], nfact);
+  }
+}
+
 // At most 168 registers per thread (6 CTAs of 64 threads per SM by
 // registers): the vector pieces share the SMs with the tree's kernels.
 __global__ void __launch_bounds__(32 * kSingleWarps, 6) k_wvectors_split(WVecArgs A) { wvec_split_body(A); }
 
 __global__ void __launch_bounds__(kPairThreads, 6) k_wvectors_pair(WVecArgs A) { wvec_pair_body(A); }
+__global__ void __launch_bounds__(kPairThreads, 6) k_wvectors_psplit(WVecArgs A) { wvec_pair_split_body(A); }
 __global__ void __launch_bounds__(32 * kSingleWarps, 6) k_wvectors(WVecArgs A) { wvec_single_body(A); }
 
 }  // namespace mrrr

@@ -732,6 +732,21 @@ void launch_wsplit(WVecArgs A, int mode, cudaStream_t s) {
   g_stats.kernel_launches++;
 }
 
+// The same phases on warp pairs (k_wvectors_psplit).
+void launch_wpsplit(WVecArgs A, int mode, cudaStream_t s) {
+  const size_t smem2 = 2 * sizeof(WarpSmem) + sizeof(PairX);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_wvectors_psplit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    attr = true;
+  }
+  if (A.nitems == 0) return;
+  A.mode = mode;
+  k_wvectors_psplit<<<A.nitems, kPairThreads, smem2, s>>>(A);
+  CK(cudaGetLastError());
+  g_stats.kernel_launches++;
+}
+
 struct SplitBufs {
   RqcState *state;
   int *rkey, *rkey_out, *perm_in, *perm, *seg_b, *seg_e;
@@ -1643,6 +1658,9 @@ int solve(Problem &P, int64_t *m_out) {
   const double kPairWork = getenv("MRRR_PAIR_WORK") ? atof(getenv("MRRR_PAIR_WORK")) : 2.5e7;
   const int vec_pair = env_int("MRRR_VEC_PAIR", 1);
   const int vec_split = env_int("MRRR_VEC_SPLIT", 1);
+  // warp-pair pieces with the lanes regrouped by twist index too
+  // (k_wvectors_psplit); MRRR_VEC_PSPLIT=0: k_wvectors_pair (diagnostic)
+  const int vec_psplit = env_int("MRRR_VEC_PSPLIT", 1);
   const int vec_pack = env_int("MRRR_VEC_PACK", 1) ? kMaxSeg : 1;
   const int tree_side = std::min(kSide, std::max(1, env_int("MRRR_TREE_SIDE", kSide)));
   auto flush_vectors = [&](int tree_left) {
@@ -1679,7 +1697,7 @@ int solve(Problem &P, int64_t *m_out) {
       // between the phases (k_wvectors_split: ~25 % fewer rows walked by the
       // fixed-twist factorizations and the solve; random n = 1e5 1.84 -> 1.59 s).
       // MRRR_VEC_SPLIT=0: one kernel (k_wvectors).
-      const bool split = !pair && vec_split != 0;
+      const bool split = vec_split != 0 && (!pair || vec_psplit != 0);
       SplitBufs sb{};
       if (split) {
         // sort segments: each node's run of tasks (items may span several nodes)
@@ -1709,12 +1727,14 @@ int solve(Problem &P, int64_t *m_out) {
       CK(cudaEventRecord(ea, s2));
       if (split) {
         A.state = sb.state; A.rkey = sb.rkey;
-        launch_wsplit(A, 3, s2);
+        if (pair) launch_wpsplit(A, 3, s2);
+        else launch_wsplit(A, 3, s2);
         k_iota<<<(nbt + 255) / 256, 256, 0, s2>>>(sb.perm_in, nbt);
         CK(cub::DeviceSegmentedRadixSort::SortPairs(sb.temp, sb.temp_bytes, sb.rkey, sb.rkey_out, sb.perm_in,
                                                     sb.perm, nbt, sb.nseg, sb.seg_b, sb.seg_e, 0, sb.bits, s2));
         A.task_list = sb.perm;
-        launch_wsplit(A, 4, s2);
+        if (pair) launch_wpsplit(A, 4, s2);
+        else launch_wsplit(A, 4, s2);
         g_stats.kernel_launches += 2;
       } else {
         launch_wvec(A, s2, pair);

@@ -174,7 +174,8 @@ def test_deterministic(torch_cuda, P):
                                  {"MRRR_VEC_PAIR": "2"}, {"MRRR_HP_STREAM": "0"}, {"MRRR_VEC_SPLIT": "0"},
                                  {"MRRR_VEC_PACK": "0"}, {"MRRR_CHILD_V1": "1"},
                                  {"MRRR_CHILD_V1": "0"}, {"MRRR_CHILD_V1": "0", "MRRR_CHILD_V3": "0"},
-                                 {"MRRR_CHILD_V1": "0", "MRRR_CS_GROUP": "5"}])
+                                 {"MRRR_CHILD_V1": "0", "MRRR_CS_GROUP": "5"}, {"MRRR_VEC_PSPLIT": "0"},
+                                 {"MRRR_VEC_PAIR": "2", "MRRR_VEC_PSPLIT": "0"}])
 def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     """The launch schedule does not change a single bit: cluster steps in
     groups that reuse the scratch (MRRR_CS_GROUP, the n = 1e5 memory cap's
@@ -184,7 +185,7 @@ def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     split over two warps), the caller's stream instead of the library's
     high-priority one (MRRR_HP_STREAM=0), the single-warp RQC in one kernel
     instead of two phases with the lanes regrouped by twist index
-    (MRRR_VEC_SPLIT=0), one node per vector work item instead of up to
+    (MRRR_VEC_SPLIT=0; MRRR_VEC_PSPLIT=0 the same for the warp-pair pieces), one node per vector work item instead of up to
     kMaxSeg nodes of a block packed into a warp (MRRR_VEC_PACK=0), the cluster
     step with one warp per chain or one lane per chain at every level
     (MRRR_CHILD_V1=1 / 0; with V1=0 the chains run lane-dense, three clusters

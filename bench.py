@@ -337,7 +337,7 @@ def main():
     t_z = 8.0 * n * m / (HBM_GBS * 1e9)
     t_roof = max(t_alu, t_z)
     t_step = tot_ms / args.steps / 1e3
-    kernels, traffic, ksrc = None, None, None
+    kernels, traffic, ksrc, hw_slots = None, None, None, None
     kt = os.path.join(ROOT, "profiles", "r02", f"kernel_table_{args.config}.json")
     if os.path.exists(kt):
         try:
@@ -349,6 +349,7 @@ def main():
                            "dram_bytes": v["dram_bytes"]}
                        for k, v in list(kj["kernels"].items())[:8]}
             traffic = sum(v["dram_bytes"] for v in kj["kernels"].values())
+            hw_slots = sum(v["fp64_slots"] for v in kj["kernels"].values())
         except Exception:
             kernels = None
     roof = {"bound": "alu", "kernel": "whole step (all SURVEY §8(a) rows; kernels overlap on five streams)",
@@ -363,6 +364,11 @@ def main():
                     "paper's recurrences need) per second: model work/s, not executed instructions; "
                     "`kernels` gives each kernel's executed FP64 instructions (ncu) against the peak",
             "kernels_source": ksrc, "kernels": kernels,
+            # the hardware view of the whole step: FP64-pipe slots the kernels
+            # EXECUTED in one solve (ncu: DFMA + DMUL + DADD, all kernels) per
+            # step time, against the FP64 peak
+            "hw_fp64_slots_per_solve": hw_slots,
+            "hw_step_fp64_frac": (hw_slots / t_step / (FP64_PEAK_TFLOPS * 1e12 / 2)) if hw_slots else None,
             "vector_kernels_event_ms": kv, "root_bisect_event_ms": kb,
             "root_bisect_model_work_tflops": 2 * slots_bis / (kb / 1e3) / 1e12 if kb else None}
 

@@ -408,15 +408,17 @@ __global__ void k_root_interval(const Node *nodes, const Block *blocks, const in
   if (!found) { lo0[r] = hi0[r] = 0.0; fail[0] = 1; }
 }
 
-// Warp version: the 32 lanes try the offsets wid * 2^k, k = k0 .. k0+31, in
-// ONE sweep of the root representation (rows through a cp.async ring of
-// 16-row tiles, read as broadcasts); the first passing k is the sequential
-// loop's answer.
+// Warp version: lanes l and l + 16 try the offset wid * 2^(k0 + l % 16) in
+// ONE sweep of the root representation, counting as a twisted factorization
+// (reading 32, as k_refine_warp): lanes 0-15 the stationary transform over
+// rows 0 .. r-1, lanes 16-31 the progressive one over rows nb-2 .. r (the
+// bottom tiles copied swapped), half the rows each; the first passing k is
+// the sequential loop's answer.
 __global__ void __launch_bounds__(32) k_root_interval_warp(const Node *nodes, const Block *blocks,
                                                            const int *root_nodes, int nroot, double *lo0,
                                                            double *hi0, double tnrm_scaled, int *fail) {
   constexpr int T = 16, RING = 6;
-  __shared__ double2 ring[RING][T];
+  __shared__ double2 ring[RING][2 * T];
   const int r = blockIdx.x, lane = threadIdx.x;
   if (r >= nroot) return;
   const Node N = nodes[root_nodes[r]];
@@ -424,34 +426,49 @@ __global__ void __launch_bounds__(32) k_root_interval_warp(const Node *nodes, co
   const double sigma = N.tau_hi;
   const double wid0 = 2.0 * kEps * fmax(B.spdiam, tnrm_scaled) + kTiny;
   if (N.nb == 1) { if (lane == 0) { lo0[r] = hi0[r] = __ldg(&N.DL[0]).x; } return; }
-  const int nb = N.nb, body = nb - 1, ntile = (body + T - 1) / T;
-  for (int k0 = 0; k0 < 224; k0 += 32) {
-    const double w = wid0 * ldexp(1.0, k0 + lane);
+  const int nb = N.nb;
+  const bool fwd = lane < 16;
+  const int hl = lane & 15;
+  const int Lf = ((nb - 1) / (2 * T)) * T, Lb = nb - 1 - Lf;
+  const int ntf = Lf / T, ntb = (Lb + T - 1) / T;
+  const double Dl = __ldg(&N.DL[nb - 1]).x;
+  for (int k0 = 0; k0 < 224; k0 += 16) {
+    const double w = wid0 * ldexp(1.0, k0 + hl);
     const double mu = B.side > 0 ? (B.gu - sigma) + w : (B.gl - sigma) - w;
     Sturm st;
     sturm_init(st, mu);
+    if (!fwd) st.p = Dl - mu;
     bool ok = true;
     auto issue = [&](int t) {
-      const int row = t * T + lane;
-      if (lane < T && t < ntile && row < body) __pipeline_memcpy_async(&ring[t % RING][lane], &N.DL[row], sizeof(double2));
+      if (fwd) {
+        if (t < ntf) __pipeline_memcpy_async(&ring[t % RING][hl], &N.DL[t * T + hl], sizeof(double2));
+      } else {
+        const int row = nb - 2 - (t * T + hl);
+        if (t < ntb && row >= Lf) {
+          double2 *dst = &ring[t % RING][T + hl];
+          __pipeline_memcpy_async(&dst->x, &N.DL[row].y, sizeof(double));
+          __pipeline_memcpy_async(&dst->y, &N.DL[row].x, sizeof(double));
+        }
+      }
       __pipeline_commit();
     };
 #pragma unroll
     for (int k = 0; k < RING - 1; ++k) issue(k);
-    for (int t = 0; t < ntile; ++t) {
+    for (int t = 0; t < ntb; ++t) {
       __pipeline_wait_prior(RING - 2);
       __syncwarp();
-      const int rows = min(T, body - t * T);
+      const double2 *TT = ring[t % RING] + (fwd ? 0 : T);
+      const int rows = fwd ? (t < ntf ? T : 0) : min(T, Lb - t * T);
       if (rows == T) {
 #pragma unroll
         for (int k = 0; k < T; ++k) {
-          const double2 v = ring[t % RING][k];
+          const double2 v = TT[k];
           sturm_step(st, v.x, v.y, mu);
           if ((k & 7) == 7) ok &= sturm_rescale(st);
         }
       } else {
         for (int k = 0; k < rows; ++k) {
-          const double2 v = ring[t % RING][k];
+          const double2 v = TT[k];
           sturm_step(st, v.x, v.y, mu);
           if ((k & 7) == 7) ok &= sturm_rescale(st);
         }
@@ -460,10 +477,17 @@ __global__ void __launch_bounds__(32) k_root_interval_warp(const Node *nodes, co
       issue(t + RING - 1);
     }
     __pipeline_wait_prior(0);
-    sturm_last(st, __ldg(&N.DL[nb - 1]).x);
-    unsigned c = st.c;
-    if (!ok || !sturm_ok(st) || g_force_safe) c = negcount_qd_safe(N.DL, nb, mu);
-    const bool pass = B.side > 0 ? ((int)c >= nb) : ((int)c <= 0);
+    ok &= sturm_rescale(st);
+    ok &= sturm_ok(st);
+    ok &= __shfl_xor_sync(0xffffffffu, (int)ok, 16) != 0;
+    const double a = __shfl_xor_sync(0xffffffffu, st.p, 16);
+    const double b = __shfl_xor_sync(0xffffffffu, st.q, 16);
+    const unsigned cb = __shfl_xor_sync(0xffffffffu, st.c, 16);
+    const double X = fma(mu, st.q, st.p);
+    const double Ng = fma(X, b, a * st.q);
+    unsigned c = st.c + cb + ((Ng != 0.0) ? (((unsigned)(hi32(Ng) ^ hi32(st.q) ^ hi32(b))) >> 31) : 0u);
+    if (fwd && (!ok || g_force_safe)) c = negcount_qd_safe(N.DL, nb, mu);
+    const bool pass = fwd && (B.side > 0 ? ((int)c >= nb) : ((int)c <= 0));
     const unsigned bal = __ballot_sync(0xffffffffu, pass);
     if (bal) {
       const int first = __ffs(bal) - 1;

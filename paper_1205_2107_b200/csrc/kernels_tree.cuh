@@ -200,7 +200,7 @@ __global__ void k_root_chain(const double *__restrict__ ds, const double *__rest
 // e_{i-1}^2), every lane runs the same chain, lane k keeps row k's t_i and
 // rescale, and each tile's values are stored with coalesced writes.  The
 // arithmetic is that of k_root_chain (same operations, same order).
-constexpr int kRCT = 16, kRCRing = 6;
+constexpr int kRCT = 32, kRCRing = 6;  // 32-row tiles: one definiteness check per 32 rows
 __global__ void __launch_bounds__(32) k_root_chain_warp(const double *__restrict__ ds,
                                                         const double *__restrict__ es2, Block *blocks,
                                                         int nblocks, double tnrm_scaled, double *tbuf,
@@ -214,10 +214,10 @@ __global__ void __launch_bounds__(32) k_root_chain_warp(const double *__restrict
   const double *er = es2 + B.row0;  // er[i-1] = e_{i-1}^2 of the block
   const int nb = B.nb, ntile = (nb + kRCT - 1) / kRCT;
   auto issue = [&](int t) {
-    const int slot = t % kRCRing, k = lane & (kRCT - 1), row = t * kRCT + k;
+    const int slot = t % kRCRing, k = lane, row = t * kRCT + k;
     if (t < ntile && row < nb) {
-      if (lane < kRCT) __pipeline_memcpy_async(&rD[slot][k], &dr[row], sizeof(double));
-      else if (row > 0) __pipeline_memcpy_async(&rE[slot][k], &er[row - 1], sizeof(double));
+      __pipeline_memcpy_async(&rD[slot][k], &dr[row], sizeof(double));
+      if (row > 0) __pipeline_memcpy_async(&rE[slot][k], &er[row - 1], sizeof(double));
     }
     __pipeline_commit();
   };
@@ -252,11 +252,14 @@ __global__ void __launch_bounds__(32) k_root_chain_warp(const double *__restrict
         if (lane == k) { kt = tt; ks = sh; }
       };
       if (rows == kRCT) {
-        double dv[kRCT], bv[kRCT];  // the tile's rows in registers before the chain
 #pragma unroll
-        for (int k = 0; k < kRCT; ++k) { dv[k] = rD[slot][k]; bv[k] = (r0 + k > 0) ? rE[slot][k] : 0.0; }
+        for (int h = 0; h < kRCT; h += 8) {
+          double dv[8], bv[8];  // 8 rows in registers before their chain steps
 #pragma unroll
-        for (int k = 0; k < kRCT; ++k) row(k, dv[k], bv[k]);
+          for (int k = 0; k < 8; ++k) { dv[k] = rD[slot][h + k]; bv[k] = (r0 + h + k > 0) ? rE[slot][h + k] : 0.0; }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) row(h + k, dv[k], bv[k]);
+        }
       } else {
         for (int k = 0; k < rows; ++k) row(k, rD[slot][k], (r0 + k > 0) ? rE[slot][k] : 0.0);
       }

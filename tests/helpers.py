@@ -101,3 +101,46 @@ def vec_diff_signfree(za, zb):
     a = np.max(np.abs(za - zb), axis=0)
     b = np.max(np.abs(za + zb), axis=0)
     return np.minimum(a, b)
+
+
+def subspace_runs(w_ref, r_a, r_b, ok, full_range=True):
+    """The eigenpairs that are NOT individually comparable (dk_comparable
+    false: inside clusters or degenerate groups, where any orthonormal basis
+    of the invariant subspace is correct) grouped into maximal runs of
+    consecutive indices.  A run's invariant subspace is unique when it is
+    well separated from the other eigenvalues: by Davis-Kahan, sin(theta)
+    between the subspace a basis spans and the exact one is at most
+    ||R||_F / gap_out, so two bases with (||R_a||_F + ||R_b||_F) / gap_out <=
+    1e-10 must span the same subspace to that accuracy.  Returns the
+    half-open index ranges (a, b) of such runs.  For an index or value
+    subset (full_range=False) runs touching the ends are skipped: their
+    nearest outside eigenvalue is not in the list."""
+    w = np.asarray(w_ref, float)
+    k = len(w)
+    out = []
+    i = 0
+    while i < k:
+        if ok[i]:
+            i += 1
+            continue
+        j = i
+        while j < k and not ok[j]:
+            j += 1
+        a, b = i, j
+        i = j
+        if not full_range and (a == 0 or b == k):
+            continue
+        gl = w[a] - w[a - 1] if a > 0 else np.inf
+        gr = w[b] - w[b - 1] if b < k else np.inf
+        gap = min(gl, gr)
+        R = np.sqrt(np.sum(r_a[a:b] ** 2)) + np.sqrt(np.sum(r_b[a:b] ** 2))
+        if gap == np.inf or R / gap <= 1e-10:
+            out.append((a, b))
+    return out
+
+
+def subspace_diff(Za, Zb):
+    """max over the columns of Za of ||z - Zb Zb^T z||_2: how far Za's columns
+    lie from the span of Zb's (orthonormal) columns."""
+    P = Za - Zb @ (Zb.T @ Za)
+    return float(np.max(np.linalg.norm(P, axis=0))) if Za.shape[1] else 0.0

@@ -147,11 +147,11 @@ def test_forced_fallback_paths(torch_cuda, P, oracle_mod, monkeypatch, env, stat
     monkeypatch.delenv(env)
     assert st[stat] > 0, st
     wo, Zo = oracle_mod.stemr(d, e, **kw)
-    compare(d, e, w, Z, wo, Zo)
+    compare(d, e, w, Z, wo, Zo, full_range=not kw)
     # switching back off restores the default path (the flag is per call)
     w2, Z2 = gpu_solve(P, torch_cuda, d, e, **kw)
     assert P.last_stats()[stat] == 0
-    compare(d, e, w2, Z2, wo, Zo)
+    compare(d, e, w2, Z2, wo, Zo, full_range=not kw)
 
 
 @pytest.mark.parametrize("k", [1000, -960, 37])
@@ -243,7 +243,7 @@ def test_value_endpoints_on_eigenvalues(torch_cuda, P, oracle_mod, vl, vu):
     w, Z = gpu_solve(P, torch_cuda, d, e, vl=vl, vu=vu)
     wo, Zo = oracle_mod.stemr(d, e, vl=vl, vu=vu)
     assert len(w) == len(wo), (len(w), len(wo), w, wo)
-    compare(d, e, w, Z, wo, Zo)
+    compare(d, e, w, Z, wo, Zo, full_range=False)
     lam = 2.0 * np.arange(1, n + 1) - n - 1
     k0 = int(np.searchsorted(lam, w[0] - 0.5)) if len(w) else 0
     assert np.max(np.abs(w - lam[k0:k0 + len(w)])) <= 4 * n * EPS * tnorm1(d, e)

@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 from helpers import (EPS, check_accuracy, dk_comparable, residuals, sturm_numpy, sturm_placement,
-                     tnorm1, vec_diff_signfree)
+                     subspace_diff, subspace_runs, tnorm1, vec_diff_signfree)
 from paper_1205_2107_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -46,7 +46,13 @@ def gpu_solve(P, torch, d, e, **kw):
     return w.cpu().numpy(), (Z.cpu().numpy() if Z is not None else None)
 
 
-def compare(d, e, w, Z, wo, Zo, *, vec_min_frac=0.0):
+def compare(d, e, w, Z, wo, Zo, *, vec_min_frac=0.0, full_range=True):
+    """GPU (w, Z) against the oracle's (wo, Zo): eigenvalues within 4 n eps
+    ||T||_1; residual and orthogonality within the contract; every vector the
+    Davis-Kahan rule makes unique (reading 18) equal to the oracle's to 1e-9
+    (sign-free); and every run of the others (clusters, degenerate groups)
+    whose invariant subspace is unique (helpers.subspace_runs) spanned by
+    both sides to 1e-9.  Returns (individually compared, in compared runs)."""
     n = len(d)
     tn = tnorm1(d, e)
     assert len(w) == len(wo)
@@ -64,6 +70,11 @@ def compare(d, e, w, Z, wo, Zo, *, vec_min_frac=0.0):
     if ok.any():
         assert np.max(vec_diff_signfree(Z[:, ok], Zo[:, ok])) <= 1e-9
     assert ok.mean() >= vec_min_frac
+    runs = subspace_runs(wo, rg, ro, ok, full_range=full_range)
+    for a, b in runs:
+        assert subspace_diff(Z[:, a:b], Zo[:, a:b]) <= 1e-9, (a, b)
+        assert subspace_diff(Zo[:, a:b], Z[:, a:b]) <= 1e-9, (a, b)
+    return int(ok.sum()), int(sum(b - a for a, b in runs))
 
 
 SMALL = {
@@ -95,7 +106,9 @@ def test_parity_small(torch_cuda, P, oracle_mod, name):
     d, e = mk()
     w, Z = gpu_solve(P, torch_cuda, d, e, **kw)
     wo, Zo = oracle_mod.stemr(d, e, **kw)
-    compare(d, e, w, Z, wo, Zo)
+    n_ind, n_sub = compare(d, e, w, Z, wo, Zo, full_range=not kw)
+    if name.startswith("glued"):
+        assert n_sub >= len(w) // 2, (n_ind, n_sub)  # the degenerate groups went through the subspace test
 
 
 @pytest.mark.parametrize("name", ["random_400_s0", "glued_10", "random_1000_idx", "random_600_value"])
@@ -122,7 +135,7 @@ def test_split_blocks(torch_cuda, P, oracle_mod, kw):
     d, e = split_matrix()
     w, Z = gpu_solve(P, torch_cuda, d, e, **kw)
     wo, Zo = oracle_mod.stemr(d, e, **kw)
-    compare(d, e, w, Z, wo, Zo)
+    compare(d, e, w, Z, wo, Zo, full_range=not kw)
     # rows outside a column's block are exactly zero
     assert np.all(np.count_nonzero(Z, axis=0) <= 40)
 
@@ -295,6 +308,9 @@ def oracle_windows(oracle_mod, d, e, w, Z, windows, base=1):
         ok = dk_comparable(wo, rg, ro)
         if ok.any():
             assert np.max(vec_diff_signfree(Z[:, a:b][:, ok], Zo[:, ok])) <= 1e-9
+        # runs of cluster members inside the window: the unique subspaces
+        for c0, c1 in subspace_runs(wo, rg, ro, ok, full_range=False):
+            assert subspace_diff(Z[:, a + c0:a + c1], Zo[:, c0:c1]) <= 1e-9, (il, c0, c1)
 
 
 def test_config1_one_two_one_2000(torch_cuda, P, oracle_mod):
@@ -348,6 +364,15 @@ def test_config3_glued_wilkinson_21000(torch_cuda, P, oracle_mod):
     assert np.max(np.abs(w - np.repeat(mu, 1000))) <= 1e-8 + 4 * n * EPS * tnorm1(d, e)
     Z = Zt.cpu().numpy()
     oracle_windows(oracle_mod, d, e, w, Z, [(1, 40), (20961, 21000)])
+    # the lowest degenerate group (1000 copies of W21+'s smallest eigenvalue,
+    # ~1.2 from the next group): its invariant subspace is unique, so the
+    # GPU's 1000 columns and the oracle's span the same space
+    wo, Zo = oracle_mod.stemr(d, e, il=1, iu=1000)
+    rg, ro = residuals(d, e, w[:1000], Z[:, :1000]), residuals(d, e, wo, Zo)
+    gap = w[1000] - w[999]
+    assert (np.sqrt(np.sum(rg ** 2)) + np.sqrt(np.sum(ro ** 2))) / gap <= 1e-10
+    assert subspace_diff(Z[:, :1000], Zo) <= 1e-9
+    assert subspace_diff(Zo, Z[:, :1000]) <= 1e-9
 
 
 @pytest.mark.parametrize("subset", [True, False])

@@ -354,13 +354,64 @@ __global__ void __launch_bounds__(POST ? 128 : 96, ADJ ? 2 : POST ? MRRR_CS2P_MI
       }
     }
   };
+  // POST's scan: each lane multiplies 8 consecutive ratios serially, one
+  // warp scan combines the 32 lane products (5 shuffle steps per 256 rows
+  // instead of 40), and each lane applies its prefix to its 8 values.  The
+  // same (mantissa, exponent) products in another association order: |z| may
+  // differ from k_child_step2's in the last bits (a weight of the growth
+  // test, reading 27; GPU test test_schedule_invariance compares the
+  // solves)
+  auto scan_from_lanes = [&](int side, int dirn, int r) {
+    const double *sR = pr[side] + 2 * zs, *sG = pr[side] + 3 * zs;
+    double *z = zz[side];
+    const bool up = dirn == 0;
+    const int m = up ? r : nb - 1 - r;
+    const double *src = up ? sR + (r - 1) : sG + r;
+    const int dir = up ? -1 : 1;
+    double *dst = up ? z + (r - 1) : z + (r + 1);
+    constexpr int kL = 8;
+    double cm = 1.0, ce = 0.0;
+    for (int b0 = 0; b0 < m; b0 += 32 * kL) {
+      const int j0 = b0 + lane * kL;
+      double xv[kL];
+#pragma unroll
+      for (int u = 0; u < kL; ++u) xv[u] = j0 + u < m ? src[dir * (j0 + u)] : 1.0;
+      double mm[kL], ee[kL];
+      double pm = 1.0, pe = 0.0;
+#pragma unroll
+      for (int u = 0; u < kL; ++u) {
+        double im, ie;
+        split(xv[u], im, ie);
+        if (j0 + u >= m) { im = 1.0; ie = 0.0; }
+        mul(pm, pe, im, ie);
+        mm[u] = pm; ee[u] = pe;
+      }
+      // inclusive scan of the lane products, then the exclusive prefix
+      double sm = pm, se = pe;
+      for (int o = 1; o < 32; o <<= 1) {
+        const double ym = __shfl_up_sync(0xffffffffu, sm, o), ye = __shfl_up_sync(0xffffffffu, se, o);
+        if (lane >= o) mul(sm, se, ym, ye);
+      }
+      double xm = __shfl_up_sync(0xffffffffu, sm, 1), xe = __shfl_up_sync(0xffffffffu, se, 1);
+      if (lane == 0) { xm = 1.0; xe = 0.0; }
+      mul(xm, xe, cm, ce);
+#pragma unroll
+      for (int u = 0; u < kL; ++u) {
+        double om = mm[u], oe = ee[u];
+        mul(om, oe, xm, xe);
+        if (j0 + u < m) dst[dir * (j0 + u)] = to_double(om, oe);
+      }
+      const double tm = __shfl_sync(0xffffffffu, sm, 31), te = __shfl_sync(0xffffffffu, se, 31);
+      mul(cm, ce, tm, te);
+    }
+  };
   if (POST) {
     if (wid < 2) {
       const int r = twist_of(wid);
       if (lane == 0) S.rr[wid] = r;
     }
     __syncthreads();
-    scan_from(wid & 1, wid >> 1, S.rr[wid & 1]);
+    scan_from_lanes(wid & 1, wid >> 1, S.rr[wid & 1]);
   } else {
     for (int side = wid; side < NPROBE; side += 3) {
       if (side >= 2 && !has_int) break;

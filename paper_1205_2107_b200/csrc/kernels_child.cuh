@@ -437,29 +437,41 @@ __global__ void __launch_bounds__(32 * (kCSWarps + 4 * ADJ), ADJ ? 1 : 3) k_chil
     const int dir = up ? -1 : 1;
     double *dst = up ? z + (r - 1) : z + (r + 1);
     double cm = 1.0, ce = 0.0;  // carry: product of all earlier blocks
-    constexpr int kBlk = 8;
-    for (int base = 0; base < m; base += 32 * kBlk) {
-      double xv[kBlk];
+    // each lane multiplies 8 consecutive ratios serially, one warp scan
+    // combines the 32 lane products, each lane applies its prefix (5 shuffle
+    // steps per 256 rows; the order k_child_step2<0, true> uses too)
+    constexpr int kL = 8;
+    for (int b0 = 0; b0 < m; b0 += 32 * kL) {
+      const int j0 = b0 + lane * kL;
+      double xv[kL];
 #pragma unroll
-      for (int u = 0; u < kBlk; ++u) {
-        const int j = base + u * 32 + lane;
-        xv[u] = j < m ? src[dir * j] : 1.0;
-      }
+      for (int u = 0; u < kL; ++u) xv[u] = j0 + u < m ? src[dir * (j0 + u)] : 1.0;
+      double mm[kL], ee[kL];
+      double pm = 1.0, pe = 0.0;
 #pragma unroll
-      for (int u = 0; u < kBlk; ++u) {
-        const int j = base + u * 32 + lane;
+      for (int u = 0; u < kL; ++u) {
         double im, ie;
         split(xv[u], im, ie);
-        if (j >= m) { im = 1.0; ie = 0.0; }
-        for (int o = 1; o < 32; o <<= 1) {  // inclusive scan over the 32 lanes
-          const double ym = __shfl_up_sync(0xffffffffu, im, o), ye = __shfl_up_sync(0xffffffffu, ie, o);
-          if (lane >= o) mul(im, ie, ym, ye);
-        }
-        mul(im, ie, cm, ce);
-        if (j < m) dst[dir * j] = to_double(im, ie);
-        cm = __shfl_sync(0xffffffffu, im, 31);
-        ce = __shfl_sync(0xffffffffu, ie, 31);
+        if (j0 + u >= m) { im = 1.0; ie = 0.0; }
+        mul(pm, pe, im, ie);
+        mm[u] = pm; ee[u] = pe;
       }
+      double sm = pm, se = pe;
+      for (int o = 1; o < 32; o <<= 1) {  // inclusive scan over the 32 lane products
+        const double ym = __shfl_up_sync(0xffffffffu, sm, o), ye = __shfl_up_sync(0xffffffffu, se, o);
+        if (lane >= o) mul(sm, se, ym, ye);
+      }
+      double xm = __shfl_up_sync(0xffffffffu, sm, 1), xe = __shfl_up_sync(0xffffffffu, se, 1);
+      if (lane == 0) { xm = 1.0; xe = 0.0; }
+      mul(xm, xe, cm, ce);
+#pragma unroll
+      for (int u = 0; u < kL; ++u) {
+        double om = mm[u], oe = ee[u];
+        mul(om, oe, xm, xe);
+        if (j0 + u < m) dst[dir * (j0 + u)] = to_double(om, oe);
+      }
+      const double tm = __shfl_sync(0xffffffffu, sm, 31), te = __shfl_sync(0xffffffffu, se, 31);
+      mul(cm, ce, tm, te);
     }
   }
   __syncthreads();

@@ -277,7 +277,7 @@ __device__ __forceinline__ double cs_absdplus_fast(const double *TP, const doubl
 // candidate, and two more probes (four more warps) at the members next to its
 // shift, whose weighted growth the interior child must also pass.
 template <int ADJ>
-__global__ void __launch_bounds__(32 * (kCSWarps + 4 * ADJ), ADJ ? 1 : 3) k_child_step(ChildArgs A) {
+__global__ void __launch_bounds__(32 * (kCSWarps + 4 * ADJ), ADJ ? 1 : 2) k_child_step(ChildArgs A) {
   constexpr int NW = kCSWarps + 4 * ADJ, NP = 2 + 2 * ADJ, ROWS = ADJ ? kCSRowsAdj : kCSRows;
   __shared__ ChildSmem S;
   if (A.c0 + (int)blockIdx.x >= A.ncl) return;

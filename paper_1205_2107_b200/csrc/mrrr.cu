@@ -1244,7 +1244,7 @@ int solve(Problem &P, int64_t *m_out) {
   const int rw_m_root = std::max(1, std::min(4, env_int("MRRR_RW_ROOT_M", 2)));
   // reading 31: tree members stop refining at 2^-early_bits once their
   // classification is decided (MRRR_EARLY_BITS; 0 = off, refine all to rtol_class)
-  const int early_bits = env_int("MRRR_EARLY_BITS", 12);
+  const int early_bits = env_int("MRRR_EARLY_BITS", 10);
   // twisted (split) counts in the refinement sweeps (reading 32): 1 = tree
   // levels, 2 = tree and root, 0 = whole stationary sweeps everywhere
   const int split_env = env_int("MRRR_SPLIT", 2);

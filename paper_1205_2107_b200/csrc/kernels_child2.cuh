@@ -40,9 +40,9 @@ struct Child2Smem {
   ChainRing ring[3];
   double stF[kCT][kCF][3];  // warp F staging: (p, q, t) per row and chain lane
   double stB[kCT][kCB][3];  // warp B staging: (b, u, a) per row and chain lane
-  double red[3][3 * kNC + 4];
-  unsigned okw[3];
-  double am2[3][2];         // per warp: the denominators of the ADJ weights
+  double red[4][3 * kNC + 4];
+  unsigned okw[4];
+  double am2[4][2];         // per warp: the denominators of the ADJ weights
   double sig[kNC];
   int has_int, jint;
   double sig_int;
@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(POST ? 128 : 96, ADJ ? 2 : POST ? MRRR_CS2P_MI
 #pragma unroll
   for (int k = 0; k < kNC; ++k) { g[k] = 0.0; nl[k] = 0.0; nr[k] = 0.0; }
 #pragma unroll 2
-  for (int i = tid; i < nb && wid < 3; i += 96) {  // (POST: warp 3 sits out -- the same sums as 96 threads)
+  constexpr int NT = POST ? 128 : 96;  // POST: all four warps (the sums in another order: ulps of a weight)
+  for (int i = tid; i < nb; i += NT) {
     const double a = zl[i], b = zr[i];
     const double a2 = a * a, b2 = b * b;
     dnl += a2; dnr += b2;
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(POST ? 128 : 96, ADJ ? 2 : POST ? MRRR_CS2P_MI
       dnb += __shfl_xor_sync(0xffffffffu, dnb, o);
     }
   }
-  if (lane == 0 && wid < 3) {
+  if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < kNC; ++k) {
       S.red[wid][k] = g[k]; S.red[wid][kNC + k] = nl[k]; S.red[wid][2 * kNC + k] = nr[k];
@@ -488,7 +489,7 @@ __global__ void __launch_bounds__(POST ? 128 : 96, ADJ ? 2 : POST ? MRRR_CS2P_MI
     double G[kNC], NL[kNC], NR[kNC], DNL = 0.0, DNR = 0.0, NA = 0.0, NB = 0.0, DNA = 0.0, DNB = 0.0;
     unsigned ok = (1u << kNC) - 1u;
     for (int k = 0; k < kNC; ++k) { G[k] = 0.0; NL[k] = 0.0; NR[k] = 0.0; }
-    for (int w = 0; w < 3; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
       for (int k = 0; k < kNC; ++k) {
         G[k] = fmax(G[k], S.red[w][k]);
         NL[k] += S.red[w][kNC + k];

@@ -33,7 +33,10 @@
 namespace mrrr {
 
 constexpr int kCT = 16;     // rows per tile
-constexpr int kCRing = 6;   // tiles in flight per warp
+#ifndef MRRR_CRING
+#define MRRR_CRING 6
+#endif
+constexpr int kCRing = MRRR_CRING;  // tiles in flight per warp
 constexpr int kCSWarps = 5; // 4 probe chains + the candidate warp
 constexpr int kNC = 7;      // candidates: 6 at the cluster ends (readings 8, 9) + the interior one (reading 30)
 constexpr int kCSRows = kNC + 11; // scratch rows per cluster: t of the candidates, 4 per probe, |z| of 2, q every 8 rows

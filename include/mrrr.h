@@ -76,10 +76,10 @@ typedef struct {
                           before the RQC; 0 = none (default; reading 10) */
   int rqc_max;         /* twisted factorizations of the RQC before the
                           bisection fallback; default 10 (reading 10) */
-  int shift_strategy;  /* 0 (default): child shifts at the cluster ends only
-                          (readings 8, 9); 1: an interior shift first for
-                          clusters of >= 2000 members -- shallower trees, less
-                          orthogonality margin (reading 30) */
+  int shift_strategy;  /* 1 (default): an interior shift first for clusters of
+                          >= 2000 members -- shallower trees (DESIGN.md
+                          reading 30); 0: child shifts at the cluster ends
+                          only (readings 8, 9) */
   double scratch_gb;   /* cap (GB) of each of the two large scratch areas: the
                           vector checkpoints (4 n B per eigenvector in flight)
                           and the cluster-step scratch (144 n B per cluster of

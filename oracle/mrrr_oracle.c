@@ -20,6 +20,9 @@
 #ifndef ORACLE_INTERIOR_PROBES
 #define ORACLE_INTERIOR_PROBES 4 /* reading 30: end members and the two next to the shift */
 #endif
+#ifndef ORACLE_INTERIOR_WG
+#define ORACLE_INTERIOR_WG 4.0 /* reading 30: the interior child's weighted-growth bound (x spdiam) */
+#endif
 
 void oracle_default_opts(oracle_opts_t *o) {
   o->tol_relgap = 1e-3;                /* P:L1069-1072 footnote */
@@ -29,7 +32,7 @@ void oracle_default_opts(oracle_opts_t *o) {
   o->seed = 0x1205210700000000ULL;     /* SURVEY §8(b) default seed */
   o->rtol_vec = 0.0;                   /* reading 10 */
   o->rqc_max = 10;                     /* reading 10 */
-  o->shift_strategy = 0;               /* reading 30 (option 1) */
+  o->shift_strategy = 1;               /* reading 30 (0: end shifts only) */
 }
 
 /* ------------------------------------------------------------------------ */
@@ -557,7 +560,7 @@ static void cluster(ctx_t *c, const rrr_t *R, int64_t s, int64_t t, int depth) {
             twisted_ws(nb, R->D, R->L, R->LD, R->LLD, &lam, R->pivmin, &c->ws, zL, &r, &gg, &nc, &rs);
             wg = fmax(wg, weighted_growth(nb, zL, DpA));
           }
-          take = wg <= 64.0 * spd;
+          take = wg <= ORACLE_INTERIOR_WG * spd;
         }
         if (take) {
           best = 6;

@@ -31,8 +31,8 @@ typedef struct {
   uint64_t seed;      /* perturbation seed */
   double rtol_vec;    /* singleton bracket refinement before the RQC; 0 = none (reading 10) */
   int rqc_max;        /* RQC factorizations before the bisection fallback; 10 (reading 10) */
-  int shift_strategy; /* 0 (default): shifts at the cluster ends only (readings 8, 9);
-                         1: an interior candidate first for large clusters (reading 30) */
+  int shift_strategy; /* 1 (default): an interior candidate first for large clusters (reading 30);
+                         0: shifts at the cluster ends only (readings 8, 9) */
 } oracle_opts_t;
 
 typedef struct {

@@ -90,7 +90,7 @@ void dump(const char *name, const T *dptr, size_t count, cudaStream_t s) {
 // destructors then ignore the errors.)
 constexpr int kSide = 4;  // side streams for the vector batches
 struct StreamSet {
-  cudaStream_t st[64][kSide + 2] = {};  // per device: kSide side streams, the copy stream, the solve stream
+  cudaStream_t st[64][kSide + 3] = {};  // per device: kSide side streams, the copy stream, the solve stream, the tree's second stream
   ~StreamSet() {
     for (auto &dv : st)
       for (cudaStream_t &x : dv)
@@ -849,6 +849,20 @@ cudaStream_t hp_stream() {
   return x;
 }
 
+// A second high-priority stream for the tree: the interior-candidate step
+// of the big clusters (reading 30) runs beside the other clusters' step.
+cudaStream_t hp_stream2() {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  cudaStream_t &x = g_streams.st[d & 63][kSide + 2];
+  if (!x) {
+    int lo_pr = 0, hi_pr = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
+    CK(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, hi_pr));
+  }
+  return x;
+}
+
 // e: shard planner.  cuts[0..nranks] start as the static division (rank r
 // owns columns [cuts[r], cuts[r+1])); each inner cut moves to the nearest
 // column j with free_cut[j] != 0 (a cluster boundary between columns j-1
@@ -1256,7 +1270,7 @@ int solve(Problem &P, int64_t *m_out) {
   const int rw_end = env_int("MRRR_RW_END", 0);
   // reading 30: weighted-growth bound of the interior candidate (x spdiam);
   // MRRR_INT_WG overrides (diagnostic)
-  const double int_wg = getenv("MRRR_INT_WG") ? atof(getenv("MRRR_INT_WG")) : 64.0;
+  const double int_wg = getenv("MRRR_INT_WG") ? atof(getenv("MRRR_INT_WG")) : 4.0;
   // the cluster step: one warp per chain (k_child_step: the shortest chain
   // latency, for levels of at most kChildV1Max clusters) or the chains packed
   // into the lanes of three warps (k_child_step2: fewer instructions, for the
@@ -1909,6 +1923,11 @@ int solve(Problem &P, int64_t *m_out) {
       // the others through the five-warp step, in groups that fit the scratch
       const bool child_v1 = child_v1_env >= 0 ? child_v1_env != 0 : nown <= kChildV1Max;
       const bool child_v3 = !child_v1 && child_v3_env != 0;
+      cudaStream_t big_stream = nullptr;
+      struct BigJoin {  // the second stream rejoins the solve stream on every exit
+        cudaStream_t main, b;
+        ~BigJoin() { if (b) join_streams_nothrow(main, b); }
+      } bjoin{s, nullptr};
       std::vector<int> small_cl, big_cl;
       for (int i = 0; i < nown; ++i)
         (P.o.shift_strategy == 1 && ocl_s1[i] - ocl_s0[i] >= 2000 ? big_cl : small_cl).push_back(i);
@@ -1930,8 +1949,15 @@ int solve(Problem &P, int64_t *m_out) {
         int *dbig = lv.alloc<int>(nbig);
         h2d(dbig, big_cl.data(), nbig, s);
         double *scr = lv.alloc<double>((size_t)kCSRowsAdj * nbig * zs_cs);
-        if (child_v1) k_child_step<1><<<nbig, 32 * kCSWarpsAdj, 0, s>>>(child_args(dbig, 0, nbig, scr));
-        else k_child_step2<1><<<nbig, 96, 0, s>>>(child_args(dbig, 0, nbig, scr));
+        // on a second high-priority stream, beside the other clusters' step
+        // (forked after the uploads above, joined before k_child_nodes)
+        big_stream = hp_stream2();
+        bjoin.b = big_stream;
+        cudaEvent_t fork = ev_sync();
+        CK(cudaEventRecord(fork, s));
+        CK(cudaStreamWaitEvent(big_stream, fork, 0));
+        if (child_v1) k_child_step<1><<<nbig, 32 * kCSWarpsAdj, 0, big_stream>>>(child_args(dbig, 0, nbig, scr));
+        else k_child_step2<1><<<nbig, 96, 0, big_stream>>>(child_args(dbig, 0, nbig, scr));
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
       }
@@ -1960,6 +1986,12 @@ int solve(Problem &P, int64_t *m_out) {
         }
         CK(cudaGetLastError());
         g_stats.kernel_launches++;
+      }
+      if (big_stream) {  // join the big clusters' step
+        cudaEvent_t join = ev_sync();
+        CK(cudaEventRecord(join, big_stream));
+        CK(cudaStreamWaitEvent(s, join, 0));
+        bjoin.b = nullptr;
       }
       tr.fine(s, "  child step");
       tl_mark("L" + std::to_string(level) + " child step done");
@@ -2303,7 +2335,7 @@ void mrrr_default_opts(mrrr_opts_t *o) {
   o->grid_factor = 4;
   o->rtol_vec = 0.0;
   o->rqc_max = 10;
-  o->shift_strategy = 0;  // DESIGN.md reading 30: the interior shift is an option
+  o->shift_strategy = 1;  // DESIGN.md reading 30: interior shift first for clusters of >= 2000 members
   o->scratch_gb = 16.0;
 }
 

@@ -68,9 +68,9 @@ def test_interior_shift_strategy(oracle_mod):
     than the end shifts' chain."""
     n = 4000
     d, e = W.clement(n)
-    w0, Z0, st0 = oracle_mod.stemr(d, e, return_stats=True)  # the default: end shifts
-    w1, Z1, st1 = oracle_mod.stemr(d, e, opts=oracle_mod.default_opts(shift_strategy=1), return_stats=True)
-    assert oracle_mod.default_opts().shift_strategy == 0
+    w0, Z0, st0 = oracle_mod.stemr(d, e, opts=oracle_mod.default_opts(shift_strategy=0), return_stats=True)
+    w1, Z1, st1 = oracle_mod.stemr(d, e, return_stats=True)  # the default: interior first
+    assert oracle_mod.default_opts().shift_strategy == 1
     lam = 2.0 * np.arange(1, n + 1) - n - 1
     tn = tnorm1(d, e)
     assert np.max(np.abs(w1 - lam)) <= 4 * n * EPS * tn

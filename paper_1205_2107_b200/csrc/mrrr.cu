@@ -88,7 +88,8 @@ void dump(const char *name, const T *dptr, size_t count, cudaStream_t s) {
 // nothing; mrrr_trim_workspace() releases the memory of the calling thread
 // earlier.  (At process exit the CUDA context may already be gone; the
 // destructors then ignore the errors.)
-constexpr int kSide = 4;  // side streams for the vector batches
+constexpr int kSide = 8;  // side streams for the vector batches (at most; MRRR_NSIDE of them are used)
+constexpr int kNSideDefault = 4;
 struct StreamSet {
   cudaStream_t st[64][kSide + 3] = {};  // per device: kSide side streams, the copy stream, the solve stream, the tree's second stream
   ~StreamSet() {
@@ -1566,8 +1567,9 @@ int solve(Problem &P, int64_t *m_out) {
   // pieces of (this rank's tasks)/4 (n = 20000: 69.9 -> 67.8 ms against /8),
   // capped so that the checkpoints (64 B per 16-row segment and task) stay
   // within scratch_bytes (16 GB by default; n = 1e5: pieces of ~nslots/10)
-  const int piece_div = std::max(1, env_int("MRRR_PIECE_DIV", kSide));  // diagnostic knob
-  const int64_t ck_mem_cap = (int64_t)(ck_bytes / (64.0 * kSide * ((nbmax + kSeg - 1) / kSeg)));
+  const int nside = std::min(kSide, std::max(1, env_int("MRRR_NSIDE", kNSideDefault)));
+  const int piece_div = std::max(1, env_int("MRRR_PIECE_DIV", 4));  // diagnostic knob
+  const int64_t ck_mem_cap = (int64_t)(ck_bytes / (64.0 * nside * ((nbmax + kSeg - 1) / kSeg)));
   const int64_t task_basis = dist ? std::min<int64_t>(nslots, wcap + 2) : nslots;
   const int64_t ck_cap =
       std::max<int64_t>(256, std::min<int64_t>((task_basis + piece_div - 1) / piece_div, ck_mem_cap)) + 32;
@@ -1700,16 +1702,49 @@ int solve(Problem &P, int64_t *m_out) {
   // (k_wvectors_psplit); MRRR_VEC_PSPLIT=0: k_wvectors_pair (diagnostic)
   const int vec_psplit = env_int("MRRR_VEC_PSPLIT", 1);
   const int vec_pack = env_int("MRRR_VEC_PACK", 1) ? kMaxSeg : 1;
-  const int tree_side = std::min(kSide, std::max(1, env_int("MRRR_TREE_SIDE", kSide)));
+  const int tree_side = std::min(nside, std::max(1, env_int("MRRR_TREE_SIDE", nside)));
+  // Which side stream takes the next piece: the first idle one in
+  // round-robin order (its last piece's end event has completed), else the
+  // one whose last piece was launched first.  Together with pieces of equal
+  // size per flush (below) this keeps a flush's pieces off each other's
+  // streams and puts them behind the pieces that started earliest.  Measured
+  // (random n = 20000, profiles/r02/setE): round robin with a full-size +
+  // remainder split 35.6 ms (a level-3 piece queued behind the longest
+  // level-2 piece, 6.8 ms vector tail); equal pieces 33.9 ms; the stream
+  // with the fewest queued tasks 37.1 ms (it put the two pieces of one flush
+  // on one stream).  The choice only moves pieces between streams: results
+  // are the same on any stream (test_schedule_invariance).
+  int side_last[kSide];
+  for (int k = 0; k < kSide; ++k) side_last[k] = -1;
+  auto pick_side = [&](int ns) {
+    if (env_int("MRRR_SIDE_RR", 0)) return nbatch % ns;  // diagnostic: round robin
+    for (int q = 0; q < ns; ++q) {
+      const int k = (nbatch + q) % ns;
+      if (side_last[k] < 0) return k;
+      const cudaError_t st = cudaEventQuery(piece_done[side_last[k]]);
+      if (st == cudaSuccess) return k;
+      if (st != cudaErrorNotReady) throw CudaError{st};
+    }
+    int best = 0;
+    for (int k = 1; k < ns; ++k)
+      if (side_last[k] < side_last[best]) best = k;
+    return best;
+  };
   auto flush_vectors = [&](int tree_left) {
+    // a flush's tasks in pieces of equal size (<= ck_cap - 32 each): with
+    // full pieces plus a remainder the remainder piece ended ~4 ms before
+    // the full ones it was launched with
+    const size_t nflush = tasks.size() - vec_done, pmax = (size_t)(ck_cap - 32);
+    const size_t npiece = (nflush + pmax - 1) / pmax;
+    const size_t pchunk = npiece > 0 ? (nflush + npiece - 1) / npiece : pmax;
     for (size_t t0 = vec_done; t0 < tasks.size();) {
-      const size_t t1 = std::min<size_t>(tasks.size(), t0 + (size_t)(ck_cap - 32));
+      const size_t t1 = std::min<size_t>(tasks.size(), t0 + pchunk);
       const int nbt = (int)(t1 - t0);
       std::vector<VecTask> bt(tasks.begin() + t0, tasks.begin() + t1);
       VecTask *dtb = ar.alloc<VecTask>(nbt);
       // side streams: tree_side of them while the tree runs (fewer vector
       // warps next to its kernels), all kSide for the last flush
-      const int sk = tree_left > 0 ? nbatch % tree_side : nbatch % kSide;
+      const int sk = pick_side(tree_left > 0 ? tree_side : nside);
       if (!ck_f[sk]) {
         ck_f[sk] = ar.alloc<FwdCk>((size_t)nseg_v * ck_cap);
         ck_b[sk] = ar.alloc<BwdCk>((size_t)nseg_v * ck_cap);
@@ -1785,6 +1820,7 @@ int solve(Problem &P, int64_t *m_out) {
           CK(cudaMemcpyAsync((void *)pfc, fail_count, sizeof(int), cudaMemcpyDeviceToHost, s2));
         }
         const int pc = (int)piece_done.size();
+        side_last[sk] = pc;
         piece_done.push_back(eb);
         piece_fail.push_back(pfc);
         piece_ok.push_back(-1);

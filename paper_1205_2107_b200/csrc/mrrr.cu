@@ -88,8 +88,22 @@ void dump(const char *name, const T *dptr, size_t count, cudaStream_t s) {
 // nothing; mrrr_trim_workspace() releases the memory of the calling thread
 // earlier.  (At process exit the CUDA context may already be gone; the
 // destructors then ignore the errors.)
+// Hardware work queues.  A CUDA context maps its streams onto
+// CUDA_DEVICE_MAX_CONNECTIONS hardware queues (8 by default); a solve uses up
+// to 11 streams of its own (below) next to the caller's, and two streams that
+// share a queue wait for one another.  Measured on one B200 (random n = 20000,
+// profiles/r02/setF): with 8 queues the tree stream's flag read-back after the
+// last level's refinement returned only when an unrelated vector piece ended
+// (~1 ms), and a piece launched on an idle side stream started only when an
+// earlier piece on another stream ended; with 32 queues neither happens
+// (34.2 -> 33.8 ms with four side streams, 32.5 ms with eight).  The variable
+// is read when the context is created, so the library sets it (without
+// overriding the caller's value) when it is loaded; a process that created its
+// context earlier keeps its own setting and the solve is only slower.
+__attribute__((constructor)) static void mrrr_on_load() { setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }
+
 constexpr int kSide = 8;  // side streams for the vector batches (at most; MRRR_NSIDE of them are used)
-constexpr int kNSideDefault = 4;
+constexpr int kNSideDefault = 8;  // with 32 hardware queues (above): 4 / 6 / 8 -> 33.7 / 32.8 / 32.6 ms at random n=20000, other configs unchanged
 struct StreamSet {
   cudaStream_t st[64][kSide + 3] = {};  // per device: kSide side streams, the copy stream, the solve stream, the tree's second stream
   ~StreamSet() {
@@ -938,12 +952,15 @@ int solve(Problem &P, int64_t *m_out) {
   // between, unlike MRRR_TRACE=2)
   const bool timeline = getenv("MRRR_TIMELINE") != nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> tline;
+  std::vector<double> tline_host;  // host clock when the mark was enqueued (ms since the call began)
+  const auto tl_host0 = std::chrono::steady_clock::now();
   int tl_level = -1;
   auto tl_mark = [&](const std::string &what) {
     if (!timeline) return;
     cudaEvent_t e = ev_time();
     cudaEventRecord(e, s);
     tline.push_back({what, e});
+    tline_host.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl_host0).count());
   };
   KTimer kt_root, kt_fin;
   memset(&g_stats, 0, sizeof(g_stats));
@@ -2113,6 +2130,7 @@ int solve(Problem &P, int64_t *m_out) {
         CK(cudaMemcpyToSymbol(g_rw_hist, hist, sizeof hist));
       }
       d2h(h_fail, dfail, 4, s);
+      tl_mark("L" + std::to_string(level) + " flags read");
       if (getenv("MRRR_DUMP")) {
         char nm[64];
         {
@@ -2313,10 +2331,11 @@ int solve(Problem &P, int64_t *m_out) {
   }
   if (timeline) {
     cudaStreamSynchronize(s);
-    for (auto &m : tline) {
+    for (size_t i = 0; i < tline.size(); ++i) {
       float v = 0;
-      cudaEventElapsedTime(&v, tall.a, m.second);
-      fprintf(stderr, "[mrrr timeline] %8.3f ms  tree  %s\n", v, m.first.c_str());
+      cudaEventElapsedTime(&v, tall.a, tline[i].second);
+      fprintf(stderr, "[mrrr timeline] %8.3f ms  tree  %s  (host enqueued it at %.3f ms)\n", v,
+              tline[i].first.c_str(), tline_host[i]);
     }
     for (size_t i = 0; i < vec_ev.size(); ++i) {
       float a = 0, b = 0;

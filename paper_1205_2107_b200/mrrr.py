@@ -10,7 +10,12 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-import torch
+# Hardware work queues for the solve's streams (csrc/mrrr.cu, mrrr_on_load): read by
+# the driver when the CUDA context is created, so it is set at import time, before
+# torch initialises CUDA; a value the caller has set is kept.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+import torch  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libmrrr_b200.so")

@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="random_20000")
+    ap.add_argument("--collective", default="torch", choices=["torch", "nccl"],
+                    help="N>1: the protocol's all-gathers through the torch.distributed NCCL group "
+                         "(mrrr_stemr_dist + callback) or issued by the library on its own ncclComm_t (mrrr_stemr_nccl)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-pairs", type=int, default=0,
@@ -267,10 +270,16 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     cb = None
-    if world > 1:
-        cb = P.mrrr.torch_allgather()  # NCCL all-gather of w (the path's only collective)
+    comm = None
+    if world > 1 and args.collective == "nccl":
+        comm = P.NcclComm(dev)  # ncclUniqueId broadcast through the default process group
+    elif world > 1:
+        cb = P.mrrr.torch_allgather()  # the protocol's all-gathers on the torch NCCL group
 
     def step():
+        if comm is not None:
+            wa, Zl, _ = P.stemr_nccl(dt_, et_, comm, stream=stream, **kw)
+            return wa, Zl
         if world > 1:
             wa, Zl, _ = P.stemr_dist(dt_, et_, rank=rank, nranks=world, allgather=cb, stream=stream, **kw)
             return wa, Zl

@@ -165,6 +165,31 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range,
                     double *Z_local, int64_t ldz, void *stream);
 
 /*
+ * mrrr_stemr_nccl -- mrrr_stemr_dist on an NCCL communicator (the sharded
+ * solve of PAPER.md L1125-1182 with the paper's gathers as ncclAllGather
+ * over NVLink).  `nccl_comm` is an ncclComm_t (passed as
+ * void* so that this header needs no nccl.h) of P ranks, one GPU each, whose
+ * device is the calling thread's current device; rank and P are read from
+ * it, and every all-gather of the protocol is enqueued on `stream` as
+ * ncclAllGather(send, recv, bytes, ncclInt8, comm, stream).  NCCL is
+ * resolved at run time (the libnccl.so.2 the process has loaded, else the
+ * one on the loader path): the library does not link against it, and the
+ * communicator stays the caller's (created and destroyed by the caller; no
+ * other NCCL call of the caller may be in flight on it during the solve).
+ * Arguments 1-8 as in mrrr_stemr; (9) nccl_comm; (10) m (HOST out, global
+ * count); (11) opts; (12) col_begin, (13) m_local (HOST out); (14) w_all;
+ * (15) Z_local; (16) ldz; (17) stream -- meaning, capacities and layout as
+ * in mrrr_stemr_dist.  Returns as mrrr_stemr_dist (-i counts THIS entry's
+ * arguments; -9: NULL communicator or one of another device), 7
+ * (MRRR_ERR_COMM) if NCCL cannot be loaded or a collective fails.
+ */
+int mrrr_stemr_nccl(int64_t n, const double *d, const double *e, int range,
+                    double vl, double vu, int64_t il, int64_t iu,
+                    void *nccl_comm, int64_t *m, const mrrr_opts_t *opts,
+                    int64_t *col_begin, int64_t *m_local, double *w_all,
+                    double *Z_local, int64_t ldz, void *stream);
+
+/*
  * mrrr_stemr_host -- the same solve with HOST buffers (end-to-end entry):
  * d[n], e[n-1], w[k] and Z (ldz x k, column major, or NULL) are host memory
  * (pinned or pageable; pinned is faster).  The call allocates device buffers

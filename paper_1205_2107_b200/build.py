@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libmrrr_b200.so")
 SRC = os.path.join(HERE, "csrc", "mrrr.cu")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-ldl"]
 
 
 def _deps():

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <dlfcn.h>
 #include <cstring>
 #include <chrono>
 #include <mutex>
@@ -2594,6 +2595,61 @@ int mrrr_stemr_dist(int64_t n, const double *d, const double *e, int range, doub
     cudaGetLastError();
     return ce.e == cudaErrorMemoryAllocation ? MRRR_ERR_NOMEM : MRRR_ERR_CUDA;
   }
+}
+
+// mrrr_stemr_nccl: mrrr_stemr_dist on an NCCL communicator (SURVEY §8(b)'s
+// signature).  NCCL is resolved at run time -- the copy the process has
+// already loaded (torch's), else libnccl.so.2 on the loader path -- so the
+// library has no link-time dependency on it and the single-GPU entries work
+// without it.
+namespace {
+struct NcclApi {
+  // ncclResult_t f(...): 0 = ncclSuccess; ncclDataType_t ncclInt8 = 0
+  int (*all_gather)(const void *, void *, size_t, int, void *, void *) = nullptr;
+  int (*comm_count)(void *, int *) = nullptr;
+  int (*comm_user_rank)(void *, int *) = nullptr;
+  int (*comm_cu_device)(void *, int *) = nullptr;
+  bool ok = false;
+};
+const NcclApi &nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.all_gather = (decltype(a.all_gather))dlsym(h, "ncclAllGather");
+    a.comm_count = (decltype(a.comm_count))dlsym(h, "ncclCommCount");
+    a.comm_user_rank = (decltype(a.comm_user_rank))dlsym(h, "ncclCommUserRank");
+    a.comm_cu_device = (decltype(a.comm_cu_device))dlsym(h, "ncclCommCuDevice");
+    a.ok = a.all_gather && a.comm_count && a.comm_user_rank && a.comm_cu_device;
+    return a;
+  }();
+  return api;
+}
+int nccl_allgather_cb(void *ctx, const void *send, void *recv, size_t bytes, void *stream) {
+  return nccl_api().all_gather(send, recv, bytes, /*ncclInt8*/ 0, ctx, stream) == 0 ? 0 : 1;
+}
+}  // namespace
+
+int mrrr_stemr_nccl(int64_t n, const double *d, const double *e, int range, double vl,
+                    double vu, int64_t il, int64_t iu, void *nccl_comm, int64_t *m,
+                    const mrrr_opts_t *opts, int64_t *col_begin, int64_t *m_local,
+                    double *w_all, double *Z_local, int64_t ldz, void *stream) {
+  if (!nccl_comm) return -9;
+  const NcclApi &A = nccl_api();
+  if (!A.ok) return MRRR_ERR_COMM;
+  int nranks = 0, rank = -1, cdev = -1, dev = -2;
+  if (A.comm_count(nccl_comm, &nranks) != 0 || A.comm_user_rank(nccl_comm, &rank) != 0 ||
+      A.comm_cu_device(nccl_comm, &cdev) != 0)
+    return MRRR_ERR_COMM;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return MRRR_ERR_CUDA; }
+  if (dev != cdev) return -9;  // the communicator belongs to another device than the current one
+  int rc = mrrr_stemr_dist(n, d, e, range, vl, vu, il, iu, rank, nranks, nccl_allgather_cb, nccl_comm, m,
+                           opts, col_begin, m_local, w_all, Z_local, ldz, stream);
+  // argument positions of mrrr_stemr_dist -> this entry's (9 comm; 10.. = dist's 13..)
+  if (rc <= -13) rc += 3;
+  return rc;
 }
 
 int mrrr_negcount(int64_t nb, const double *D, const double *LLD, int64_t k, const double *mu,

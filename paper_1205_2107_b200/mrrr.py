@@ -80,6 +80,12 @@ def lib():
                                       C.POINTER(C.c_int64), C.c_void_p, C.c_void_p, C.c_int64,
                                       C.c_void_p]
         L.mrrr_stemr_dist.restype = C.c_int
+        L.mrrr_stemr_nccl.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                      C.c_double, C.c_int64, C.c_int64, C.c_void_p,
+                                      C.POINTER(C.c_int64), C.POINTER(Opts), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64), C.c_void_p, C.c_void_p, C.c_int64,
+                                      C.c_void_p]
+        L.mrrr_stemr_nccl.restype = C.c_int
         L.mrrr_workspace_bytes.argtypes = [C.c_int64, C.c_int64]
         L.mrrr_workspace_bytes.restype = C.c_size_t
         L.mrrr_strerror.argtypes = [C.c_int]
@@ -345,6 +351,115 @@ def stemr_dist(d: torch.Tensor, e: torch.Tensor, *, il=None, iu=None, vl=None, v
         raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
     k = m.value
     return w_all[:k], (Zl[:ml.value].T if vectors else None), c0.value
+
+
+class _NcclUniqueId(C.Structure):
+    _fields_ = [("internal", C.c_char * 128)]  # nccl.h: NCCL_UNIQUE_ID_BYTES
+
+
+_nccl = None
+
+
+def _nccl_lib():
+    """The NCCL the process already has (torch's bundled libnccl.so.2), else
+    the loader path's -- the same one mrrr_stemr_nccl resolves."""
+    global _nccl
+    if _nccl is None:
+        mode = getattr(os, "RTLD_NOLOAD", 4) | os.RTLD_NOW
+        try:
+            L = C.CDLL("libnccl.so.2", mode=mode)
+        except OSError:
+            L = C.CDLL("libnccl.so.2")
+        L.ncclGetUniqueId.argtypes = [C.POINTER(_NcclUniqueId)]
+        L.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, _NcclUniqueId, C.c_int]
+        L.ncclCommDestroy.argtypes = [C.c_void_p]
+        for f in (L.ncclGetUniqueId, L.ncclCommInitRank, L.ncclCommDestroy):
+            f.restype = C.c_int
+        _nccl = L
+    return _nccl
+
+
+def broadcast_bytes(payload: bytes, rank: int, group=None, device=None) -> bytes:
+    """Rank 0's ``payload`` on every rank of ``group`` (the ncclUniqueId
+    bootstrap of :class:`NcclComm`; a gloo group broadcasts host memory, an
+    nccl group the bytes staged on ``device``)."""
+    import torch.distributed as dist
+    t = torch.frombuffer(bytearray(payload if rank == 0 else bytes(len(payload))), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.to(device)
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return t.cpu().numpy().tobytes()
+
+
+class NcclComm:
+    """An ncclComm_t owned by the caller of :func:`stemr_nccl` (SURVEY §8(b):
+    the communicator is bootstrapped by broadcasting the ncclUniqueId through
+    a torch.distributed process group; torch is plumbing only).  ``group`` may
+    be a gloo or nccl group; with ``nranks == 1`` no process group is needed."""
+
+    def __init__(self, device, group=None, rank=None, nranks=None):
+        import torch.distributed as dist
+        self.handle = C.c_void_p(0)
+        self.device = torch.device(device)
+        if rank is None or nranks is None:
+            if dist.is_available() and dist.is_initialized():
+                rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+            else:
+                rank, nranks = 0, 1
+        self.rank, self.nranks = int(rank), int(nranks)
+        uid = _NcclUniqueId()
+        L = _nccl_lib()
+        if self.rank == 0 and L.ncclGetUniqueId(C.byref(uid)) != 0:
+            raise RuntimeError("ncclGetUniqueId failed")
+        if self.nranks > 1:
+            raw = broadcast_bytes(C.string_at(C.addressof(uid), 128), self.rank, group, self.device)
+            C.memmove(C.byref(uid), raw, 128)
+        with torch.cuda.device(self.device):
+            rc = L.ncclCommInitRank(C.byref(self.handle), self.nranks, uid, self.rank)
+        if rc != 0:
+            raise RuntimeError(f"ncclCommInitRank failed ({rc})")
+
+    def destroy(self):
+        if self.handle:
+            _nccl_lib().ncclCommDestroy(self.handle)
+            self.handle = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def stemr_nccl(d: torch.Tensor, e: torch.Tensor, comm: NcclComm, *, il=None, iu=None, vl=None, vu=None,
+               vectors: bool = True, opts: Opts | None = None, stream=None):
+    """Sharded MRRR on an NCCL communicator (``mrrr_stemr_nccl``): the library
+    itself issues the protocol's ncclAllGather calls on ``stream``.  Returns
+    ``(w_all, Z_local, col_begin)`` as :func:`stemr_dist`."""
+    if not (d.is_cuda and d.dtype == torch.float64):
+        raise TypeError("d must be a torch.float64 CUDA tensor (no CPU fallback)")
+    if d.device != comm.device and not (d.device.index is None or comm.device.index is None):
+        raise ValueError("the communicator belongs to another device than d")
+    n = d.shape[0]
+    d = d.contiguous()
+    e = e.contiguous() if n > 1 else d
+    rng, a, b, ilv, iuv, kcap = _range_args(n, il, iu, vl, vu)
+    kcap = max(kcap, 1)
+    w_all = torch.empty(kcap, dtype=torch.float64, device=d.device)
+    Zl = torch.empty((dist_capacity(kcap, comm.nranks), n), dtype=torch.float64, device=d.device) if vectors else None
+    if stream is None:
+        stream = torch.cuda.current_stream(d.device)
+    m = C.c_int64(0)
+    c0 = C.c_int64(0)
+    ml = C.c_int64(0)
+    o = opts if opts is not None else default_opts()
+    with torch.cuda.device(d.device):
+        rc = lib().mrrr_stemr_nccl(n, _ptr(d), _ptr(e), rng, a, b, ilv, iuv, comm.handle,
+                                   C.byref(m), C.byref(o), C.byref(c0), C.byref(ml), _ptr(w_all),
+                                   _ptr(Zl) if vectors else C.c_void_p(0), n, C.c_void_p(stream.cuda_stream))
+    if rc != 0:
+        raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
+    return w_all[:m.value], (Zl[:ml.value].T if vectors else None), c0.value
 
 
 def stemr_raw(n, d, e, rng, vl, vu, il, iu, m_ok=True, w=None, Z=None, ldz=None):

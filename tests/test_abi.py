@@ -24,7 +24,7 @@ def so():
 
 def test_header_declares_the_boundary():
     names = header_functions()
-    for required in ["mrrr_stemr", "mrrr_stemr_dist", "mrrr_stemr_host", "mrrr_workspace_bytes",
+    for required in ["mrrr_stemr", "mrrr_stemr_dist", "mrrr_stemr_nccl", "mrrr_stemr_host", "mrrr_workspace_bytes",
                      "mrrr_strerror", "mrrr_default_opts", "mrrr_get_stats", "mrrr_version"]:
         assert required in names
 
@@ -48,6 +48,13 @@ def test_host_only_calls(so):
     assert M.version().startswith("mrrr-b200")
     st = M.last_stats()
     assert set(st) >= {"nodes", "ms_k_vectors", "vec_elems"}
+
+
+def test_nccl_entry_rejects_null_communicator(so):
+    """mrrr_stemr_nccl validates its communicator before touching NCCL or CUDA."""
+    from paper_1205_2107_b200 import mrrr as M
+    rc = M.lib().mrrr_stemr_nccl(4, None, None, 0, 0.0, 0.0, 0, 0, None, None, None, None, None, None, None, 4, None)
+    assert rc == -9
 
 
 def test_stats_struct_matches_header():

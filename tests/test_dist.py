@@ -165,3 +165,26 @@ def test_exchange_payloads_gloo_world2():
         # the status word of rank 1 reaches rank 0 (worst code = 2 on both)
         assert status == [0, 2] and max(status) == 2
         assert ncl == [7, 7]
+
+
+def _worker_uid(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        payload = bytes((7 * k + 1) % 256 for k in range(128)) if rank == 0 else bytes(range(128))
+        out[rank] = M.broadcast_bytes(payload, rank)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_unique_id_bootstrap_gloo_world2():
+    """NcclComm's bootstrap: every rank ends with rank 0's 128 ncclUniqueId
+    bytes (zero bytes included), whatever it held before."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_uid, args=(world, port, out), nprocs=world, join=True)
+    expect = bytes((7 * k + 1) % 256 for k in range(128))
+    assert out[0] == expect and out[1] == expect

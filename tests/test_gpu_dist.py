@@ -165,3 +165,29 @@ def test_dist_argument_errors(torch_cuda):
     with pytest.raises(P.mrrr.MrrrError) as ex:
         P.stemr_dist(dt, et, rank=0, nranks=0, allgather=cb)
     assert ex.value.code == -10
+
+
+def test_nccl_entry_single_rank(torch_cuda):
+    """mrrr_stemr_nccl on a one-rank ncclComm_t (what one GPU can run): the
+    library resolves NCCL itself, reads rank / size from the communicator and
+    issues every all-gather of the protocol as ncclAllGather on the solve
+    stream; the eigenpairs equal mrrr_stemr's bit for bit (with vectors, values
+    only and an index range), and a communicator of another device is refused."""
+    import paper_1205_2107_b200 as P
+    torch = torch_cuda
+    comm = P.NcclComm("cuda:0", rank=0, nranks=1)
+    try:
+        for n, seed, kw in [(700, 6, {}), (1500, 2, {"il": 100, "iu": 900}), (900, 1, {"vectors": False})]:
+            d, e = W.random_uniform(n, seed)
+            dt, et = torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda")
+            w1, Z1 = P.stemr(dt, et, **kw)
+            w2, Z2, c0 = P.stemr_nccl(dt, et, comm, **kw)
+            assert c0 == 0
+            assert torch.equal(w1, w2)
+            assert (Z1 is None and Z2 is None) or torch.equal(Z1, Z2)
+        assert P.last_stats()["kernel_launches"] > 0
+    finally:
+        comm.destroy()
+    with pytest.raises(P.mrrr.MrrrError) as ex:
+        P.stemr_nccl(dt, et, comm)  # destroyed: NULL handle
+    assert ex.value.code == -9

@@ -30,6 +30,17 @@
  * below); 1 root RRR not found; 2 child RRR not acceptable; 3 tree depth cap
  * exceeded; 4 bisection/RQC non-convergence; 5 CUDA error; 6 out of device
  * memory; 7 collective (multi-GPU) error.  On error, outputs are unspecified.
+ *
+ * Process environment: a solve runs on up to 11 CUDA streams of its own (the
+ * tree, the vector pieces, the Z download), and streams that share one of the
+ * context's hardware work queues wait for one another.  When the library is
+ * LOADED it therefore sets CUDA_DEVICE_MAX_CONNECTIONS=32 in the process
+ * environment if (and only if) the variable is not set; the driver reads it
+ * when the CUDA context is created, so a process that created its context
+ * before loading the library, or set the variable itself, keeps its setting
+ * (the results are the same; with the default 8 queues the headline solve is
+ * ~5 % slower).  Nothing else in the environment is written; the MRRR_*
+ * variables the library reads are diagnostics.
  */
 #ifndef MRRR_H
 #define MRRR_H

@@ -57,6 +57,21 @@ def test_nccl_entry_rejects_null_communicator(so):
     assert rc == -9
 
 
+def test_load_sets_work_queues_unless_set(so):
+    """include/mrrr.h "Process environment": loading the library sets
+    CUDA_DEVICE_MAX_CONNECTIONS=32 only when the caller has not set it."""
+    import subprocess
+    import sys
+    code = ("import ctypes, sys; ctypes.CDLL(sys.argv[1]); g = ctypes.CDLL(None).getenv; "
+            "g.restype = ctypes.c_char_p; print(g(b'CUDA_DEVICE_MAX_CONNECTIONS').decode())")
+    env = {k: v for k, v in os.environ.items() if k != "CUDA_DEVICE_MAX_CONNECTIONS"}
+    out = subprocess.run([sys.executable, "-c", code, so], env=env, capture_output=True, text=True, check=True)
+    assert out.stdout.strip() == "32"
+    env["CUDA_DEVICE_MAX_CONNECTIONS"] = "8"
+    out = subprocess.run([sys.executable, "-c", code, so], env=env, capture_output=True, text=True, check=True)
+    assert out.stdout.strip() == "8"
+
+
 def test_stats_struct_matches_header():
     """The ctypes Stats/Opts layouts mirror mrrr_stats_t / mrrr_opts_t."""
     from paper_1205_2107_b200 import mrrr as M

@@ -21,7 +21,10 @@
 namespace mrrr {
 
 constexpr int kTR = 16;          // rows per tile (= checkpoint segment)
-constexpr int kRing = 6;         // tiles in flight per warp
+#ifndef MRRR_VRING
+#define MRRR_VRING 6
+#endif
+constexpr int kRing = MRRR_VRING;  // tiles in flight per warp
 static_assert(kTR == kSeg, "tiles and checkpoint segments coincide");
 
 // A work item may hold the eigenpairs of up to kMaxSeg nodes ("segments") of
@@ -31,7 +34,10 @@ static_assert(kTR == kSeg, "tiles and checkpoint segments coincide");
 // into one warp keeps the lanes busy: deep tree levels deliver a few
 // singletons per node, and one node per warp left ~79 % of the lanes idle at
 // n = 20000 (3000 items for 20000 eigenpairs).
-constexpr int kMaxSeg = 8;
+#ifndef MRRR_VSEG
+#define MRRR_VSEG 8
+#endif
+constexpr int kMaxSeg = MRRR_VSEG;
 
 // Shared memory of one warp.
 struct WarpSmem {

@@ -1564,6 +1564,8 @@ int solve(Problem &P, int64_t *m_out) {
   CK(cudaMemsetAsync(fail_count, 0, sizeof(int), s));
   // MRRR_VEC_MODE=1 (diagnostic): all vectors in one batch after the tree
   const int vec_mode = env_int("MRRR_VEC_MODE", 0);
+  const int flush_late = env_int("MRRR_FLUSH_LATE", 0);
+  const int flush_late_min = env_int("MRRR_FLUSH_LATE_MIN", 64);
   // batches go round-robin to kSide side streams so that they overlap one
   // another as well as the tree (one side stream ran them back to back: the
   // batches are latency-bound, ~12 ms each at n = 20000, and their chain
@@ -1913,7 +1915,12 @@ int solve(Problem &P, int64_t *m_out) {
       }
     }
     const int ncl = (int)cl_parent.size(), nown = (int)own_cl.size();
-    if (vectors && (vec_mode == 0 || ncl == 0)) guarded([&] { flush_vectors(nown); });
+    // When the level's singletons go out: at the level's start, or (flush_late,
+    // levels with at least flush_late_min clusters) behind the level's cluster
+    // step, so that the step's kernels do not share the SMs' registers with
+    // the new pieces (see the note at the late flush below)
+    const bool late_flush = vectors && vec_mode == 0 && flush_late && ncl >= flush_late_min;
+    if (vectors && (vec_mode == 0 || ncl == 0) && !late_flush) guarded([&] { flush_vectors(nown); });
     if (ncl == 0) break;
     if (level + 1 > P.o.max_depth) throw MrrrError{MRRR_ERR_DEPTH};  // the same level on every rank
     g_stats.nodes += nown;
@@ -2071,6 +2078,9 @@ int solve(Problem &P, int64_t *m_out) {
       // the child node entries are written before the translate kernel reads sigma
       k_child_nodes<<<(ncl + 63) / 64, 64, 0, s>>>(dnodes, node_base, dcl_parent, dcl_s0, dcl_s1, dsig, ncl,
                                                    dcl_rrr, slot_j);
+      // late flush: the pieces wait for the cluster step (event on this stream)
+      // and are registered with their nodes before the parents' slots are released
+      if (late_flush) flush_vectors(nown);
       // the parents' RRRs (read by the child step above, last reader on this
       // stream) go back to the pool once their vector pieces are done
       pool_release_level(level_nodes);

@@ -188,7 +188,9 @@ def test_deterministic(torch_cuda, P):
                                  {"MRRR_VEC_PACK": "0"}, {"MRRR_CHILD_V1": "1"},
                                  {"MRRR_CHILD_V1": "0"}, {"MRRR_CHILD_V1": "0", "MRRR_CHILD_V3": "0"},
                                  {"MRRR_CHILD_V1": "0", "MRRR_CS_GROUP": "5"}, {"MRRR_VEC_PSPLIT": "0"},
-                                 {"MRRR_VEC_PAIR": "2", "MRRR_VEC_PSPLIT": "0"}])
+                                 {"MRRR_VEC_PAIR": "2", "MRRR_VEC_PSPLIT": "0"},
+                                 {"MRRR_FLUSH_LATE": "1", "MRRR_FLUSH_LATE_MIN": "1"},
+                                 {"MRRR_NSIDE": "3"}, {"MRRR_NSIDE": "4", "MRRR_SIDE_RR": "1", "MRRR_PIECE_DIV": "7"}])
 def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     """The launch schedule does not change a single bit: cluster steps in
     groups that reuse the scratch (MRRR_CS_GROUP, the n = 1e5 memory cap's
@@ -205,7 +207,10 @@ def test_schedule_invariance(torch_cuda, P, monkeypatch, env):
     per warp, unless MRRR_CHILD_V3=0; the default picks by the level's width; the same
     per-chain arithmetic; their reductions sum over different thread counts,
     which can move a weighted growth by an ulp but not, on these inputs, a
-    decision) -- against the default schedule.
+    decision), a level's singletons launched behind its cluster step instead of
+    at its start (MRRR_FLUSH_LATE), fewer side streams, round-robin stream
+    choice and other piece sizes (MRRR_NSIDE, MRRR_SIDE_RR, MRRR_PIECE_DIV)
+    -- against the default schedule.
     Each cluster's step and each eigenpair's RQC depend on their own data only."""
     for d, e in (W.glued_wilkinson(40), W.random_uniform(3000, 2)):
         w1, Z1 = gpu_solve(P, torch_cuda, d, e)

@@ -330,7 +330,7 @@ def main():
     B = bisection_steps(d, e, w_host)
     slots_bis = float(np.sum(B)) * (2 + W_DIV) * n
     # The roofline UNIT is the whole step: the path's kernels run
-    # concurrently on five streams (the tree on a high-priority stream, the
+    # concurrently on up to ten streams (the tree on a high-priority stream, the
     # vector pieces on four side streams), so no single kernel's launch
     # duration is a share of the step (summed piece durations
     # were 1.8x the step).  achieved = the work model's FP64-pipe slots per
@@ -361,7 +361,7 @@ def main():
             hw_slots = sum(v["fp64_slots"] for v in kj["kernels"].values())
         except Exception:
             kernels = None
-    roof = {"bound": "alu", "kernel": "whole step (all SURVEY §8(a) rows; kernels overlap on five streams)",
+    roof = {"bound": "alu", "kernel": "whole step (all SURVEY §8(a) rows; kernels overlap on up to ten streams)",
             "achieved": 2 * w_slots / t_step / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": t_roof / t_step, "traffic": traffic,
             "algorithmic_bytes": 8.0 * n * m, "t_roof_ms": 1e3 * t_roof, "t_alu_ms": 1e3 * t_alu,

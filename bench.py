@@ -305,6 +305,7 @@ def main():
         wk = step()[0]  # (keep no view of Z: e2e below frees it)
         evs[i][1].record(stream)
         stats.append(P.last_stats())
+        hist_last = P.rqc_histogram()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -331,7 +332,7 @@ def main():
     slots_bis = float(np.sum(B)) * (2 + W_DIV) * n
     # The roofline UNIT is the whole step: the path's kernels run
     # concurrently on up to ten streams (the tree on a high-priority stream, the
-    # vector pieces on four side streams), so no single kernel's launch
+    # vector pieces on eight side streams), so no single kernel's launch
     # duration is a share of the step (summed piece durations
     # were 1.8x the step).  achieved = the work model's FP64-pipe slots per
     # step (x2 flop) over the step time; frac = T_roof / T_step with T_roof =
@@ -457,6 +458,7 @@ def main():
             cpu["single_core"] = {"value": v1, "sample": desc1, "seconds": dt1}
 
     s0 = stats[-1]
+    rqc_hist = hist_last  # eigenpairs by twisted factorizations of their RQC (mrrr_get_rqc_histogram)
     launches = sum(int(s["kernel_launches"]) for s in stats)
     line = {"metric": METRIC, "value": value, "unit": "eigenpairs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
@@ -473,7 +475,8 @@ def main():
                           "total": s0["ms_total"]},
             "tree": {"nodes": s0["nodes"], "levels": s0["levels"], "rqc_iters": s0["rqc_iters"],
                      "rqc_fallbacks": s0["rqc_fallbacks"], "safe_resweeps": s0["safe_resweeps"],
-                     "vec_items": s0["vec_items"], "vec_nudges": s0["vec_nudges"]},
+                     "vec_items": s0["vec_items"], "vec_nudges": s0["vec_nudges"],
+                     "rqc_hist": rqc_hist},
             "memory": {"pool_bytes": s0["pool_bytes"], "workspace_bytes": s0["workspace_bytes"],
                        "z_bytes": 8 * n * m if world == 1 else None,
                        "note": "device workspace the library holds (all of it, child RRR pools included) "

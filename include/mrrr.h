@@ -267,6 +267,17 @@ int mrrr_trim_workspace(void);
 int mrrr_negcount(int64_t nb, const double *D, const double *LLD, int64_t k,
                   const double *mu, int64_t *count, int mode, void *stream);
 
+/* Metrics: how many twisted factorizations the Rayleigh-quotient correction
+ * of each eigenpair took in the calling thread's last mrrr_stemr* call
+ * (the paper's step is one inverse iteration on a
+ * twisted factorization; reading 10 iterates it).  hist16[k], k =
+ * 1 .. 14: eigenpairs (of this rank) that needed k factorizations; [15]: 15
+ * or more; [0]: unused.  sum_k hist16[k] = eigenvectors computed by the
+ * tree's vector kernels (1 x 1 blocks are not counted), sum_k k hist16[k] =
+ * mrrr_stats_t.rqc_iters without the fallback passes.  HOST out, 16 entries.
+ * Returns 0 or -1 (NULL). */
+int mrrr_get_rqc_histogram(int64_t *hist16);
+
 /* Static description of a return code. */
 const char *mrrr_strerror(int code);
 

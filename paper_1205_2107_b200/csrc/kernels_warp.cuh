@@ -802,9 +802,17 @@ struct WVecArgs {
   int *fail_count;
   int task_base;             // global index of this launch's task 0
   unsigned long long *ctr;   // [0] factorizations, [1] fallbacks, [2..3] nudges, [4..7] slowest item
+  unsigned long long *hist;  // mode 0 / 4: eigenpairs by twisted factorizations of their RQC ([k], k = min(count, 15))
   struct RqcState *state;    // modes 3, 4: per-task RQC state between the split phases
   int *rkey;                 // mode 3: per-task twist index (sort key)
 };
+
+// An eigenpair's RQC is done after `nfact` twisted factorizations: the call's
+// total and the histogram (mrrr_get_rqc_histogram).
+__device__ __forceinline__ void rqc_count(const WVecArgs &A, unsigned long long nfact) {
+  atomicAdd(&A.ctr[0], nfact);
+  if (A.hist) atomicAdd(&A.hist[nfact < 15ull ? nfact : 15ull], 1ull);
+}
 
 constexpr int kPairThreads = 64;  // pair kernel: one item per CTA, warp F + warp B
 constexpr int kSingleWarps = 2;   // single-warp kernel: independent items per CTA
@@ -913,7 +921,7 @@ __device__ __forceinline__ void wvec_pair_body(const WVecArgs &A) {
     w_solve_pair(W, lam, tw.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !failed, role);
     if (lead) {
       if (active && !failed) A.lam_out[tix] = lam_fin;
-      if (active) atomicAdd(&A.ctr[0], nfact);
+      if (active) rqc_count(A, nfact);
       if (lane == 0) {  // slowest item: cycles of the first factorization, the RQC loop, the solve;
                         // factorizations of the item (MRRR_TRACE)
         const long long clk_end = clock64();
@@ -1034,7 +1042,7 @@ __device__ __forceinline__ void wvec_single_body(const WVecArgs &A) {
     const double sc = 1.0 / sqrt(tw.nrm2);
     w_twist_solve(W, lam, tw.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !failed);
     if (active && !failed) A.lam_out[tix] = lam_fin;
-    if (active) atomicAdd(&A.ctr[0], nfact);
+    if (active) rqc_count(A, nfact);
     if (lane == 0) {  // slowest warp: cycles of the first factorization, the RQC loop, the solve;
                       // factorizations of the warp (MRRR_TRACE)
       const long long clk_end = clock64();
@@ -1204,7 +1212,7 @@ __device__ __forceinline__ void wvec_split_body(const WVecArgs &A) {
   const double sc = 1.0 / sqrt(Q.best.nrm2);
   w_twist_solve(W, Q.lam_best, Q.best.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !Q.failed);
   if (active && !Q.failed) A.lam_out[tix] = Q.lam_fin;
-  if (active) atomicAdd(&A.ctr[0], nfact);
+  if (active) rqc_count(A, nfact);
   if (lane == 0) atomicMax(&A.ctr[7], nfact);
 }
 
@@ -1328,7 +1336,7 @@ __device__ __forceinline__ void wvec_pair_split_body(const WVecArgs &A) {
   w_solve_pair(W, Q.lam_best, Q.best.r, sc, A.Z + tk.col * A.ldz + N.row0, active && !Q.failed, role);
   if (lead) {
     if (active && !Q.failed) A.lam_out[tix] = Q.lam_fin;
-    if (active) atomicAdd(&A.ctr[0], nfact);
+    if (active) rqc_count(A, nfact);
     if (lane == 0) atomicMax(&A.ctr[7], nfact);
   }
 }

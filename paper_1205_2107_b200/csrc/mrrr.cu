@@ -32,6 +32,7 @@ using namespace mrrr;
 namespace {
 
 thread_local mrrr_stats_t g_stats;
+thread_local int64_t g_rqc_hist[16];  // the calling thread's last solve (mrrr_get_rqc_histogram)
 
 struct CudaError {
   cudaError_t e;
@@ -965,6 +966,7 @@ int solve(Problem &P, int64_t *m_out) {
   };
   KTimer kt_root, kt_fin;
   memset(&g_stats, 0, sizeof(g_stats));
+  memset(g_rqc_hist, 0, sizeof(g_rqc_hist));
   const bool vectors = P.Z != nullptr;
 
   // ---------------- a1: prep ----------------
@@ -972,8 +974,8 @@ int solve(Problem &P, int64_t *m_out) {
   double *ds = ar.alloc<double>(n), *es = ar.alloc<double>(n), *es2 = ar.alloc<double>(n);
   int *brk = ar.alloc<int>(n);
   double *hdr = ar.alloc<double>(8);
-  unsigned long long *ctr = ar.alloc<unsigned long long>(32);
-  CK(cudaMemsetAsync(ctr, 0, 32 * sizeof(unsigned long long), s));
+  unsigned long long *ctr = ar.alloc<unsigned long long>(48);  // [32..47]: the RQC histogram
+  CK(cudaMemsetAsync(ctr, 0, 48 * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(brk, 0, n * sizeof(int), s));
   k_prep<<<1, 1024, 0, s>>>(P.d, P.e, n, ds, es, es2, brk, hdr);
   CK(cudaGetLastError());
@@ -1554,7 +1556,7 @@ int solve(Problem &P, int64_t *m_out) {
   double *wlo = ar.alloc<double>(nslots), *whi = ar.alloc<double>(nslots);
   const int64_t nbmax = [&] { int x = 1; for (auto &B : hb) x = std::max(x, B.nb); return (int64_t)x; }();
   int level = 0;
-  unsigned long long h_ctr[32];
+  unsigned long long h_ctr[48];
   // ---- a6 overlapped with the tree: the singletons a level classifies are
   // final, so their vectors start at once on a lower-priority side stream
   // (events order them after the kernels that produced their node and
@@ -1782,7 +1784,7 @@ int solve(Problem &P, int64_t *m_out) {
       WVecArgs A{};
       A.nodes = dnodes; A.LDv = LDv; A.tasks = dtb; A.items = ditems; A.nitems = (int)items.size();
       A.lo = slo; A.hi = shi; A.fck = ck_f[sk]; A.bck = ck_b[sk]; A.ck_stride = ck_cap; A.ntask = nbt;
-      A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam + t0; A.mode = 0; A.ctr = ctr + 8;
+      A.Z = P.Z; A.ldz = P.ldz; A.lam_out = lam + t0; A.mode = 0; A.ctr = ctr + 8; A.hist = ctr + 32;
       A.slot_j = slot_j; A.rqc_max = std::max(1, P.o.rqc_max);
       A.fail_list = fail_list; A.fail_count = fail_count; A.task_base = (int)t0;
       const bool pair = vec_pair == 2 || (vec_pair == 1 && (double)tree_left * (double)nbmax <= kPairWork);
@@ -2312,7 +2314,8 @@ int solve(Problem &P, int64_t *m_out) {
   }
   });
   finish_w();
-  d2h(h_ctr, ctr, 32, s);
+  d2h(h_ctr, ctr, 48, s);
+  for (int k = 0; k < 16; ++k) g_rqc_hist[k] = (int64_t)h_ctr[32 + k];
   if (tr.on)
     fprintf(stderr, "[mrrr] probes %llu; nudged vector factorizations %llu (why %llu); slowest vector warp: "
             "cycles full %llu rqc %llu solve %llu, max factorizations per warp %llu\n",
@@ -2749,6 +2752,12 @@ const char *mrrr_strerror(int code) {
 int mrrr_get_stats(mrrr_stats_t *out) {
   if (!out) return -1;
   *out = g_stats;
+  return 0;
+}
+
+int mrrr_get_rqc_histogram(int64_t *hist16) {
+  if (!hist16) return -1;
+  memcpy(hist16, g_rqc_hist, sizeof(g_rqc_hist));
   return 0;
 }
 

@@ -99,6 +99,8 @@ def lib():
         L.mrrr_plan_columns.argtypes = [C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
         L.mrrr_plan_columns.restype = C.c_int
         L.mrrr_trim_workspace.restype = C.c_int
+        L.mrrr_get_rqc_histogram.argtypes = [C.POINTER(C.c_int64)]
+        L.mrrr_get_rqc_histogram.restype = C.c_int
         _lib = L
     return _lib
 
@@ -488,6 +490,14 @@ def negcount(D: torch.Tensor, LLD: torch.Tensor, mu: torch.Tensor, mode: int = 0
     if rc != 0:
         raise MrrrError(rc, lib().mrrr_strerror(rc).decode())
     return out
+
+
+def rqc_histogram() -> list:
+    """Eigenpairs of the last solve by the twisted factorizations their RQC
+    took (``mrrr_get_rqc_histogram``; index k = factorizations, 15 = 15+)."""
+    h = (C.c_int64 * 16)()
+    lib().mrrr_get_rqc_histogram(h)
+    return list(h)
 
 
 def trim_workspace() -> None:

@@ -312,3 +312,23 @@ def test_zero_diagonal_exact_zero_eigenvalue(torch_cuda, P, oracle_mod, monkeypa
     assert np.max(np.abs(w - lam)) <= 4 * n * EPS * tnorm1(d, e)
     res, orth = check_accuracy(d, e, w, Z)
     assert res <= 1 and orth <= 1, (res, orth)
+
+
+def test_rqc_histogram(torch_cuda, P):
+    """mrrr_get_rqc_histogram: every eigenvector of the tree's vector kernels is
+    counted once, under the number of twisted factorizations its RQC took; the
+    weighted sum is the call's factorization count (no fallback on this input);
+    a values-only solve counts nothing."""
+    torch = torch_cuda
+    d, e = W.random_uniform(3000, 4)
+    dt, et = torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda")
+    w, Z = P.stemr(dt, et)
+    st = P.last_stats()
+    h = P.rqc_histogram()
+    assert len(h) == 16 and h[0] == 0
+    assert sum(h) == 3000
+    assert st["rqc_fallbacks"] == 0
+    assert sum(k * c for k, c in enumerate(h)) == st["rqc_iters"]
+    assert max(k for k, c in enumerate(h) if c) <= 10  # reading 10: at most 10 factorizations
+    w, _ = P.stemr(dt, et, vectors=False)
+    assert sum(P.rqc_histogram()) == 0

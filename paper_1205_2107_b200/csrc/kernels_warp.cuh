@@ -889,7 +889,7 @@ __device__ __forceinline__ void wvec_pair_body(const WVecArgs &A) {
         // stop (reading 10): |delta| <= 4 eps |lambda|, fl(lambda + delta) ==
         // lambda, or stagnation (the correction no longer halves)
         if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam ||
-            (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
+            (it > 1 && (fabs(delta) >= 0.5 * fabs(delta_prev) || fabs(delta_prev) <= g_rqc_prev_tol * fabs(lam)))) {
           conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
         } else {
           bool stuck;
@@ -1011,7 +1011,7 @@ __device__ __forceinline__ void wvec_single_body(const WVecArgs &A) {
         // stop (reading 10): |delta| <= 4 eps |lambda|, fl(lambda + delta) ==
         // lambda, or stagnation (the correction no longer halves)
         if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam ||
-            (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
+            (it > 1 && (fabs(delta) >= 0.5 * fabs(delta_prev) || fabs(delta_prev) <= g_rqc_prev_tol * fabs(lam)))) {
           conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
         } else {
           bool stuck;
@@ -1091,7 +1091,7 @@ struct RqcLane {
     if (tw.negc >= j) { if (lam < hi) hi = lam; } else { if (lam > lo) lo = lam; }
     const double delta = tw.gamma / tw.nrm2;
     if (fabs(delta) <= 4.0 * kEps * fabs(lam) || lam + delta == lam ||
-        (it > 1 && fabs(delta) >= 0.5 * fabs(delta_prev))) {
+        (it > 1 && (fabs(delta) >= 0.5 * fabs(delta_prev) || fabs(delta_prev) <= g_rqc_prev_tol * fabs(lam)))) {
       conv = true; best = tw; lam_best = lam; lam_fin = lam + delta;
     } else {
       bool stuck;

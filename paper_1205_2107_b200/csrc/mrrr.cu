@@ -913,6 +913,19 @@ void set_diag_flags(cudaStream_t s) {
     last_safe[dev & 63] = fs;
   }
   {
+    // diagnostic: MRRR_RQC_PREV_TOL=<x> sets the previous-correction stop of the RQC (reading 33; 0 = off)
+    static double last_pt[64];
+    static bool have_pt[64];
+    const char *ev = getenv("MRRR_RQC_PREV_TOL");
+    const double pt = ev ? atof(ev) : 4.656612873077393e-10;
+    if (!have_pt[dev & 63] ? ev != nullptr : pt != last_pt[dev & 63]) {
+      CK(cudaMemcpyToSymbolAsync(g_rqc_prev_tol, &pt, sizeof(double), 0, cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    have_pt[dev & 63] = true;
+    last_pt[dev & 63] = pt;
+  }
+  {
     static int last_dbg[64];
     const int fd = env_int("MRRR_DEBUG_RQC", 0);
     if (fd != last_dbg[dev & 63]) {

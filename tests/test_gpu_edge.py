@@ -332,3 +332,30 @@ def test_rqc_histogram(torch_cuda, P):
     assert max(k for k, c in enumerate(h) if c) <= 10  # reading 10: at most 10 factorizations
     w, _ = P.stemr(dt, et, vectors=False)
     assert sum(P.rqc_histogram()) == 0
+
+
+@pytest.mark.parametrize("case", ["random_3000", "glued_40", "clement_2000"])
+def test_rqc_previous_correction_stop(torch_cuda, P, monkeypatch, case):
+    """DESIGN.md reading 33 (GPU only): the RQC stops at a factorization whose
+    shift was reached by a Rayleigh-quotient step of at most 2^-31 |lambda|.
+    With the rule and without it (MRRR_RQC_PREV_TOL=0: reading 10 alone, as
+    the oracle iterates) the eigenvalues agree to rounding level, both meet the
+    residual / orthogonality contract, and the rule never costs a factorization."""
+    d, e = {"random_3000": lambda: W.random_uniform(3000, 4), "glued_40": lambda: W.glued_wilkinson(40),
+            "clement_2000": lambda: W.clement(2000)}[case]()
+    w1, Z1 = gpu_solve(P, torch_cuda, d, e)
+    h1, st1 = P.rqc_histogram(), P.last_stats()
+    monkeypatch.setenv("MRRR_RQC_PREV_TOL", "0")
+    w0, Z0 = gpu_solve(P, torch_cuda, d, e)
+    h0, st0 = P.rqc_histogram(), P.last_stats()
+    monkeypatch.delenv("MRRR_RQC_PREV_TOL")
+    w2, Z2 = gpu_solve(P, torch_cuda, d, e)  # the default is restored for the tests that follow
+    assert np.array_equal(w1, w2) and np.array_equal(Z1, Z2)
+    n, tn = len(d), tnorm1(d, e)
+    assert np.max(np.abs(w1 - w0)) <= 8 * EPS * tn
+    for w, Z in ((w1, Z1), (w0, Z0)):
+        res, orth = check_accuracy(d, e, w, Z)
+        assert res <= 1 and orth <= 1, (res, orth)
+    assert sum(h1) == sum(h0) == n
+    assert st1["rqc_iters"] <= st0["rqc_iters"]
+    assert max(k for k, c in enumerate(h1) if c) <= max(k for k, c in enumerate(h0) if c)

@@ -1291,8 +1291,9 @@ int solve(Problem &P, int64_t *m_out) {
   // one shift per thread, against 625 warps of chunk 32 with M = 4)
   const int rw_m_root = std::max(1, std::min(4, env_int("MRRR_RW_ROOT_M", 2)));
   // reading 31: tree members stop refining at 2^-early_bits once their
-  // classification is decided (MRRR_EARLY_BITS; 0 = off, refine all to rtol_class)
-  const int early_bits = env_int("MRRR_EARLY_BITS", 10);
+  // classification is decided (MRRR_EARLY_BITS; 0 = off, refine all to rtol_class);
+  // 2^-7 since the RQC stop of reading 33 (sweep: profiles/r02/setG/r2G_early_bits_sweep.txt)
+  const int early_bits = env_int("MRRR_EARLY_BITS", 7);
   // twisted (split) counts in the refinement sweeps (reading 32): 1 = tree
   // levels, 2 = tree and root, 0 = whole stationary sweeps everywhere
   const int split_env = env_int("MRRR_SPLIT", 2);
